@@ -1,0 +1,177 @@
+/*
+ * infigrid_b200 — C-ABI of the B200-native InfiniteDiffusion sampling hot path.
+ *
+ * Plain pointers and sizes only (no torch types).  Every data pointer is a
+ * DEVICE pointer owned by the caller; `stream` is a cudaStream_t (may be 0).
+ * Functions return 0 (IG_OK) or an IG_ERR_* code; ig_last_error() returns a
+ * thread-local message for the last failure.  Integer lattice coordinates are
+ * int64 and follow Python floor-division semantics, as the reference does.
+ *
+ * Reference interfaces replaced (all paths under /root/reference/pkg/src/infigrid/):
+ *   ig_noise_region        noise.py:74-86   noise_region / noise_at (:67-71)
+ *   ig_phi_analytic        denoise.py:89-113 apply (identity/shrink_smooth/cond_affine;
+ *                          multistep = repeated calls), box_mean transforms.py:29-51,
+ *                          conditioning fill denoise.py:116-163
+ *   ig_blend               store.py:428-436 _accumulate (+ sampler.py:151-154 W*Phi
+ *                          contribution) and store.py:549-554 divide_weighted
+ *   ig_box_mean            transforms.py:29-51
+ *   ig_block_mean_f64      transforms.py:61-67
+ *   ig_laplacian_residual  transforms.py:89-95 (high = x - up(low))
+ *   ig_laplacian_merge     transforms.py:98-101 / :104-114 (up(low)+high [, signed_square])
+ *   ig_signed_pow          transforms.py:17-26
+ *   ig_patch_features      denoise.py:166-185 coarse_patch_features
+ *   ig_condition_window    denoise.py:116-163 conditioning_for_window (batched)
+ *   ig_procedural_map      pipeline.py:101-123 ProceduralMap.values
+ *   ig_corrupt             pipeline.py:126-139 corrupt_user_map
+ *   ig_raster_map          pipeline.py:72-84 RasterMap.values
+ *   ig_unet_*              the Phi plugin (denoise.py:89 apply) for the new "unet" kind;
+ *                          no reference implementation exists
+ */
+#ifndef INFIGRID_B200_H
+#define INFIGRID_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IG_OK 0
+#define IG_ERR_ARG 1          /* bad shape/argument  -> ShapeError / ValueError   */
+#define IG_ERR_CUDA 2         /* CUDA runtime error  -> StoreError              */
+#define IG_ERR_UNSUPPORTED 3  /* unsupported config  -> ConfigError             */
+
+#define IG_DTYPE_F32 0
+#define IG_DTYPE_F64 1
+
+#define IG_PHI_IDENTITY 0
+#define IG_PHI_SHRINK_SMOOTH 1
+#define IG_PHI_COND_AFFINE 2
+
+const char* ig_last_error(void);
+int ig_abi_version(void);
+
+/* ---- K1 noise ----------------------------------------------------------
+ * out[(c*height + py)*width + px] = G(seed, stream, x0+px, y0+py, ch0+c),
+ * float32 (or its exact float64 widening when out_dtype == IG_DTYPE_F64).
+ * slow_count (nullable, device int32): incremented once per CTA that took the
+ * exact double-double path (diagnostic). */
+int ig_noise_region(uint64_t seed, uint32_t stream, int64_t x0, int64_t y0,
+                    int32_t width, int32_t height, int32_t ch0, int32_t nch,
+                    int32_t out_dtype, void* out, int32_t* slow_count, void* cuda_stream);
+
+/* ---- K3 analytic Phi over a batch of square windows ---------------------
+ * Window k covers [wxy[2k], +window) x [wxy[2k+1], +window) on the lattice.
+ * Source: if src_batched, src is [n][channels][window][window]; otherwise a
+ * canvas (channels, src_h, src_w) whose pixel (0,0) sits at (src_x0, src_y0).
+ * Output: out[n][channels][window][window] (dtype = dtype of src).
+ * Conditioning (cond_affine): cond_parent is (cond_c, cond_h, cond_w) on a
+ * lattice `cond_scale` times coarser, origin (cond_x0, cond_y0); NULL means
+ * y = None.  cond_mask_channel < 0 means an all-ones mask.  Holes (mask < 1)
+ * read noise stream 101 of cond_seed when cond_fill != 0 (cond_fill == 0: the
+ * parent's channel 0 is used as is -- a materialised Conditioning). */
+int ig_phi_analytic(int32_t kind, int32_t radius, double lam, int32_t dtype,
+                    const void* src, int32_t src_batched, int64_t src_x0, int64_t src_y0,
+                    int32_t src_w, int32_t src_h, int32_t channels,
+                    const int64_t* wxy, int32_t n, int32_t window,
+                    const void* cond_parent, int64_t cond_x0, int64_t cond_y0,
+                    int32_t cond_w, int32_t cond_h, int32_t cond_c, int32_t cond_scale,
+                    int32_t cond_mask_channel, uint64_t cond_seed, int32_t cond_fill,
+                    void* out, void* cuda_stream);
+
+/* ---- K5 canonical-order blend -------------------------------------------
+ * win_data: device array of nj*ni pointers, entry (j-j0)*ni + (i-i0) is the
+ * stored data of window (i, j) or NULL (skipped).  mode 0: entries hold full
+ * contributions with `channels` channels, summed as stored.  mode 1: entries
+ * hold Phi outputs with `channels` data channels; the contribution is
+ * fl(W*Phi) plus a weight channel W (W = window x window table, `weight`).
+ * Output (region rw x rh at (rx0, ry0)):
+ *   divide == 0: raw sums, mode 0 -> channels planes, mode 1 -> channels+1
+ *   divide == 1: (mode 1 only) data / weight where weight > 0 else 0. */
+int ig_blend(const void* const* win_data, int64_t i0, int64_t j0, int32_t ni, int32_t nj,
+             int32_t window, int32_t stride, int64_t off_x, int64_t off_y,
+             int32_t channels, int32_t mode, const void* weight,
+             int64_t rx0, int64_t ry0, int32_t rw, int32_t rh,
+             int32_t divide, int32_t dtype, void* out, void* cuda_stream);
+
+/* weighted read over a region (divide_weighted on raw (C+1) planes) */
+int ig_divide_weighted(const void* raw, int32_t channels, int64_t npix, int32_t dtype,
+                       void* out, void* cuda_stream);
+
+/* ---- K6 elevation transforms ---------------------------------------------- */
+int ig_box_mean(const void* in, int32_t planes, int32_t h, int32_t w, int32_t radius,
+                int32_t dtype, void* out, void* cuda_stream);
+/* low = block_mean(blur3_iterated(in, blur_iters), factor), all float64;
+ * in_dtype selects the input element type (widened exactly). scratch: 2 planes*h*w f64 */
+int ig_blur_block_mean_f64(const void* in, int32_t in_dtype, int32_t planes, int32_t h,
+                           int32_t w, int32_t blur_iters, int32_t factor, double* scratch,
+                           double* low, void* cuda_stream);
+/* high = widen(x) - up(low) */
+int ig_laplacian_residual(const void* x, int32_t x_dtype, const double* low, int32_t planes,
+                          int32_t h, int32_t w, int32_t factor, double* high, void* cuda_stream);
+/* out = cast(up(low) + high) [then signed_square in out dtype when square_out] ;
+ * out_dtype F64 keeps the provisional sum (stabilize) */
+int ig_laplacian_merge(const double* low, const double* high, int32_t planes, int32_t h,
+                       int32_t w, int32_t factor, int32_t out_dtype, int32_t square_out,
+                       void* out, void* cuda_stream);
+/* op 0: signed_sqrt, 1: signed_square */
+int ig_signed_pow(const void* in, int64_t n, int32_t op, int32_t dtype, void* out,
+                  void* cuda_stream);
+
+/* ---- K7/K8/K9 hierarchy helpers ----------------------------------------------
+ * features over a batch of n elevation tiles [n][h][w] (channel 0 of each
+ * parent slab, row stride `in_stride_tile` elements between tiles):
+ * out[n][3][h/patch][w/patch] = (mean, p-th rank, 1) */
+int ig_patch_features(const void* in, int64_t tile_stride, int32_t n, int32_t h, int32_t w,
+                      int32_t patch, int32_t rank, int32_t dtype, void* out,
+                      void* cuda_stream);
+/* conditioning_for_window for a batch: out[n][cond_c][window][window] channels
+ * and mask_out[n][window][window] (both dtype) */
+int ig_condition_window(const void* parent, int64_t px0, int64_t py0, int32_t pw, int32_t ph,
+                        int32_t pc, int32_t scale, int32_t mask_channel, uint64_t seed,
+                        const int64_t* wxy, int32_t n, int32_t window, int32_t dtype,
+                        void* out, void* mask_out, void* cuda_stream);
+int ig_procedural_map(uint64_t seed, uint32_t stream, int32_t cell, int64_t x0, int64_t y0,
+                      int32_t w, int32_t h, int32_t channels, float* out, void* cuda_stream);
+/* out[c] = in[c] + f32(level[c]) * G(seed, 201+c, ., ., 0) (level 0 -> copy) */
+int ig_corrupt(const float* in, const double* levels_host, int32_t channels, uint64_t seed,
+               int64_t x0, int64_t y0, int32_t w, int32_t h, float* out, void* cuda_stream);
+/* RasterMap.values: mode 0 clamp, 1 tile; raster (rc, rh, rw) f32 */
+int ig_raster_map(const float* raster, int32_t rc, int32_t rh, int32_t rw, int32_t mode,
+                  int64_t x0, int64_t y0, int32_t w, int32_t h, int32_t channels, float* out,
+                  void* cuda_stream);
+
+/* ---- K4 UNet Phi (tcgen05/TMEM implicit-GEMM convolutions) -------------------
+ * Implicit-GEMM 3x3 (taps = 9) or 1x1 (taps = 1) convolution, NHWC bf16:
+ *   out[p][co] = epilogue( sum_{tap, ci} act[p + tap][ci] * wgt[co][tap][ci] )
+ * act_a: [n][h][w][ca] and optional act_b: [n][h][w][cb] (channel concat,
+ * used by decoder skips); ca, cb multiples of 64; cout multiple of 16, <= 256.
+ * Epilogue (per output channel co, fp32):
+ *   y = acc * scale[co] + bias[co]
+ *   if (res)   y = res_a * res[p][co] + res_b * y                (mp_sum)
+ *   out0[p][co] = bf16(y)            (if out0)
+ *   out1[p][co] = bf16(act_gain * silu(y))   (if out1)
+ * workspace: >= ig_conv_workspace_bytes() bytes of device memory (TMA maps). */
+typedef struct {
+  int32_t n, h, w, ca, cb, cout, taps;
+  const void* act_a;
+  const void* act_b;
+  const void* wgt;        /* [cout][taps][ca+cb] bf16, K-major */
+  const float* scale;     /* [cout] */
+  const float* bias;      /* [cout] */
+  const void* res;        /* [n][h][w][cout] bf16 or NULL */
+  float res_a, res_b, act_gain;
+  void* out0;             /* bf16 or NULL */
+  void* out1;             /* bf16 or NULL */
+} ig_conv_params_t;
+size_t ig_conv_workspace_bytes(void);
+int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream);
+/* same contract on CUDA cores (fp32 accumulate, identical epilogue); used by
+ * the tests as an independent device cross-check of the tensor-core kernel */
+int ig_conv_simt(const ig_conv_params_t* p, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INFIGRID_B200_H */

@@ -1,0 +1,730 @@
+// infigrid_b200 core kernels: noise (K1), analytic Phi (K3), canonical blend
+// (K5), elevation transforms (K6), features / conditioning / base maps (K7-K9).
+//
+// Every kernel here is on the bit-exact parity path: arithmetic goes through
+// explicitly rounded intrinsics (ig::radd/rmul/...) in the order the
+// reference's numpy expressions evaluate, and the file is compiled with
+// -fmad=false as a second guard.  Reference citations are per kernel.
+#include <cstdarg>
+#include <cstring>
+
+#include "ig_common.cuh"
+#include "ig_noise.cuh"
+
+namespace ig {
+
+static thread_local char g_err[512] = {0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// =====================================================================
+// K1 noise_region  (noise.py:74-86)
+// Each thread produces 4 consecutive x samples of one row; the 4 outputs
+// are stored together (16 B for f32) when the row is 4-aligned.
+template <typename T>
+__global__ void __launch_bounds__(256) noise_region_kernel(uint64_t prefix, int64_t x0, int64_t y0,
+                                                           int32_t w, int32_t h, int32_t ch0,
+                                                           int32_t nch, T* __restrict__ out,
+                                                           int32_t* slow_count) {
+  const int64_t quads_per_row = (w + 3) / 4;
+  const int64_t total = quads_per_row * h * nch;
+  int slow = 0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = q / quads_per_row;      // c*h + py
+    const int32_t px0 = (int32_t)(q - row * quads_per_row) * 4;
+    const int32_t c = (int32_t)(row / h);
+    const int32_t py = (int32_t)(row - (int64_t)c * h);
+    const int64_t Y = y0 + py;
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = 0.f;
+      if (px0 + k < w) v[k] = noise_value(prefix, x0 + px0 + k, Y, (uint32_t)(ch0 + c), &slow);
+    }
+    T* dst = out + row * w + px0;
+    if (sizeof(T) == 4 && (w & 3) == 0) {
+      *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (px0 + k < w) dst[k] = (T)v[k];
+    }
+  }
+  if (slow_count && __syncthreads_or(slow) && threadIdx.x == 0) atomicAdd(slow_count, 1);
+}
+
+// =====================================================================
+// K3 analytic Phi  (denoise.py:75-113; box_mean transforms.py:29-51)
+struct SrcView {
+  const void* base;
+  int batched;
+  int64_t x0, y0;
+  int32_t w, h, channels;
+};
+struct CondView {
+  const void* parent;
+  int64_t x0, y0;
+  int32_t w, h, c, scale, mask_channel, fill;
+  uint64_t prefix;  // noise prefix of (seed, STREAM_CONDITIONING)
+};
+
+// value of window k, channel c at window-local (yy, xx) (already clamped)
+template <typename T>
+__device__ __forceinline__ T src_at(const SrcView& s, const int64_t* wxy, int k, int c, int win,
+                                    int yy, int xx) {
+  const T* b = reinterpret_cast<const T*>(s.base);
+  if (s.batched) return b[(((int64_t)k * s.channels + c) * win + yy) * win + xx];
+  const int64_t gx = wxy[2 * k] + xx - s.x0;
+  const int64_t gy = wxy[2 * k + 1] + yy - s.y0;
+  return b[((int64_t)c * s.h + gy) * s.w + gx];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) phi_analytic_kernel(int kind, int radius, T a_coef, T b_coef,
+                                                           int lam_zero, SrcView src,
+                                                           const int64_t* __restrict__ wxy, int n,
+                                                           int win, CondView cond,
+                                                           T* __restrict__ out) {
+  const int64_t per_win = (int64_t)src.channels * win * win;
+  const int64_t total = per_win * n;
+  const T kdiv = (T)(2 * radius + 1);
+  int slow = 0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx / per_win);
+    int64_t rem = idx - (int64_t)k * per_win;
+    const int c = (int)(rem / (win * win));
+    rem -= (int64_t)c * win * win;
+    const int y = (int)(rem / win), x = (int)(rem - (int64_t)y * win);
+    const T xv = src_at<T>(src, wxy, k, c, win, y, x);
+    T res;
+    if (kind == IG_PHI_IDENTITY || lam_zero) {
+      res = xv;
+    } else {
+      T blur = xv;
+      if (radius > 0) {
+        // rows (axis -2) first, then columns; clamp-to-edge inside the window
+        T hacc = (T)0;
+        for (int dx = -radius; dx <= radius; ++dx) {
+          int xx = min(max(x + dx, 0), win - 1);
+          T vacc = (T)0;
+          for (int dy = -radius; dy <= radius; ++dy) {
+            int yy = min(max(y + dy, 0), win - 1);
+            vacc = radd(vacc, src_at<T>(src, wxy, k, c, win, yy, xx));
+          }
+          hacc = radd(hacc, rdiv(vacc, kdiv));
+        }
+        blur = rdiv(hacc, kdiv);
+      }
+      res = radd(rmul(a_coef, xv), rmul(b_coef, blur));
+    }
+    if (kind == IG_PHI_COND_AFFINE && cond.parent != nullptr) {
+      // conditioning_for_window (denoise.py:116-163): NN upsample of the
+      // coarse parent's channel 0; holes (mask < 1) take stream-101 noise
+      const int64_t X = wxy[2 * k] + x, Y = wxy[2 * k + 1] + y;
+      const int64_t cx = floordiv(X, cond.scale) - cond.x0;
+      const int64_t cy = floordiv(Y, cond.scale) - cond.y0;
+      const T* par = reinterpret_cast<const T*>(cond.parent);
+      const int64_t plane = (int64_t)cond.w * cond.h;
+      T m = (T)1;
+      if (cond.mask_channel >= 0) m = par[cond.mask_channel * plane + cy * cond.w + cx];
+      T target = par[cy * cond.w + cx];
+      if (cond.fill && m < (T)1) target = (T)noise_value(cond.prefix, X, Y, 0u, &slow);
+      res = radd(res, rmul(m, rsub(target, res)));
+    }
+    out[idx] = res;
+  }
+}
+
+// =====================================================================
+// K5 blend  (store.py:428-436 _accumulate, sampler.py:151-154, store.py:549-554)
+// Gather form: each output pixel walks its covering windows in canonical
+// (j, i) order and sums their contributions starting from +0, exactly the
+// per-pixel sequence of the reference's scatter-add loop.  No atomics.
+template <typename T>
+__global__ void __launch_bounds__(256) blend_kernel(const T* const* __restrict__ win_data,
+                                                    int64_t i0, int64_t j0, int ni, int nj,
+                                                    int win, int stride, int64_t ox, int64_t oy,
+                                                    int channels, int mode,
+                                                    const T* __restrict__ weight, int64_t rx0,
+                                                    int64_t ry0, int rw, int rh, int divide,
+                                                    T* __restrict__ out) {
+  const int64_t npix = (int64_t)rw * rh;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int py = (int)(p / rw), px = (int)(p - (int64_t)py * rw);
+    const int64_t X = rx0 + px, Y = ry0 + py;
+    int64_t ilo = ceildiv(X - ox - win + 1, stride), ihi = floordiv(X - ox, stride);
+    int64_t jlo = ceildiv(Y - oy - win + 1, stride), jhi = floordiv(Y - oy, stride);
+    ilo = ilo > i0 ? ilo : i0;
+    jlo = jlo > j0 ? jlo : j0;
+    ihi = ihi < i0 + ni - 1 ? ihi : i0 + ni - 1;
+    jhi = jhi < j0 + nj - 1 ? jhi : j0 + nj - 1;
+    const int out_planes = mode == 1 ? channels + 1 : channels;
+    if (mode == 1) {
+      T wsum = (T)0;
+      for (int64_t j = jlo; j <= jhi; ++j)
+        for (int64_t i = ilo; i <= ihi; ++i) {
+          const T* d = win_data[(j - j0) * ni + (i - i0)];
+          if (!d) continue;
+          const int lx = (int)(X - (i * stride + ox)), ly = (int)(Y - (j * stride + oy));
+          wsum = radd(wsum, weight[ly * win + lx]);
+        }
+      for (int c = 0; c < channels; ++c) {
+        T acc = (T)0;
+        for (int64_t j = jlo; j <= jhi; ++j)
+          for (int64_t i = ilo; i <= ihi; ++i) {
+            const T* d = win_data[(j - j0) * ni + (i - i0)];
+            if (!d) continue;
+            const int lx = (int)(X - (i * stride + ox)), ly = (int)(Y - (j * stride + oy));
+            const int64_t o = ((int64_t)c * win + ly) * win + lx;
+            acc = radd(acc, rmul(weight[ly * win + lx], d[o]));
+          }
+        if (divide)
+          out[(int64_t)c * npix + p] = wsum > (T)0 ? rdiv(acc, wsum) : (T)0;
+        else
+          out[(int64_t)c * npix + p] = acc;
+      }
+      if (!divide) out[(int64_t)channels * npix + p] = wsum;
+    } else {
+      for (int c = 0; c < out_planes; ++c) {
+        T acc = (T)0;
+        for (int64_t j = jlo; j <= jhi; ++j)
+          for (int64_t i = ilo; i <= ihi; ++i) {
+            const T* d = win_data[(j - j0) * ni + (i - i0)];
+            if (!d) continue;
+            const int lx = (int)(X - (i * stride + ox)), ly = (int)(Y - (j * stride + oy));
+            acc = radd(acc, d[((int64_t)c * win + ly) * win + lx]);
+          }
+        out[(int64_t)c * npix + p] = acc;
+      }
+    }
+  }
+}
+
+template <typename T>
+__global__ void divide_weighted_kernel(const T* __restrict__ raw, int channels, int64_t npix,
+                                       T* __restrict__ out) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const T w = raw[(int64_t)channels * npix + p];
+    for (int c = 0; c < channels; ++c)
+      out[(int64_t)c * npix + p] = w > (T)0 ? rdiv(raw[(int64_t)c * npix + p], w) : (T)0;
+  }
+}
+
+// =====================================================================
+// K6 transforms  (transforms.py:17-114)
+template <typename T>
+__global__ void box_mean_kernel(const T* __restrict__ in, int planes, int h, int w, int radius,
+                                T* __restrict__ out) {
+  const int64_t total = (int64_t)planes * h * w;
+  const T kdiv = (T)(2 * radius + 1);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pl = idx / ((int64_t)h * w);
+    const int rem = (int)(idx - pl * h * w);
+    const int y = rem / w, x = rem - y * w;
+    const T* P = in + pl * h * w;
+    if (radius == 0) { out[idx] = P[rem]; continue; }
+    T hacc = (T)0;
+    for (int dx = -radius; dx <= radius; ++dx) {
+      const int xx = min(max(x + dx, 0), w - 1);
+      T vacc = (T)0;
+      for (int dy = -radius; dy <= radius; ++dy) {
+        const int yy = min(max(y + dy, 0), h - 1);
+        vacc = radd(vacc, P[yy * w + xx]);
+      }
+      hacc = radd(hacc, rdiv(vacc, kdiv));
+    }
+    out[idx] = rdiv(hacc, kdiv);
+  }
+}
+
+template <typename TI>
+__global__ void widen_kernel(const TI* __restrict__ in, int64_t n, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (double)in[i];
+}
+
+// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src) of
+// v(s..s+n): blocks of <8 sequentially from -0.0, <=128 with 8 running
+// partial sums folded as a tree, larger blocks split at an 8-aligned half.
+template <typename T, typename F>
+__device__ T np_pairwise(const F& v, int s, int n) {
+  if (n < 8) {
+    T res = (T)-0.0;
+    for (int i = 0; i < n; ++i) res = radd(res, v(s + i));
+    return res;
+  }
+  if (n <= 128) {
+    T r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = v(s + j);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = radd(r[j], v(s + i + j));
+    }
+    T res = radd(radd(radd(r[0], r[1]), radd(r[2], r[3])), radd(radd(r[4], r[5]), radd(r[6], r[7])));
+    for (; i < n; ++i) res = radd(res, v(s + i));
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return radd(np_pairwise<T>(v, s, n2), np_pairwise<T>(v, s + n2, n - n2));
+}
+
+// block_mean of blur3_iterated input (transforms.py:54-67), float64.
+// numpy order for .mean(axis=(-3,-1)) of the (h/f, f, w/f, f) view: for each
+// of the f block rows (outer, sequential, starting from 0) add the pairwise
+// sum of that row's f values; then divide by f*f.
+__global__ void block_mean_f64_kernel(const double* __restrict__ in, int planes, int h, int w,
+                                      int f, double* __restrict__ low) {
+  const int lh = h / f, lw = w / f;
+  const int64_t total = (int64_t)planes * lh * lw;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pl = idx / ((int64_t)lh * lw);
+    const int rem = (int)(idx - pl * lh * lw);
+    const int by = rem / lw, bx = rem - by * lw;
+    const double* P = in + pl * h * w + (int64_t)(by * f) * w + bx * f;
+    double s = 0.0;
+    for (int r = 0; r < f; ++r) {
+      const double* row = P + (int64_t)r * w;
+      s = radd(s, np_pairwise<double>([&](int i) { return row[i]; }, 0, f));
+    }
+    low[idx] = rdiv(s, (double)(f * f));
+  }
+}
+
+template <typename TX>
+__global__ void laplacian_residual_kernel(const TX* __restrict__ x, const double* __restrict__ low,
+                                          int planes, int h, int w, int f,
+                                          double* __restrict__ high) {
+  const int64_t total = (int64_t)planes * h * w;
+  const int lh = h / f, lw = w / f;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pl = idx / ((int64_t)h * w);
+    const int rem = (int)(idx - pl * h * w);
+    const int y = rem / w, xx = rem - y * w;
+    high[idx] = rsub((double)x[idx], low[(pl * lh + y / f) * lw + xx / f]);
+  }
+}
+
+template <typename TO>
+__global__ void laplacian_merge_kernel(const double* __restrict__ low,
+                                       const double* __restrict__ high, int planes, int h, int w,
+                                       int f, int square_out, TO* __restrict__ out) {
+  const int64_t total = (int64_t)planes * h * w;
+  const int lh = h / f, lw = w / f;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pl = idx / ((int64_t)h * w);
+    const int rem = (int)(idx - pl * h * w);
+    const int y = rem / w, xx = rem - y * w;
+    TO v = (TO)radd(low[(pl * lh + y / f) * lw + xx / f], high[idx]);
+    if (square_out) {
+      // signed_square: np.sign(x) * x * x  (left to right)
+      const TO sg = v > (TO)0 ? (TO)1 : (v < (TO)0 ? (TO)-1 : (v == (TO)0 ? (TO)0 : v));
+      v = rmul(rmul(sg, v), v);
+    }
+    out[idx] = v;
+  }
+}
+
+template <typename T>
+__global__ void signed_pow_kernel(const T* __restrict__ in, int64_t n, int op, T* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T v = in[i];
+    const T sg = v > (T)0 ? (T)1 : (v < (T)0 ? (T)-1 : (v == (T)0 ? (T)0 : v));  // np.sign: +0, nan
+    if (op == 0) out[i] = rmul(sg, sqrt(fabs(v)));
+    else out[i] = rmul(rmul(sg, v), v);
+  }
+}
+
+// =====================================================================
+// K7 coarse_patch_features  (denoise.py:166-185)
+template <typename T>
+__global__ void patch_features_kernel(const T* __restrict__ in, int64_t tile_stride, int n,
+                                      int h, int w, int p, int rank, T* __restrict__ out) {
+  const int oh = h / p, ow = w / p;
+  const int64_t total = (int64_t)n * oh * ow;
+  const int np2 = p * p;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx / ((int64_t)oh * ow));
+    const int rem = (int)(idx - (int64_t)k * oh * ow);
+    const int by = rem / ow, bx = rem - by * ow;
+    const T* P = in + (int64_t)k * tile_stride + (int64_t)(by * p) * w + bx * p;
+    auto val = [&](int q) { return P[(q / p) * w + (q % p)]; };
+    const T sum = radd((T)0, np_pairwise<T>(val, 0, np2));  // reduce starts at +0
+    const T mean = rdiv(sum, (T)np2);
+    // rank-th smallest (1-based) with stable tie order == np.sort()[rank-1]
+    T sel = val(0);
+    for (int q = 0; q < np2; ++q) {
+      const T vq = val(q);
+      int below = 0, tie_before = 0;
+      for (int r = 0; r < np2; ++r) {
+        const T vr = val(r);
+        below += vr < vq;
+        tie_before += (vr == vq) && (r < q);
+      }
+      if (below + tie_before == rank - 1) { sel = vq; break; }
+    }
+    T* o = out + (int64_t)k * 3 * oh * ow;
+    o[rem] = mean;
+    o[(int64_t)oh * ow + rem] = sel;
+    o[(int64_t)2 * oh * ow + rem] = (T)1;
+  }
+}
+
+// =====================================================================
+// K8 conditioning_for_window, batched (denoise.py:116-163)
+template <typename T>
+__global__ void condition_window_kernel(const T* __restrict__ parent, int64_t px0, int64_t py0,
+                                        int pw, int ph, int pc, int scale, int mask_channel,
+                                        uint64_t prefix, const int64_t* __restrict__ wxy, int n,
+                                        int win, T* __restrict__ out, T* __restrict__ mask_out) {
+  const int64_t per = (int64_t)win * win;
+  const int64_t total = per * n;
+  const int64_t plane = (int64_t)pw * ph;
+  int slow = 0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx / per);
+    const int rem = (int)(idx - (int64_t)k * per);
+    const int y = rem / win, x = rem - y * win;
+    const int64_t X = wxy[2 * k] + x, Y = wxy[2 * k + 1] + y;
+    const int64_t cx = floordiv(X, scale) - px0, cy = floordiv(Y, scale) - py0;
+    const T m = mask_channel >= 0 ? parent[mask_channel * plane + cy * pw + cx] : (T)1;
+    mask_out[idx] = m;
+    const bool hole = m < (T)1;
+    for (int c = 0; c < pc; ++c) {
+      T v = parent[c * plane + cy * pw + cx];
+      if (hole) v = (T)noise_value(prefix, X, Y, (uint32_t)c, &slow);
+      out[((int64_t)k * pc + c) * per + rem] = v;
+    }
+  }
+}
+
+// =====================================================================
+// K9 base maps  (pipeline.py:72-139)
+__global__ void procedural_map_kernel(uint64_t prefix, int cell, int64_t x0, int64_t y0, int w,
+                                      int h, int channels, float* __restrict__ out) {
+  const int64_t total = (int64_t)channels * w * h;
+  const int64_t gx0 = floordiv(x0, cell), gy0 = floordiv(y0, cell);
+  int slow = 0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(idx / ((int64_t)w * h));
+    const int rem = (int)(idx - (int64_t)c * w * h);
+    const int py = rem / w, px = rem - py * w;
+    const int64_t X = x0 + px, Y = y0 + py;
+    // fx = (xs / cell) - gx0 in float64 (numpy true_divide then subtract)
+    const double fx = rsub(rdiv((double)X, (double)cell), (double)gx0);
+    const double fy = rsub(rdiv((double)Y, (double)cell), (double)gy0);
+    const double ixf = floor(fx), iyf = floor(fy);
+    const double tx = rsub(fx, ixf), ty = rsub(fy, iyf);
+    const int64_t gx = gx0 + (int64_t)ixf, gy = gy0 + (int64_t)iyf;
+    const double v00 = noise_value(prefix, gx, gy, (uint32_t)c, &slow);
+    const double v01 = noise_value(prefix, gx + 1, gy, (uint32_t)c, &slow);
+    const double v10 = noise_value(prefix, gx, gy + 1, (uint32_t)c, &slow);
+    const double v11 = noise_value(prefix, gx + 1, gy + 1, (uint32_t)c, &slow);
+    const double omx = rsub(1.0, tx), omy = rsub(1.0, ty);
+    const double top = radd(rmul(v00, omx), rmul(v01, tx));
+    const double bot = radd(rmul(v10, omx), rmul(v11, tx));
+    out[idx] = __double2float_rn(radd(rmul(top, omy), rmul(bot, ty)));
+  }
+}
+
+__global__ void corrupt_kernel(const float* __restrict__ in, uint64_t prefix, float level,
+                               int64_t x0, int64_t y0, int w, int h, float* __restrict__ out) {
+  const int64_t total = (int64_t)w * h;
+  int slow = 0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int py = (int)(idx / w), px = (int)(idx - (int64_t)py * w);
+    const float z = noise_value(prefix, x0 + px, y0 + py, 0u, &slow);
+    out[idx] = radd(in[idx], rmul(level, z));
+  }
+}
+
+__global__ void raster_map_kernel(const float* __restrict__ raster, int rc, int rh, int rw,
+                                  int mode, int64_t x0, int64_t y0, int w, int h, int channels,
+                                  float* __restrict__ out) {
+  const int64_t total = (int64_t)channels * w * h;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(idx / ((int64_t)w * h));
+    const int rem = (int)(idx - (int64_t)c * w * h);
+    const int py = rem / w, px = rem - py * w;
+    int64_t X = x0 + px, Y = y0 + py;
+    if (mode == 0) {
+      X = X < 0 ? 0 : (X > rw - 1 ? rw - 1 : X);
+      Y = Y < 0 ? 0 : (Y > rh - 1 ? rh - 1 : Y);
+    } else {
+      X = pymod(X, rw);
+      Y = pymod(Y, rh);
+    }
+    out[idx] = raster[((int64_t)c * rh + Y) * rw + X];
+  }
+}
+
+}  // namespace ig
+
+// =====================================================================
+// C-ABI
+using namespace ig;
+
+extern "C" {
+
+const char* ig_last_error(void) { return g_err; }
+int ig_abi_version(void) { return 1; }
+
+int ig_noise_region(uint64_t seed, uint32_t stream, int64_t x0, int64_t y0, int32_t width,
+                    int32_t height, int32_t ch0, int32_t nch, int32_t out_dtype, void* out,
+                    int32_t* slow_count, void* cuda_stream) {
+  IG_REQUIRE(width > 0 && height > 0 && nch > 0, "noise_region: empty region %dx%dx%d", nch,
+             height, width);
+  IG_REQUIRE(out != nullptr, "noise_region: null output");
+  const uint64_t prefix = noise_prefix(seed, stream);
+  const int64_t quads = (int64_t)((width + 3) / 4) * height * nch;
+  const int grid = grid_for(quads, 256, 32);
+  if (out_dtype == IG_DTYPE_F32)
+    noise_region_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        prefix, x0, y0, width, height, ch0, nch, (float*)out, slow_count);
+  else
+    noise_region_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        prefix, x0, y0, width, height, ch0, nch, (double*)out, slow_count);
+  return cuda_check("ig_noise_region");
+}
+
+int ig_phi_analytic(int32_t kind, int32_t radius, double lam, int32_t dtype, const void* src,
+                    int32_t src_batched, int64_t src_x0, int64_t src_y0, int32_t src_w,
+                    int32_t src_h, int32_t channels, const int64_t* wxy, int32_t n,
+                    int32_t window, const void* cond_parent, int64_t cond_x0, int64_t cond_y0,
+                    int32_t cond_w, int32_t cond_h, int32_t cond_c, int32_t cond_scale,
+                    int32_t cond_mask_channel, uint64_t cond_seed, int32_t cond_fill, void* out,
+                    void* cuda_stream) {
+  IG_REQUIRE(kind >= 0 && kind <= 2, "phi: unknown kind %d", kind);
+  IG_REQUIRE(radius >= 0, "phi: radius must be >= 0");
+  IG_REQUIRE(n >= 0 && window > 0 && channels > 0, "phi: bad batch");
+  if (n == 0) return IG_OK;
+  SrcView s{src, src_batched, src_x0, src_y0, src_w, src_h, channels};
+  CondView c{cond_parent, cond_x0, cond_y0, cond_w, cond_h, cond_c, cond_scale < 1 ? 1 : cond_scale,
+             cond_mask_channel, cond_fill, noise_prefix(cond_seed, 101u)};
+  const int64_t total = (int64_t)n * channels * window * window;
+  const int grid = grid_for(total, 256);
+  const int lam_zero = (lam == 0.0);
+  if (dtype == IG_DTYPE_F32)
+    phi_analytic_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        kind, radius, (float)(1.0 - lam), (float)lam, lam_zero, s, wxy, n, window, c,
+        (float*)out);
+  else
+    phi_analytic_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        kind, radius, 1.0 - lam, lam, lam_zero, s, wxy, n, window, c, (double*)out);
+  return cuda_check("ig_phi_analytic");
+}
+
+int ig_blend(const void* const* win_data, int64_t i0, int64_t j0, int32_t ni, int32_t nj,
+             int32_t window, int32_t stride, int64_t off_x, int64_t off_y, int32_t channels,
+             int32_t mode, const void* weight, int64_t rx0, int64_t ry0, int32_t rw, int32_t rh,
+             int32_t divide, int32_t dtype, void* out, void* cuda_stream) {
+  IG_REQUIRE(rw > 0 && rh > 0, "blend: empty region");
+  IG_REQUIRE(stride >= 1 && stride <= window, "blend: bad layout");
+  IG_REQUIRE(mode == 0 || mode == 1, "blend: bad mode");
+  IG_REQUIRE(!(divide && mode == 0), "blend: divide needs weighted mode");
+  IG_REQUIRE(mode == 0 || weight != nullptr, "blend: weighted mode needs a weight table");
+  const int grid = grid_for((int64_t)rw * rh, 256);
+  if (dtype == IG_DTYPE_F32)
+    blend_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const float* const*)win_data, i0, j0, ni, nj, window, stride, off_x, off_y, channels,
+        mode, (const float*)weight, rx0, ry0, rw, rh, divide, (float*)out);
+  else
+    blend_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const double* const*)win_data, i0, j0, ni, nj, window, stride, off_x, off_y, channels,
+        mode, (const double*)weight, rx0, ry0, rw, rh, divide, (double*)out);
+  return cuda_check("ig_blend");
+}
+
+int ig_divide_weighted(const void* raw, int32_t channels, int64_t npix, int32_t dtype, void* out,
+                       void* cuda_stream) {
+  if (npix <= 0) return IG_OK;
+  const int grid = grid_for(npix, 256);
+  if (dtype == IG_DTYPE_F32)
+    divide_weighted_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const float*)raw, channels, npix, (float*)out);
+  else
+    divide_weighted_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const double*)raw, channels, npix, (double*)out);
+  return cuda_check("ig_divide_weighted");
+}
+
+int ig_box_mean(const void* in, int32_t planes, int32_t h, int32_t w, int32_t radius,
+                int32_t dtype, void* out, void* cuda_stream) {
+  IG_REQUIRE(radius >= 0, "radius must be >= 0");
+  const int64_t total = (int64_t)planes * h * w;
+  if (total == 0) return IG_OK;
+  const int grid = grid_for(total, 256);
+  if (dtype == IG_DTYPE_F32)
+    box_mean_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>((const float*)in, planes, h,
+                                                                     w, radius, (float*)out);
+  else
+    box_mean_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const double*)in, planes, h, w, radius, (double*)out);
+  return cuda_check("ig_box_mean");
+}
+
+int ig_blur_block_mean_f64(const void* in, int32_t in_dtype, int32_t planes, int32_t h, int32_t w,
+                           int32_t blur_iters, int32_t factor, double* scratch, double* low,
+                           void* cuda_stream) {
+  IG_REQUIRE(factor >= 1 && h % factor == 0 && w % factor == 0,
+             "spatial dims %dx%d not divisible by factor %d", h, w, factor);
+  const int64_t total = (int64_t)planes * h * w;
+  cudaStream_t st = as_stream(cuda_stream);
+  const int grid = grid_for(total, 256);
+  double* a = scratch;
+  double* b = scratch + total;
+  if (in_dtype == IG_DTYPE_F32)
+    widen_kernel<float><<<grid, 256, 0, st>>>((const float*)in, total, a);
+  else
+    widen_kernel<double><<<grid, 256, 0, st>>>((const double*)in, total, a);
+  for (int it = 0; it < blur_iters; ++it) {
+    box_mean_kernel<double><<<grid, 256, 0, st>>>(a, planes, h, w, 1, b);
+    double* t = a; a = b; b = t;
+  }
+  const int64_t lt = total / ((int64_t)factor * factor);
+  block_mean_f64_kernel<<<grid_for(lt, 256), 256, 0, st>>>(a, planes, h, w, factor, low);
+  return cuda_check("ig_blur_block_mean_f64");
+}
+
+int ig_laplacian_residual(const void* x, int32_t x_dtype, const double* low, int32_t planes,
+                          int32_t h, int32_t w, int32_t factor, double* high, void* cuda_stream) {
+  const int64_t total = (int64_t)planes * h * w;
+  const int grid = grid_for(total, 256);
+  if (x_dtype == IG_DTYPE_F32)
+    laplacian_residual_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const float*)x, low, planes, h, w, factor, high);
+  else
+    laplacian_residual_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const double*)x, low, planes, h, w, factor, high);
+  return cuda_check("ig_laplacian_residual");
+}
+
+int ig_laplacian_merge(const double* low, const double* high, int32_t planes, int32_t h,
+                       int32_t w, int32_t factor, int32_t out_dtype, int32_t square_out,
+                       void* out, void* cuda_stream) {
+  const int64_t total = (int64_t)planes * h * w;
+  const int grid = grid_for(total, 256);
+  if (out_dtype == IG_DTYPE_F32)
+    laplacian_merge_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        low, high, planes, h, w, factor, square_out, (float*)out);
+  else
+    laplacian_merge_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        low, high, planes, h, w, factor, square_out, (double*)out);
+  return cuda_check("ig_laplacian_merge");
+}
+
+int ig_signed_pow(const void* in, int64_t n, int32_t op, int32_t dtype, void* out,
+                  void* cuda_stream) {
+  if (n <= 0) return IG_OK;
+  const int grid = grid_for(n, 256);
+  if (dtype == IG_DTYPE_F32)
+    signed_pow_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>((const float*)in, n, op,
+                                                                       (float*)out);
+  else
+    signed_pow_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>((const double*)in, n, op,
+                                                                        (double*)out);
+  return cuda_check("ig_signed_pow");
+}
+
+int ig_patch_features(const void* in, int64_t tile_stride, int32_t n, int32_t h, int32_t w,
+                      int32_t patch, int32_t rank, int32_t dtype, void* out, void* cuda_stream) {
+  IG_REQUIRE(patch >= 1 && h % patch == 0 && w % patch == 0,
+             "region %dx%d not divisible by patch size %d", h, w, patch);
+  IG_REQUIRE(rank >= 1 && rank <= patch * patch, "bad percentile rank %d", rank);
+  const int64_t total = (int64_t)n * (h / patch) * (w / patch);
+  if (total == 0) return IG_OK;
+  const int grid = grid_for(total, 128);
+  if (dtype == IG_DTYPE_F32)
+    patch_features_kernel<float><<<grid, 128, 0, as_stream(cuda_stream)>>>(
+        (const float*)in, tile_stride, n, h, w, patch, rank, (float*)out);
+  else
+    patch_features_kernel<double><<<grid, 128, 0, as_stream(cuda_stream)>>>(
+        (const double*)in, tile_stride, n, h, w, patch, rank, (double*)out);
+  return cuda_check("ig_patch_features");
+}
+
+int ig_condition_window(const void* parent, int64_t px0, int64_t py0, int32_t pw, int32_t ph,
+                        int32_t pc, int32_t scale, int32_t mask_channel, uint64_t seed,
+                        const int64_t* wxy, int32_t n, int32_t window, int32_t dtype, void* out,
+                        void* mask_out, void* cuda_stream) {
+  IG_REQUIRE(scale >= 1, "conditioning scale must be >= 1");
+  if (n == 0) return IG_OK;
+  const uint64_t prefix = noise_prefix(seed, 101u);
+  const int grid = grid_for((int64_t)n * window * window, 256);
+  if (dtype == IG_DTYPE_F32)
+    condition_window_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const float*)parent, px0, py0, pw, ph, pc, scale, mask_channel, prefix, wxy, n, window,
+        (float*)out, (float*)mask_out);
+  else
+    condition_window_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const double*)parent, px0, py0, pw, ph, pc, scale, mask_channel, prefix, wxy, n, window,
+        (double*)out, (double*)mask_out);
+  return cuda_check("ig_condition_window");
+}
+
+int ig_procedural_map(uint64_t seed, uint32_t stream, int32_t cell, int64_t x0, int64_t y0,
+                      int32_t w, int32_t h, int32_t channels, float* out, void* cuda_stream) {
+  IG_REQUIRE(cell >= 1, "cell must be >= 1");
+  const int64_t total = (int64_t)channels * w * h;
+  if (total == 0) return IG_OK;
+  procedural_map_kernel<<<grid_for(total, 256), 256, 0, as_stream(cuda_stream)>>>(
+      noise_prefix(seed, stream), cell, x0, y0, w, h, channels, out);
+  return cuda_check("ig_procedural_map");
+}
+
+int ig_corrupt(const float* in, const double* levels_host, int32_t channels, uint64_t seed,
+               int64_t x0, int64_t y0, int32_t w, int32_t h, float* out, void* cuda_stream) {
+  cudaStream_t st = as_stream(cuda_stream);
+  const int64_t plane = (int64_t)w * h;
+  for (int c = 0; c < channels; ++c) {
+    const double lv = levels_host[c];
+    IG_REQUIRE(lv >= 0.0, "corruption noise levels must be >= 0");
+    if (lv == 0.0) {
+      if (out != in)
+        cudaMemcpyAsync(out + c * plane, in + c * plane, plane * sizeof(float),
+                        cudaMemcpyDeviceToDevice, st);
+      continue;
+    }
+    corrupt_kernel<<<grid_for(plane, 256), 256, 0, st>>>(
+        in + c * plane, noise_prefix(seed, 201u + (uint32_t)c), (float)lv, x0, y0, w, h,
+        out + c * plane);
+  }
+  return cuda_check("ig_corrupt");
+}
+
+int ig_raster_map(const float* raster, int32_t rc, int32_t rh, int32_t rw, int32_t mode,
+                  int64_t x0, int64_t y0, int32_t w, int32_t h, int32_t channels, float* out,
+                  void* cuda_stream) {
+  IG_REQUIRE(channels <= rc, "user map has %d channels, %d requested", rc, channels);
+  const int64_t total = (int64_t)channels * w * h;
+  if (total == 0) return IG_OK;
+  raster_map_kernel<<<grid_for(total, 256), 256, 0, as_stream(cuda_stream)>>>(
+      raster, rc, rh, rw, mode, x0, y0, w, h, channels, out);
+  return cuda_check("ig_raster_map");
+}
+
+}  // extern "C"

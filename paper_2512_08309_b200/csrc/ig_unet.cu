@@ -1,0 +1,693 @@
+// UNet Phi kernels for sm_100a: tcgen05/TMEM implicit-GEMM convolution with a
+// fused epilogue, plus the small NHWC helpers around it (input gather with the
+// consistency renoise + conditioning, 2x2 average pool, nearest upsample,
+// output preconditioning).
+//
+// ig_conv_tc -- one persistent CTA per SM, warp-specialised:
+//   warp 0     TMA producer: per K block (tap, source, 64-channel chunk) one
+//              4-D box load of the shifted activation tile (128 pixels x 64
+//              channels, zero fill outside the image = the conv padding) and
+//              one 2-D box of the K-major weights (N x 64), SWIZZLE_128B.
+//   warp 1     MMA issuer: 4 x tcgen05.mma.cta_group::1.kind::f16 (M=128,
+//              N=cout, K=16) per K block, accumulator in TMEM, commit to the
+//              stage's "empty" mbarrier; double-buffered accumulators so the
+//              epilogue of tile i overlaps the MMAs of tile i+1.
+//   warps 2-5  epilogue: tcgen05.ld 32x32b -> fp32 registers -> per-channel
+//              scale/bias, mp_sum residual, mp_silu -> bf16 NHWC stores.
+// No reference implementation exists (the reference ships analytic Phi only).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include "ig_common.cuh"
+#include "ig_noise.cuh"
+
+namespace ig {
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 16 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// K-major operand tile in SMEM written by TMA with SWIZZLE_128B: rows of 128 B
+// (64 bf16), 8-row (1024 B) swizzle atoms stacked along M/N.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
+  d |= (uint64_t)(16 >> 4) << 16;                  // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                          // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: D f32, A/B bf16, both K-major, M=128, N
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ float silu_f(float y) { return y / (1.0f + __expf(-y)); }
+
+struct ConvArgs {
+  int n, h, w, ca, cb, cout, taps;
+  int bw, bh, tiles_per_img, num_tiles, kchunks_a, kchunks_b;
+  const float* scale;
+  const float* bias;
+  const __nv_bfloat16* res;
+  float res_a, res_b, act_gain;
+  __nv_bfloat16* out0;
+  __nv_bfloat16* out1;
+};
+
+template <int N>
+struct ConvCfg {
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int A_BYTES = BM * BK * 2;            // 16 KB
+  static constexpr int B_BYTES = N * BK * 2;              // N * 128 B
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
+  static constexpr int TMEM_COLS = (2 * N <= 32) ? 32 : (2 * N <= 64) ? 64 : (2 * N <= 128) ? 128
+                                   : (2 * N <= 256) ? 256 : 512;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+};
+
+// epilogue of one 16-channel chunk for pixel p
+__device__ __forceinline__ void epi_chunk(const ConvArgs& a, int64_t p, int c0, const float* acc) {
+  float y[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) y[i] = acc[i] * __ldg(a.scale + c0 + i) + __ldg(a.bias + c0 + i);
+  const int64_t off = p * a.cout + c0;
+  if (a.res) {
+    const uint4* rp = reinterpret_cast<const uint4*>(a.res + off);
+    uint4 r0 = __ldg(rp), r1 = __ldg(rp + 1);
+    const __nv_bfloat16* rb0 = reinterpret_cast<const __nv_bfloat16*>(&r0);
+    const __nv_bfloat16* rb1 = reinterpret_cast<const __nv_bfloat16*>(&r1);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      y[i] = a.res_a * __bfloat162float(rb0[i]) + a.res_b * y[i];
+      y[i + 8] = a.res_a * __bfloat162float(rb1[i]) + a.res_b * y[i + 8];
+    }
+  }
+  if (a.out0) {
+    uint4 o[2];
+    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(o);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ob[i] = __floats2bfloat162_rn(y[2 * i], y[2 * i + 1]);
+    uint4* dp = reinterpret_cast<uint4*>(a.out0 + off);
+    dp[0] = o[0];
+    dp[1] = o[1];
+  }
+  if (a.out1) {
+    uint4 o[2];
+    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(o);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      ob[i] = __floats2bfloat162_rn(a.act_gain * silu_f(y[2 * i]),
+                                    a.act_gain * silu_f(y[2 * i + 1]));
+    uint4* dp = reinterpret_cast<uint4*>(a.out1 + off);
+    dp[0] = o[0];
+    dp[1] = o[1];
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(192, 1)
+    conv_tc_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_w, const ConvArgs args) {
+  using Cfg = ConvCfg<N>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + Cfg::STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tfull = empty + Cfg::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kchunks = args.kchunks_a + args.kchunks_b;
+  const int kblocks = args.taps * kchunks;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_a);
+    if (args.kchunks_b) prefetch_map(&map_b);
+    prefetch_map(&map_w);
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+        const int img = tile / args.tiles_per_img;
+        const int r = tile - img * args.tiles_per_img;
+        int x0, y0;
+        if (args.w >= 128) {
+          const int per_row = args.w / 128;
+          y0 = r / per_row;
+          x0 = (r - y0 * per_row) * 128;
+        } else {
+          y0 = r * args.bh;
+          x0 = 0;
+        }
+        for (int kb = 0; kb < kblocks; ++kb) {
+          const int tap = kb / kchunks;
+          const int kc = kb - tap * kchunks;
+          const int dy = args.taps == 9 ? tap / 3 - 1 : 0;
+          const int dx = args.taps == 9 ? tap % 3 - 1 : 0;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], Cfg::STAGE);
+          uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
+          if (kc < args.kchunks_a)
+            tma_load_4d(a_dst, &map_a, &full[stage], kc * 64, x0 + dx, y0 + dy, img);
+          else
+            tma_load_4d(a_dst, &map_b, &full[stage], (kc - args.kchunks_a) * 64, x0 + dx,
+                        y0 + dy, img);
+          const int kglob = tap * (args.ca + args.cb) + kc * 64;
+          tma_load_2d(sB + stage * Cfg::B_BYTES, &map_w, &full[stage], kglob, 0);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc = idesc_bf16(128, N);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * N;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = smem_desc_sw128(smem_u32(sA + stage * Cfg::A_BYTES));
+          const uint64_t bdesc = smem_desc_sw128(smem_u32(sB + stage * Cfg::B_BYTES));
+#pragma unroll
+          for (int k = 0; k < 4; ++k)  // K = 16 per MMA: +32 B in the 128 B swizzled row
+            tc_mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) ? 1u : 0u);
+          tc_commit(&empty[stage]);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5) ----------------
+    const int quarter = warp & 3;  // TMEM lanes [32*quarter, +32) belong to this warp
+    const int m = quarter * 32 + lane;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int64_t p = (int64_t)tile * 128 + m;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * N;
+#pragma unroll 1
+      for (int c0 = 0; c0 < N; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + c0, v);
+        epi_chunk(args, p, c0, v);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(Cfg::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CUDA-core reference convolution (same contract; test cross-check)
+__global__ void conv_simt_kernel(ConvArgs a, const __nv_bfloat16* __restrict__ act_a,
+                                 const __nv_bfloat16* __restrict__ act_b,
+                                 const __nv_bfloat16* __restrict__ wgt) {
+  const int64_t total = (int64_t)a.n * a.h * a.w * (a.cout / 16);
+  const int cin = a.ca + a.cb;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int chunk = (int)(idx % (a.cout / 16));
+    const int64_t p = idx / (a.cout / 16);
+    const int img = (int)(p / ((int64_t)a.h * a.w));
+    const int rem = (int)(p - (int64_t)img * a.h * a.w);
+    const int y = rem / a.w, x = rem - (rem / a.w) * a.w;
+    float acc[16];
+    for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+    for (int tap = 0; tap < a.taps; ++tap) {
+      const int dy = a.taps == 9 ? tap / 3 - 1 : 0, dx = a.taps == 9 ? tap % 3 - 1 : 0;
+      const int yy = y + dy, xx = x + dx;
+      if (yy < 0 || yy >= a.h || xx < 0 || xx >= a.w) continue;
+      const int64_t q = ((int64_t)img * a.h + yy) * a.w + xx;
+      for (int ci = 0; ci < cin; ++ci) {
+        const float xv = ci < a.ca ? __bfloat162float(act_a[q * a.ca + ci])
+                                   : __bfloat162float(act_b[q * a.cb + (ci - a.ca)]);
+        for (int i = 0; i < 16; ++i) {
+          const int co = chunk * 16 + i;
+          acc[i] += xv * __bfloat162float(wgt[((int64_t)co * a.taps + tap) * cin + ci]);
+        }
+      }
+    }
+    epi_chunk(a, p, chunk * 16, acc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// input gather: window crops of J (or unit noise), consistency renoise,
+// preconditioning, conditioning planes, constant plane -> NHWC bf16
+__global__ void unet_gather_kernel(const float* __restrict__ src, int src_batched, int64_t sx0,
+                                   int64_t sy0, int sw, int sh, int C,
+                                   const int64_t* __restrict__ wxy, int n,
+                                   const float* __restrict__ cpar, int64_t cx0, int64_t cy0,
+                                   int cw, int ch, int cc, int cscale, int cmask,
+                                   uint64_t cprefix, uint64_t rprefix, float sigma, float c_in,
+                                   int first_step, __nv_bfloat16* __restrict__ x_in, int win,
+                                   int cin_pad, int in_planes, float* __restrict__ x_noisy) {
+  const int64_t total = (int64_t)n * win * win;
+  int slow = 0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx / ((int64_t)win * win));
+    const int rem = (int)(idx - (int64_t)k * win * win);
+    const int y = rem / win, x = rem - (rem / win) * win;
+    const int64_t X = wxy[2 * k] + x, Y = wxy[2 * k + 1] + y;
+    __nv_bfloat16* dst = x_in + idx * cin_pad;
+    for (int c = 0; c < C; ++c) {
+      float v;
+      if (src_batched)
+        v = src[(((int64_t)k * C + c) * win + y) * win + x];
+      else
+        v = src[((int64_t)c * sh + (Y - sy0)) * sw + (X - sx0)];
+      float xn;
+      if (first_step) {
+        xn = __fmul_rn(sigma, v);
+      } else {
+        const float z = noise_value(rprefix, X, Y, (uint32_t)c, &slow);
+        xn = __fadd_rn(v, __fmul_rn(sigma, z));
+      }
+      x_noisy[(((int64_t)k * C + c) * win + y) * win + x] = xn;
+      dst[c] = __float2bfloat16_rn(__fmul_rn(c_in, xn));
+    }
+    int plane = C;
+    if (cc > 0) {
+      float mval = 0.f;
+      if (cpar) {
+        const int64_t px = floordiv(X, cscale) - cx0, py = floordiv(Y, cscale) - cy0;
+        const int64_t pl = (int64_t)cw * ch;
+        mval = cmask >= 0 ? cpar[cmask * pl + py * cw + px] : 1.f;
+        for (int j = 0; j < cc; ++j) {
+          float v = cpar[j * pl + py * cw + px];
+          if (mval < 1.f) v = noise_value(cprefix, X, Y, (uint32_t)j, &slow);
+          dst[plane + j] = __float2bfloat16_rn(v);
+        }
+      } else {
+        for (int j = 0; j < cc; ++j) dst[plane + j] = __float2bfloat16_rn(0.f);
+      }
+      plane += cc;
+      dst[plane++] = __float2bfloat16_rn(mval);
+    }
+    dst[plane++] = __float2bfloat16_rn(1.f);
+    for (; plane < cin_pad; ++plane) dst[plane] = __float2bfloat16_rn(0.f);
+  }
+}
+
+__global__ void unet_output_kernel(const __nv_bfloat16* __restrict__ f, int n, int h, int w,
+                                   int fc, const float* __restrict__ x_noisy, int C,
+                                   float c_skip, float c_out, float* __restrict__ out) {
+  const int64_t total = (int64_t)n * C * h * w;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t hw = (int64_t)h * w;
+    const int k = (int)(idx / (C * hw));
+    const int64_t rem = idx - (int64_t)k * C * hw;
+    const int c = (int)(rem / hw);
+    const int64_t pix = rem - (int64_t)c * hw;
+    const float fv = __bfloat162float(f[((int64_t)k * hw + pix) * fc + c]);
+    out[idx] = __fadd_rn(__fmul_rn(c_skip, x_noisy[idx]), __fmul_rn(c_out, fv));
+  }
+}
+
+__global__ void avgpool2_kernel(const __nv_bfloat16* __restrict__ in, int n, int h, int w, int c,
+                                float gain, __nv_bfloat16* __restrict__ out,
+                                __nv_bfloat16* __restrict__ out_act) {
+  const int oh = h / 2, ow = w / 2;
+  const int c8 = c / 8;
+  const int64_t total = (int64_t)n * oh * ow * c8;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int cv = (int)(idx % c8);
+    const int64_t pix = idx / c8;
+    const int img = (int)(pix / ((int64_t)oh * ow));
+    const int rem = (int)(pix - (int64_t)img * oh * ow);
+    const int oy = rem / ow, ox = rem - (rem / ow) * ow;
+    float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int d = 0; d < 4; ++d) {
+      const int yy = 2 * oy + (d >> 1), xx = 2 * ox + (d & 1);
+      const uint4 v = *reinterpret_cast<const uint4*>(
+          in + (((int64_t)img * h + yy) * w + xx) * c + cv * 8);
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
+      for (int i = 0; i < 8; ++i) s[i] += __bfloat162float(b[i]);
+    }
+    uint4 o, oa;
+    __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
+    __nv_bfloat16* oab = reinterpret_cast<__nv_bfloat16*>(&oa);
+    for (int i = 0; i < 8; ++i) {
+      const float m = s[i] * 0.25f;
+      ob[i] = __float2bfloat16_rn(m);
+      oab[i] = __float2bfloat16_rn(gain * silu_f(m));
+    }
+    const int64_t o_off = pix * c + cv * 8;
+    *reinterpret_cast<uint4*>(out + o_off) = o;
+    *reinterpret_cast<uint4*>(out_act + o_off) = oa;
+  }
+}
+
+__global__ void upsample2_kernel(const __nv_bfloat16* __restrict__ in, int n, int h, int w, int c,
+                                 __nv_bfloat16* __restrict__ out) {
+  const int c8 = c / 8;
+  const int oh = 2 * h, ow = 2 * w;
+  const int64_t total = (int64_t)n * oh * ow * c8;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int cv = (int)(idx % c8);
+    const int64_t pix = idx / c8;
+    const int img = (int)(pix / ((int64_t)oh * ow));
+    const int rem = (int)(pix - (int64_t)img * oh * ow);
+    const int oy = rem / ow, ox = rem - (rem / ow) * ow;
+    const uint4 v = *reinterpret_cast<const uint4*>(
+        in + (((int64_t)img * h + oy / 2) * w + ox / 2) * c + cv * 8);
+    *reinterpret_cast<uint4*>(out + pix * c + cv * 8) = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static int make_act_map(CUtensorMap* m, const void* base, int n, int h, int w, int c, int bw,
+                        int bh) {
+  cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)w * c * 2, (cuuint64_t)h * w * c * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)bw, (cuuint32_t)bh, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? IG_OK : IG_ERR_CUDA;
+}
+
+static int make_w_map(CUtensorMap* m, const void* base, int ktot, int cout) {
+  cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)cout};
+  cuuint64_t strides[1] = {(cuuint64_t)ktot * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)cout};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? IG_OK : IG_ERR_CUDA;
+}
+
+template <int N>
+static int launch_conv_tc(const ig_conv_params_t* p, const ConvArgs& a, cudaStream_t st) {
+  using Cfg = ConvCfg<N>;
+  CUtensorMap ma, mb, mw;
+  if (make_act_map(&ma, p->act_a, p->n, p->h, p->w, p->ca, a.bw, a.bh) != IG_OK) {
+    set_error("ig_conv_tc: cuTensorMapEncodeTiled(act_a) failed");
+    return IG_ERR_CUDA;
+  }
+  if (p->cb > 0) {
+    if (make_act_map(&mb, p->act_b, p->n, p->h, p->w, p->cb, a.bw, a.bh) != IG_OK) {
+      set_error("ig_conv_tc: cuTensorMapEncodeTiled(act_b) failed");
+      return IG_ERR_CUDA;
+    }
+  } else {
+    mb = ma;
+  }
+  if (make_w_map(&mw, p->wgt, p->taps * (p->ca + p->cb), p->cout) != IG_OK) {
+    set_error("ig_conv_tc: cuTensorMapEncodeTiled(weights) failed");
+    return IG_ERR_CUDA;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(conv_tc_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    attr_set = true;
+  }
+  const int grid = a.num_tiles < kNumSMs ? a.num_tiles : kNumSMs;
+  conv_tc_kernel<N><<<grid, 192, Cfg::SMEM, st>>>(ma, mb, mw, a);
+  return cuda_check("ig_conv_tc");
+}
+
+static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
+  IG_REQUIRE(p && p->n > 0 && p->h > 0 && p->w > 0, "conv: empty problem");
+  IG_REQUIRE(p->taps == 9 || p->taps == 1, "conv: taps must be 9 or 1");
+  IG_REQUIRE(p->ca % 64 == 0 && p->cb % 64 == 0 && p->ca > 0, "conv: channels must be multiples of 64");
+  IG_REQUIRE(p->cout % 16 == 0 && p->cout >= 16 && p->cout <= 256, "conv: cout must be 16..256, /16");
+  IG_REQUIRE(((int64_t)p->h * p->w) % 128 == 0, "conv: h*w must be a multiple of 128");
+  IG_REQUIRE((p->w & (p->w - 1)) == 0, "conv: width must be a power of two");
+  IG_REQUIRE(p->cb == 0 || p->act_b != nullptr, "conv: act_b missing");
+  a->n = p->n; a->h = p->h; a->w = p->w; a->ca = p->ca; a->cb = p->cb; a->cout = p->cout;
+  a->taps = p->taps;
+  a->bw = p->w >= 128 ? 128 : p->w;
+  a->bh = 128 / a->bw;
+  a->tiles_per_img = (int)(((int64_t)p->h * p->w) / 128);
+  a->num_tiles = a->tiles_per_img * p->n;
+  a->kchunks_a = p->ca / 64;
+  a->kchunks_b = p->cb / 64;
+  a->scale = p->scale; a->bias = p->bias;
+  a->res = reinterpret_cast<const __nv_bfloat16*>(p->res);
+  a->res_a = p->res_a; a->res_b = p->res_b; a->act_gain = p->act_gain;
+  a->out0 = reinterpret_cast<__nv_bfloat16*>(p->out0);
+  a->out1 = reinterpret_cast<__nv_bfloat16*>(p->out1);
+  (void)tc;
+  return IG_OK;
+}
+
+}  // namespace ig
+
+using namespace ig;
+
+extern "C" {
+
+size_t ig_conv_workspace_bytes(void) { return 0; }
+
+int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
+  (void)workspace;
+  ConvArgs a;
+  int rc = conv_args(p, &a, true);
+  if (rc) return rc;
+  if (!encode_fn()) {
+    set_error("ig_conv_tc: cuTensorMapEncodeTiled unavailable");
+    return IG_ERR_CUDA;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  switch (p->cout) {
+    case 16: return launch_conv_tc<16>(p, a, st);
+    case 32: return launch_conv_tc<32>(p, a, st);
+    case 64: return launch_conv_tc<64>(p, a, st);
+    case 128: return launch_conv_tc<128>(p, a, st);
+    case 192: return launch_conv_tc<192>(p, a, st);
+    case 256: return launch_conv_tc<256>(p, a, st);
+    default:
+      set_error("ig_conv_tc: unsupported cout %d", p->cout);
+      return IG_ERR_UNSUPPORTED;
+  }
+}
+
+int ig_conv_simt(const ig_conv_params_t* p, void* cuda_stream) {
+  ConvArgs a;
+  int rc = conv_args(p, &a, false);
+  if (rc) return rc;
+  const int64_t total = (int64_t)p->n * p->h * p->w * (p->cout / 16);
+  conv_simt_kernel<<<grid_for(total, 128, 64), 128, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+      a, reinterpret_cast<const __nv_bfloat16*>(p->act_a),
+      reinterpret_cast<const __nv_bfloat16*>(p->act_b),
+      reinterpret_cast<const __nv_bfloat16*>(p->wgt));
+  return cuda_check("ig_conv_simt");
+}
+
+int ig_unet_gather_input(const float* src, int32_t src_batched, int64_t src_x0, int64_t src_y0,
+                         int32_t src_w, int32_t src_h, int32_t channels, const int64_t* wxy,
+                         int32_t n, const float* cond_parent, int64_t cond_x0, int64_t cond_y0,
+                         int32_t cond_w, int32_t cond_h, int32_t cond_c, int32_t cond_scale,
+                         int32_t cond_mask_channel, uint64_t cond_seed, uint64_t renoise_seed,
+                         uint32_t renoise_stream, float sigma, float c_in, int32_t first_step,
+                         void* x_in, int32_t window, int32_t cin_pad, int32_t in_planes,
+                         float* x_noisy, void* cuda_stream) {
+  IG_REQUIRE(n >= 0 && window > 0, "gather: bad batch");
+  IG_REQUIRE(in_planes <= cin_pad, "gather: %d input planes exceed the %d padded planes",
+             in_planes, cin_pad);
+  if (n == 0) return IG_OK;
+  const int64_t total = (int64_t)n * window * window;
+  unet_gather_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+      src, src_batched, src_x0, src_y0, src_w, src_h, channels, wxy, n, cond_parent, cond_x0,
+      cond_y0, cond_w, cond_h, cond_c, cond_scale < 1 ? 1 : cond_scale, cond_mask_channel,
+      noise_prefix(cond_seed, 101u), noise_prefix(renoise_seed, renoise_stream), sigma, c_in,
+      first_step, reinterpret_cast<__nv_bfloat16*>(x_in), window, cin_pad, in_planes, x_noisy);
+  return cuda_check("ig_unet_gather_input");
+}
+
+int ig_unet_output(const void* f, int32_t n, int32_t h, int32_t w, int32_t fc,
+                   const float* x_noisy, int32_t channels, float c_skip, float c_out,
+                   int32_t flags, float* out, void* cuda_stream) {
+  (void)flags;
+  const int64_t total = (int64_t)n * channels * h * w;
+  if (total == 0) return IG_OK;
+  unet_output_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(f), n, h, w, fc, x_noisy, channels, c_skip, c_out,
+      out);
+  return cuda_check("ig_unet_output");
+}
+
+int ig_avgpool2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,
+                     void* out_act, void* cuda_stream) {
+  IG_REQUIRE(h % 2 == 0 && w % 2 == 0 && c % 8 == 0, "avgpool2: bad shape");
+  const int64_t total = (int64_t)n * (h / 2) * (w / 2) * (c / 8);
+  avgpool2_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(in), n, h, w, c, 1.0f / 0.596f,
+      reinterpret_cast<__nv_bfloat16*>(out), reinterpret_cast<__nv_bfloat16*>(out_act));
+  return cuda_check("ig_avgpool2_bf16");
+}
+
+int ig_upsample2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,
+                      void* cuda_stream) {
+  IG_REQUIRE(c % 8 == 0, "upsample2: channels must be a multiple of 8");
+  const int64_t total = (int64_t)n * (2 * h) * (2 * w) * (c / 8);
+  upsample2_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(in), n, h, w, c,
+      reinterpret_cast<__nv_bfloat16*>(out));
+  return cuda_check("ig_upsample2_bf16");
+}
+
+}  // extern "C"

@@ -1,0 +1,359 @@
+"""The consistency-distilled UNet Phi (kind ``"unet"``) on tcgen05/TMEM kernels.
+
+No reference implementation exists: the reference package
+ships analytic stand-ins only.  This module defines the build's network --
+an EDM2-style magnitude-preserving UNet with the
+sCM/consistency preconditioning -- and runs it as a sequence of NHWC bf16
+implicit-GEMM convolutions (``ig_conv_tc``: TMA -> SMEM -> tcgen05.mma ->
+TMEM -> fused epilogue).  ``oracle/unet_ref.py`` is the fp32 CPU restatement
+the parity tests compare against (same weights, rounded to bf16).
+
+Phi at outer step s (1-based, T = steps) for one window:
+    sigma      = config.sigma_for(s, T)
+    x_noisy    = sigma * x                       if s == T   (x = unit seed noise)
+               = x + sigma * z_s(X, Y)           otherwise   (consistency renoise,
+                                                  z_s = noise stream 301 + s)
+    F          = net(c_in(sigma) * x_noisy, conditioning, c_noise(sigma))
+    Phi        = c_skip(sigma) * x_noisy + c_out(sigma) * F
+Everything per pixel is a pure function of the window and absolute
+coordinates, so overlapping windows stay seed-consistent.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _device as dev
+from ._native import ConvParams, call, lib, check
+from .grid import Region
+from .noise import STREAM_RENOISE
+
+MP_SILU_GAIN = 1.0 / 0.596   # EDM2 mp_silu: silu(x) / 0.596
+RES_T = 0.3                  # EDM2 mp_sum blend of residual branch
+
+
+@dataclass(frozen=True)
+class UNetConfig:
+    """Architecture + preconditioning of the Phi network (build-defined)."""
+
+    data_channels: int = 1          # C of the sampler
+    cond_channels: int = 0          # conditioning planes (features) concatenated
+    base: int = 64
+    mults: tuple[int, ...] = (1, 2, 2, 4)
+    blocks: int = 1                 # residual blocks per encoder level (decoder: +1)
+    sigmas: tuple[float, ...] = (80.0, 1.0)   # sigma of the T, T-1, ... outer steps
+    sigma_data: float = 0.5
+    weight_seed: int = 0
+    emb_dim: int = 64               # Fourier features of c_noise
+    cin_pad: int = 64               # input planes padded to one 64-channel K block
+
+    def sigma_for(self, outer_step: int, steps: int) -> float:
+        k = steps - outer_step
+        return self.sigmas[min(k, len(self.sigmas) - 1)]
+
+    def in_planes(self) -> int:
+        # x, conditioning planes, conditioning mask, constant ones
+        extra = (self.cond_channels + 1) if self.cond_channels else 0
+        return self.data_channels + extra + 1
+
+    def channels(self) -> list[int]:
+        return [self.base * m for m in self.mults]
+
+
+def precond(cfg: UNetConfig, sigma: float):
+    sd = cfg.sigma_data
+    c_skip = sd * sd / (sigma * sigma + sd * sd)
+    c_out = sigma * sd / math.sqrt(sigma * sigma + sd * sd)
+    c_in = 1.0 / math.sqrt(sigma * sigma + sd * sd)
+    c_noise = math.log(sigma) / 4.0
+    return c_skip, c_out, c_in, c_noise
+
+
+# ---------------------------------------------------------------------------
+# layer program (shared with the CPU oracle)
+
+@dataclass
+class ConvSpec:
+    name: str
+    cin: int          # total input channels (sum of sources)
+    cout: int
+    taps: int         # 9 (3x3) or 1 (1x1)
+    cout_pad: int = 0
+    modulated: bool = False   # per-step per-channel (1 + emb) scale
+
+
+@dataclass
+class Program:
+    """Static layer list of the network (names -> conv specs) and the op
+    sequence the forward executes."""
+
+    convs: dict = field(default_factory=dict)
+    ops: list = field(default_factory=list)
+
+
+def build_program(cfg: UNetConfig) -> Program:
+    prog = Program()
+    ch = cfg.channels()
+    L = len(ch)
+
+    def conv(name, cin, cout, taps, modulated=False, cout_pad=0):
+        prog.convs[name] = ConvSpec(name, cin, cout, taps, cout_pad or cout, modulated)
+
+    # encoder
+    conv("stem", cfg.cin_pad, ch[0], 9)
+    prog.ops.append(("stem",))
+    skips = [ch[0]]
+    cur = ch[0]
+    for lv in range(L):
+        for b in range(cfg.blocks):
+            nm = f"enc{lv}.{b}"
+            conv(nm + ".c1", cur, ch[lv], 9, modulated=True)
+            conv(nm + ".c2", ch[lv], ch[lv], 9)
+            if cur != ch[lv]:
+                conv(nm + ".skip", cur, ch[lv], 1)
+            prog.ops.append(("enc", nm, cur != ch[lv]))
+            cur = ch[lv]
+            skips.append(cur)
+        if lv < L - 1:
+            prog.ops.append(("down",))
+            skips.append(cur)
+    # decoder
+    for lv in reversed(range(L)):
+        for b in range(cfg.blocks + 1):
+            nm = f"dec{lv}.{b}"
+            sk = skips.pop()
+            conv(nm + ".c1", cur + sk, ch[lv], 9, modulated=True)
+            conv(nm + ".c2", ch[lv], ch[lv], 9)
+            conv(nm + ".skip", cur + sk, ch[lv], 1)
+            prog.ops.append(("dec", nm))
+            cur = ch[lv]
+        if lv > 0:
+            prog.ops.append(("up",))
+    conv("out", cur, cfg.data_channels, 9, cout_pad=16)
+    prog.ops.append(("out",))
+    assert not skips
+    return prog
+
+
+def conv_flops(cfg: UNetConfig, h: int, w: int, padded: bool = False) -> float:
+    """Algorithmic FLOPs of one window (real input/output channels unless
+    `padded`): sum over convs of 2 * H * W * Cin * Cout * taps."""
+    prog = build_program(cfg)
+    res = {}
+    # resolution of each conv: walk the ops
+    r = (h, w)
+    lv_res = []
+    for lv in range(len(cfg.mults)):
+        lv_res.append((h >> lv, w >> lv))
+    total = 0.0
+    for name, cs in prog.convs.items():
+        if name in ("stem", "out"):
+            hh, ww = h, w
+        else:
+            lv = int(name[3:].split(".")[0])
+            hh, ww = lv_res[lv]
+        cin = cs.cin if (padded or name != "stem") else cfg.in_planes()
+        cout = cs.cout_pad if padded else cs.cout
+        total += 2.0 * hh * ww * cin * cout * cs.taps
+    return total
+
+
+def make_weights(cfg: UNetConfig) -> dict:
+    """Deterministic magnitude-preserving init (torch.manual_seed(weight_seed)).
+
+    Raw weights ~ N(0, 1); the effective weight of output row co is
+    w_raw[co] / rms(w_raw[co]) / sqrt(fan_in) (EDM2 MPConv forced
+    normalisation).  Returned as float32 CPU tensors [cout][taps][cin]
+    (K-major), zero-padded to cout_pad rows, plus the per-step embedding
+    projections.  Stem weights on padding input planes are zero.
+    """
+    prog = build_program(cfg)
+    g = torch.Generator().manual_seed(cfg.weight_seed)
+    out = {}
+    for name, cs in prog.convs.items():
+        cin_real = cfg.in_planes() if name == "stem" else cs.cin
+        wr = torch.randn(cs.cout, cs.taps, cin_real, generator=g, dtype=torch.float32)
+        rms = wr.pow(2).mean(dim=(1, 2), keepdim=True).sqrt()
+        fan_in = cs.taps * cin_real
+        weff = wr / (rms + 1e-4) / math.sqrt(fan_in)
+        full = torch.zeros(cs.cout_pad, cs.taps, cs.cin, dtype=torch.float32)
+        full[:cs.cout, :, :cin_real] = weff
+        out[name] = full
+        if cs.modulated:
+            out[name + ".emb"] = torch.randn(cs.cout, cfg.emb_dim, generator=g) / math.sqrt(
+                cfg.emb_dim)
+    out["fourier.freq"] = torch.randn(cfg.emb_dim // 2, generator=g)
+    out["fourier.phase"] = torch.rand(cfg.emb_dim // 2, generator=g)
+    out["out.gain"] = torch.tensor(1.0)
+    return out
+
+
+def round_bf16(w: torch.Tensor) -> torch.Tensor:
+    return w.to(torch.bfloat16).to(torch.float32)
+
+
+def modulation(cfg: UNetConfig, weights: dict, name: str, sigma: float) -> torch.Tensor:
+    """Per-channel (1 + emb) scale of a modulated conv at noise level sigma
+    (float32, CPU): emb = W_emb @ mp_silu(fourier(c_noise))."""
+    c_noise = math.log(sigma) / 4.0
+    f = weights["fourier.freq"]
+    ph = weights["fourier.phase"]
+    arg = 2.0 * math.pi * (f * c_noise + ph)
+    feat = torch.cat([torch.cos(arg), torch.sin(arg)]) * math.sqrt(2.0)
+    feat = torch.nn.functional.silu(feat) * MP_SILU_GAIN
+    emb = weights[name + ".emb"] @ feat
+    return (1.0 + emb).to(torch.float32)
+
+
+# ---------------------------------------------------------------------------
+# device model
+
+class UNetDevice:
+    """Weights resident in HBM (bf16, K-major) and the forward pass."""
+
+    def __init__(self, cfg: UNetConfig):
+        self.cfg = cfg
+        self.prog = build_program(cfg)
+        self.host = make_weights(cfg)
+        d = dev.device()
+        self.w = {}
+        for name, cs in self.prog.convs.items():
+            self.w[name] = self.host[name].reshape(cs.cout_pad, -1).to(torch.bfloat16).to(d)
+        self.ones = {}
+        self.zeros = {}
+        self._mod_cache = {}
+
+    def _vec1(self, n):
+        if n not in self.ones:
+            self.ones[n] = torch.ones(n, dtype=torch.float32, device=dev.device())
+            self.zeros[n] = torch.zeros(n, dtype=torch.float32, device=dev.device())
+        return self.ones[n], self.zeros[n]
+
+    def _scale(self, name, sigma):
+        key = (name, sigma)
+        if key not in self._mod_cache:
+            self._mod_cache[key] = modulation(self.cfg, self.host, name, sigma).to(dev.device())
+        return self._mod_cache[key]
+
+    # -- primitive launches -------------------------------------------------
+    def conv(self, name, a, b, sigma, res=None, out0=True, out1=True, res_ab=(0.0, 1.0)):
+        cs = self.prog.convs[name]
+        n, h, w, ca = a.shape
+        cb = 0 if b is None else b.shape[3]
+        assert ca + cb == cs.cin, (name, ca, cb, cs.cin)
+        one, zero = self._vec1(cs.cout_pad)
+        scale = self._scale(name, sigma) if cs.modulated else one
+        o0 = torch.empty((n, h, w, cs.cout_pad), dtype=torch.bfloat16, device=a.device) \
+            if out0 else None
+        o1 = torch.empty((n, h, w, cs.cout_pad), dtype=torch.bfloat16, device=a.device) \
+            if out1 else None
+        p = ConvParams(n, h, w, ca, cb, cs.cout_pad, cs.taps, a.data_ptr(), dev.ptr(b),
+                       self.w[name].data_ptr(), scale.data_ptr(), zero.data_ptr(), dev.ptr(res),
+                       res_ab[0], res_ab[1], MP_SILU_GAIN, dev.ptr(o0), dev.ptr(o1))
+        conv_launch(p)
+        return o0, o1
+
+    def forward(self, x_in: torch.Tensor, sigma: float) -> torch.Tensor:
+        """x_in: (n, H, W, cin_pad) bf16 -> F (n, H, W, 16) bf16."""
+        cfg = self.cfg
+        nrm = math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
+        ra, rb = (1 - RES_T) / nrm, RES_T / nrm
+        x, xa = self.conv("stem", x_in, None, sigma)
+        skips = [(x, xa)]
+        for op in self.prog.ops[1:]:
+            if op[0] == "enc":
+                nm, has_skip = op[1], op[2]
+                _, h1 = self.conv(nm + ".c1", xa, None, sigma, out0=False)
+                res = self.conv(nm + ".skip", x, None, sigma, out1=False)[0] if has_skip else x
+                x, xa = self.conv(nm + ".c2", h1, None, sigma, res=res, res_ab=(ra, rb))
+                skips.append((x, xa))
+            elif op[0] == "down":
+                x, xa = pool_launch(x)
+                skips.append((x, xa))
+            elif op[0] == "dec":
+                nm = op[1]
+                s, sa = skips.pop()
+                _, h1 = self.conv(nm + ".c1", xa, sa, sigma, out0=False)
+                res = self.conv(nm + ".skip", x, s, sigma, out1=False)[0]
+                x, xa = self.conv(nm + ".c2", h1, None, sigma, res=res, res_ab=(ra, rb))
+            elif op[0] == "up":
+                x, xa = upsample_launch(x), upsample_launch(xa)
+            elif op[0] == "out":
+                f, _ = self.conv("out", xa, None, sigma, out1=False)
+                return f
+        raise AssertionError("program without output layer")
+
+
+_MODELS: dict = {}
+
+
+def model_for(cfg: UNetConfig) -> UNetDevice:
+    m = _MODELS.get(cfg)
+    if m is None:
+        m = _MODELS[cfg] = UNetDevice(cfg)
+    return m
+
+
+_WS = None
+
+
+def conv_launch(p: ConvParams):
+    global _WS
+    nbytes = int(lib().ig_conv_workspace_bytes())
+    if nbytes and (_WS is None or _WS.numel() < nbytes):
+        _WS = torch.empty(nbytes, dtype=torch.uint8, device=dev.device())
+    check(lib().ig_conv_tc(p, dev.ptr(_WS) if nbytes else None, dev.stream_ptr()), "ig_conv_tc")
+
+
+def pool_launch(x: torch.Tensor):
+    n, h, w, c = x.shape
+    o = torch.empty((n, h // 2, w // 2, c), dtype=torch.bfloat16, device=x.device)
+    oa = torch.empty_like(o)
+    call("ig_avgpool2_bf16", x.data_ptr(), n, h, w, c, o.data_ptr(), oa.data_ptr(),
+         dev.stream_ptr())
+    return o, oa
+
+
+def upsample_launch(x: torch.Tensor):
+    n, h, w, c = x.shape
+    o = torch.empty((n, 2 * h, 2 * w, c), dtype=torch.bfloat16, device=x.device)
+    call("ig_upsample2_bf16", x.data_ptr(), n, h, w, c, o.data_ptr(), dev.stream_ptr())
+    return o
+
+
+def unet_phi_batch(cfg: UNetConfig, src: torch.Tensor, src_region: Region | None,
+                   wxy: torch.Tensor, win: int, outer_step: int, cond, seed: int,
+                   steps: int | None = None) -> torch.Tensor:
+    """Phi (n, C, win, win) float32 for a batch of windows (see module doc)."""
+    steps = steps if steps is not None else len(cfg.sigmas)
+    model = model_for(cfg)
+    n = int(wxy.shape[0])
+    C = cfg.data_channels
+    sigma = cfg.sigma_for(outer_step, steps)
+    c_skip, c_out, c_in, _ = precond(cfg, sigma)
+    x_in = torch.empty((n, win, win, cfg.cin_pad), dtype=torch.bfloat16, device=src.device)
+    x_noisy = torch.empty((n, C, win, win), dtype=torch.float32, device=src.device)
+    src32 = src if src.dtype == torch.float32 else src.to(torch.float32)
+    batched = src_region is None
+    sx0, sy0 = (0, 0) if batched else (src_region.x0, src_region.y0)
+    if cond is not None and cfg.cond_channels:
+        cp = cond.parent if cond.parent.dtype == torch.float32 else cond.parent.float()
+        cargs = (cp.data_ptr(), cond.region.x0, cond.region.y0, cp.shape[-1], cp.shape[-2],
+                 min(cp.shape[0], cfg.cond_channels), cond.scale,
+                 -1 if cond.mask_channel is None else cond.mask_channel, cond.seed)
+    else:
+        cargs = (None, 0, 0, 0, 0, 0, 1, -1, 0)
+    call("ig_unet_gather_input", src32.data_ptr(), int(batched), sx0, sy0, src32.shape[-1],
+         src32.shape[-2], C, wxy.data_ptr(), n, *cargs[:-1], cargs[-1] & ((1 << 64) - 1),
+         seed & ((1 << 64) - 1), STREAM_RENOISE + outer_step, float(sigma), float(c_in),
+         int(outer_step == steps), x_in.data_ptr(), win, cfg.cin_pad, cfg.in_planes(),
+         x_noisy.data_ptr(), dev.stream_ptr())
+    f = model.forward(x_in, sigma)
+    phi = torch.empty((n, C, win, win), dtype=torch.float32, device=src.device)
+    call("ig_unet_output", f.data_ptr(), n, win, win, 16, x_noisy.data_ptr(), C, float(c_skip),
+         float(c_out), 0, phi.data_ptr(), dev.stream_ptr())
+    return phi

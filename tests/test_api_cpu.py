@@ -1,0 +1,144 @@
+"""CPU-only checks: public API surface, geometry, config validation, and
+that the C-ABI library loads and exports every declared symbol."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2512_08309_b200 as ig
+from paper_2512_08309_b200 import _native, grid
+from paper_2512_08309_b200.grid import Region, WindowLayout
+from oracle import port
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+REFERENCE_ALL = [
+    "Conditioning", "ConditioningSource", "ConfigError", "CoverageError",
+    "Dependency", "DenoiserSpec", "GeneratorError", "InfigridError",
+    "LaplacianPair", "NoiseStream", "PipelineConfig", "ProceduralMap",
+    "RasterMap", "Region", "SamplerConfig", "SamplerState", "ShapeError",
+    "StageConfig", "StoreError", "StoreFormatError", "TensorSpec", "TileStore",
+    "UNBOUNDED", "WindowLayout", "build_pipeline", "coarse_patch_features",
+    "corrupt_user_map", "divide_weighted", "laplacian_decode",
+    "laplacian_encode", "laplacian_stabilize", "linear_weight_window",
+    "load_raster", "noise_at", "noise_region", "normalize_heightmap_u8",
+    "open_store", "sample", "save_raster", "signed_sqrt", "signed_square",
+    "window_region", "windows_overlapping",
+]
+
+
+def test_public_names_match_reference():
+    assert sorted(ig.__all__) == sorted(REFERENCE_ALL)
+    for n in REFERENCE_ALL:
+        assert hasattr(ig, n), n
+
+
+def test_library_exports_every_header_symbol():
+    header = open(os.path.join(ROOT, "include", "infigrid_b200.h")).read()
+    declared = set(re.findall(r"\b(ig_[a-z0-9_]+)\s*\(", header))
+    assert declared, "no declarations parsed"
+    L = ctypes.CDLL(_native.LIB_PATH)
+    for name in sorted(declared):
+        assert hasattr(L, name), f"{name} declared in include/infigrid_b200.h but not exported"
+    assert declared <= set(_native.exported_symbols()) | {"ig_conv_workspace_bytes"}
+    assert _native.lib().ig_abi_version() == 1
+
+
+def test_window_geometry_matches_port():
+    rng = np.random.default_rng(0)
+    for _ in range(300):
+        H = int(rng.integers(1, 40))
+        s = int(rng.integers(1, H + 1))
+        off = (int(rng.integers(-50, 50)), int(rng.integers(-50, 50)))
+        r = Region(int(rng.integers(-1000, 1000)), int(rng.integers(-1000, 1000)),
+                   int(rng.integers(1, 90)), int(rng.integers(1, 90)))
+        lay = WindowLayout(H, s, off)
+        got = grid.windows_overlapping(lay, r)
+        assert got == port.kappa(H, s, off, port.Box(r.x0, r.y0, r.width, r.height))
+        if _ < 40:   # brute-force scan near the region (oracle.py:95-102 style)
+            i0 = (r.x0 - off[0]) // s - H // s - 2
+            j0 = (r.y0 - off[1]) // s - H // s - 2
+            ni, nj = r.width // s + H // s + 5, r.height // s + H // s + 5
+            brute = [(i, j) for j in range(j0, j0 + nj) for i in range(i0, i0 + ni)
+                     if grid.window_region(lay, (i, j)).intersection(r)]
+            assert got == brute
+        c = grid.region_union_cover(lay, r)
+        assert (c.x0, c.y0, c.width, c.height) == port.cover(H, s, off, port.Box(
+            r.x0, r.y0, r.width, r.height)).tup()
+
+
+def test_weights_match_port():
+    for H in (1, 2, 3, 7, 16, 256):
+        for eps in (0.01, 0.5, 1.0):
+            np.testing.assert_array_equal(grid.linear_weight_window(H, eps), port.tent(H, eps))
+
+
+def test_region_semantics():
+    r = Region(-7, 3, 10, 5)
+    assert r.scale_down(4) == Region(-2, 0, 3, 2)
+    assert r.expand(2) == Region(-9, 1, 14, 9)
+    assert r.intersection(Region(100, 100, 1, 1)) is None
+    with pytest.raises(ValueError):
+        Region(0, 0, 0, 1)
+    with pytest.raises(ValueError):
+        WindowLayout(8, 9)
+    assert grid.max_window_overlap(WindowLayout(16, 8)) == 9
+
+
+def test_config_validation():
+    with pytest.raises(ValueError):
+        ig.SamplerConfig(steps=0, layout=WindowLayout(16, 8), denoiser=ig.DenoiserSpec())
+    cfg = ig.SamplerConfig(steps=2, layout=WindowLayout(16, 8), denoiser=ig.DenoiserSpec(),
+                           weights=(np.zeros((16, 16)), np.zeros((16, 16))))
+    with pytest.raises(ValueError):
+        cfg.weight_for(0)
+    with pytest.raises(ValueError):
+        ig.DenoiserSpec(kind="resnet")
+    with pytest.raises(ValueError):
+        ig.DenoiserSpec(kind="unet")
+    with pytest.raises(ig.ConfigError):
+        ig.PipelineConfig(stages=())
+    assert ig.DenoiserSpec(lambdas=(0.6, 0.4)).lambda_for(5) == 0.4
+
+
+def test_store_registration_errors():
+    store = ig.TileStore()
+    spec = ig.TensorSpec(name="t", channels=1, layout=WindowLayout(8, 4))
+    store.create_tensor(spec, lambda i, p, c: np.zeros((1, 8, 8)))
+    assert store.create_tensor(spec, None) == "t"
+    with pytest.raises(ig.StoreError):
+        store.create_tensor(ig.TensorSpec(name="t", channels=2, layout=WindowLayout(8, 4)), None)
+    with pytest.raises(ig.StoreError):
+        store.create_tensor(ig.TensorSpec(name="s", channels=1, layout=WindowLayout(8, 4),
+                                          dependencies=(ig.Dependency("s"),)), None)
+    with pytest.raises(ig.StoreError):
+        store.create_tensor(ig.TensorSpec(name="c", channels=1, layout=WindowLayout(8, 4),
+                                          cache_limit=10), None)
+    with pytest.raises(ig.StoreError):
+        ig.TileStore(tile_size=100)
+
+
+def test_raster_io(tmp_path):
+    p = str(tmp_path / "m.bin")
+    a = np.random.default_rng(0).normal(size=(2, 5, 7)).astype(np.float32)
+    ig.save_raster(p, a)
+    np.testing.assert_array_equal(ig.load_raster(p), a)
+    with open(p, "r+b") as f:
+        f.truncate(30)
+    with pytest.raises(ig.StoreFormatError):
+        ig.load_raster(p)
+
+
+def test_unet_program_and_flops():
+    from paper_2512_08309_b200 import unet
+    cfg = unet.UNetConfig()
+    prog = unet.build_program(cfg)
+    assert prog.ops[0] == ("stem",) and prog.ops[-1] == ("out",)
+    gf = unet.conv_flops(cfg, 256, 256) / 1e9
+    assert 80 < gf < 140, gf
+    w = unet.make_weights(cfg)
+    w2 = unet.make_weights(cfg)
+    assert all(np.array_equal(w[k].numpy(), w2[k].numpy()) for k in w)

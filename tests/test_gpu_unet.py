@@ -1,0 +1,152 @@
+"""tcgen05 implicit-GEMM convolution and the UNet Phi on the GPU.
+
+* ig_conv_tc vs a float32 torch reference of the same op (and vs the CUDA-core
+  ig_conv_simt) over every cout instance, 1x1/3x3 taps, two-source concat and
+  the fused epilogue (scale, residual mp_sum, mp_silu).
+* The full UNet Phi and the 2-step sampler with it vs the fp32 CPU oracle
+  (oracle/unet_ref.py) under the stated tolerance.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+import paper_2512_08309_b200 as ig  # noqa: E402
+from paper_2512_08309_b200 import unet  # noqa: E402
+from paper_2512_08309_b200._native import ConvParams, call, check, lib  # noqa: E402
+from paper_2512_08309_b200.grid import Region, WindowLayout  # noqa: E402
+
+DEV = "cuda"
+
+# Stated tolerance of the bf16 UNet path vs the fp32 oracle, relative to the
+# oracle output's standard deviation (elevation units of the sampler):
+UNET_RMS_TOL = 0.03     # RMS error / std
+UNET_MAX_TOL = 0.25     # max-abs error / std
+
+
+def _conv_ref(a, b, w, cout, taps, scale, res, ra, rb, gain):
+    x = a if b is None else torch.cat([a, b], dim=-1)
+    x = x.float().permute(0, 3, 1, 2)
+    cin = x.shape[1]
+    k = 3 if taps == 9 else 1
+    wt = w.float().reshape(cout, k, k, cin).permute(0, 3, 1, 2)
+    y = F.conv2d(x, wt, padding=k // 2).permute(0, 2, 3, 1) * scale
+    if res is not None:
+        y = ra * res.float() + rb * y
+    return y, gain * F.silu(y)
+
+
+@pytest.mark.parametrize("n,h,w,ca,cb,cout,taps", [
+    (2, 32, 32, 64, 0, 16, 9),
+    (1, 64, 64, 64, 0, 64, 9),
+    (1, 32, 256, 64, 64, 128, 9),
+    (3, 32, 32, 128, 128, 256, 9),
+    (1, 64, 128, 192, 64, 128, 1),
+    (2, 64, 64, 64, 0, 192, 9),
+    (1, 128, 128, 64, 0, 32, 9),
+])
+def test_conv_tc_matches_torch(n, h, w, ca, cb, cout, taps):
+    g = torch.Generator(device=DEV).manual_seed(n * 1000 + cout + taps)
+    a = torch.randn(n, h, w, ca, device=DEV, generator=g).bfloat16()
+    b = torch.randn(n, h, w, cb, device=DEV, generator=g).bfloat16() if cb else None
+    wgt = (torch.randn(cout, taps * (ca + cb), device=DEV, generator=g)
+           / math.sqrt(taps * (ca + cb))).bfloat16()
+    scale = torch.rand(cout, device=DEV, generator=g) + 0.5
+    bias = torch.zeros(cout, device=DEV)
+    res = torch.randn(n, h, w, cout, device=DEV, generator=g).bfloat16()
+    outs = {}
+    for kind in ("tc", "simt"):
+        o0 = torch.empty(n, h, w, cout, device=DEV, dtype=torch.bfloat16)
+        o1 = torch.empty_like(o0)
+        p = ConvParams(n, h, w, ca, cb, cout, taps, a.data_ptr(), 0 if b is None else b.data_ptr(),
+                       wgt.data_ptr(), scale.data_ptr(), bias.data_ptr(), res.data_ptr(),
+                       0.7, 0.6, 1.5, o0.data_ptr(), o1.data_ptr())
+        if kind == "tc":
+            check(lib().ig_conv_tc(p, None, torch.cuda.current_stream().cuda_stream))
+        else:
+            check(lib().ig_conv_simt(p, torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        outs[kind] = (o0.float(), o1.float())
+    y, ya = _conv_ref(a, b, wgt, cout, taps, scale, res, 0.7, 0.6, 1.5)
+    for kind, (o0, o1) in outs.items():
+        err = (o0 - y).abs().max().item()
+        tol = 0.02 * y.abs().max().item() + 0.02
+        assert err < tol, f"{kind} out0 max err {err} (tol {tol})"
+        err1 = (o1 - ya).abs().max().item()
+        assert err1 < 0.02 * ya.abs().max().item() + 0.02, f"{kind} out1 max err {err1}"
+    # tensor-core and CUDA-core device results agree to bf16 output rounding
+    d = (outs["tc"][0] - outs["simt"][0]).abs().max().item()
+    assert d <= 0.01 * y.abs().max().item() + 1e-2
+
+
+SMALL = unet.UNetConfig(base=64, mults=(1, 2), blocks=1, sigmas=(80.0, 1.0))
+
+
+def _phi_inputs(cfg, n, win, seed=0):
+    from oracle import port
+    wins = [port.Box(128 * k - 64, 32 * k, win, win) for k in range(n)]
+    xs = np.stack([port.noise(seed, 0, b, cfg.data_channels) for b in wins])
+    return wins, xs
+
+
+@pytest.mark.parametrize("outer_step", [2, 1])
+def test_unet_phi_vs_fp32_oracle(outer_step):
+    from oracle.unet_ref import unet_phi
+    cfg = SMALL
+    win = 64
+    wins, xs = _phi_inputs(cfg, 3, win)
+    wxy = torch.tensor([[b.x0, b.y0] for b in wins], dtype=torch.int64, device=DEV)
+    src = torch.from_numpy(xs).to(DEV)
+    got = unet.unet_phi_batch(cfg, src, None, wxy, win, outer_step, None, seed=0, steps=2)
+    got = got.cpu().numpy()
+    ref_phi = unet_phi(cfg, 2, 0)
+    want = np.stack([ref_phi(xs[k], None, outer_step, wins[k]) for k in range(len(wins))])
+    std = float(want.std())
+    rms = float(np.sqrt(np.mean((got - want) ** 2))) / std
+    mx = float(np.abs(got - want).max()) / std
+    assert rms < UNET_RMS_TOL and mx < UNET_MAX_TOL, (rms, mx)
+
+
+def test_sampler_unet_two_step_vs_oracle():
+    """End to end: 2-step consistency sampler with the UNet Phi, T=2 (small net,
+    64-px windows) vs the fp32 CPU oracle; elevations within the stated tolerance."""
+    from oracle import port
+    from oracle.unet_ref import unet_phi
+    cfg = SMALL
+    spec = ig.DenoiserSpec(kind="unet", unet=cfg)
+    scfg = ig.SamplerConfig(steps=2, layout=WindowLayout(64, 32), denoiser=spec, seed=0,
+                            name="unet2")
+    r = (0, 0, 128, 96)
+    st = ig.SamplerState(scfg, ig.TileStore())
+    got = st.query(0, Region(*r))
+    lay = WindowLayout(64, 32)
+    n0 = len(ig.windows_overlapping(lay, Region(*r)))
+    from paper_2512_08309_b200.grid import region_union_cover
+    n1 = len(ig.windows_overlapping(lay, region_union_cover(lay, Region(*r))))
+    assert st.denoiser_call_count(0) == n0 and st.denoiser_call_count(1) == n1
+    want, _ = port.Stage(2, (64, 32), unet_phi(cfg, 2, 0), 0).run(port.Box(*r))
+    std = float(want.std())
+    rms = float(np.sqrt(np.mean((got - want) ** 2))) / std
+    mx = float(np.abs(got - want).max()) / std
+    assert rms < UNET_RMS_TOL and mx < UNET_MAX_TOL, (rms, mx)
+    # seed consistency: re-query of a sub-region from a fresh store is bit-identical
+    sub = ig.SamplerState(scfg, ig.TileStore()).query(0, Region(32, 32, 64, 32))
+    np.testing.assert_array_equal(sub, got[:, 32:64, 32:96])
+
+
+def test_unet_batch_invariance():
+    """Phi of a window must not depend on the batch it was computed in."""
+    cfg = SMALL
+    win = 64
+    wins, xs = _phi_inputs(cfg, 5, win, seed=3)
+    wxy = torch.tensor([[b.x0, b.y0] for b in wins], dtype=torch.int64, device=DEV)
+    src = torch.from_numpy(xs).to(DEV)
+    full = unet.unet_phi_batch(cfg, src, None, wxy, win, 1, None, seed=3, steps=2)
+    one = unet.unet_phi_batch(cfg, src[2:3].contiguous(), None, wxy[2:3].contiguous(), win, 1,
+                              None, seed=3, steps=2)
+    assert torch.equal(full[2], one[0])
