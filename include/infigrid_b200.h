@@ -51,6 +51,8 @@ extern "C" {
 
 const char* ig_last_error(void);
 int ig_abi_version(void);
+/* number of kernels this library has launched in the process (instrumentation) */
+long long ig_launch_count(void);
 
 /* ---- K1 noise ----------------------------------------------------------
  * out[(c*height + py)*width + px] = G(seed, stream, x0+px, y0+py, ch0+c),

@@ -8,6 +8,9 @@ import torch
 
 _device = None
 
+# host<->device traffic issued through upload()/download() (bench e2e accounting)
+traffic = {"h2d": 0, "d2h": 0}
+
 
 def device() -> torch.device:
     global _device
@@ -51,7 +54,8 @@ def empty(shape, dtype) -> torch.Tensor:
 
 def upload(arr: np.ndarray) -> torch.Tensor:
     """Host array -> device tensor via pinned staging (async on the current stream)."""
-    t = torch.from_numpy(np.ascontiguousarray(arr))
+    t = torch.from_numpy(np.array(arr, copy=False, order="C"))
+    traffic["h2d"] += t.numel() * t.element_size()
     if t.numel() * t.element_size() >= 1 << 16:
         t = t.pin_memory()
     return t.to(device(), non_blocking=True)
@@ -62,6 +66,7 @@ def upload_i64(values) -> torch.Tensor:
 
 
 def download(t: torch.Tensor) -> np.ndarray:
+    traffic["d2h"] += t.numel() * t.element_size()
     return t.detach().to("cpu").numpy()
 
 

@@ -36,6 +36,7 @@ class ConvParams(ctypes.Structure):
 SIGNATURES = {
     "ig_last_error": [],
     "ig_abi_version": [],
+    "ig_launch_count": [],
     "ig_noise_region": [U64, U32, I64, I64, I32, I32, I32, I32, I32, V, V, V],
     "ig_phi_analytic": [I32, I32, F64, I32, V, I32, I64, I64, I32, I32, I32, V, I32, I32,
                         V, I64, I64, I32, I32, I32, I32, I32, U64, I32, V, V],
@@ -63,6 +64,7 @@ SIGNATURES = {
     "ig_upsample2_bf16": [V, I32, I32, I32, I32, V, V],
 }
 _RESTYPES = {"ig_last_error": c_char_p, "ig_abi_version": c_int32,
+             "ig_launch_count": ctypes.c_longlong,
              "ig_conv_workspace_bytes": c_size_t}
 
 _lib = None
@@ -100,6 +102,11 @@ def check(rc: int, what: str = ""):
     if rc == IG_ERR_UNSUPPORTED:
         raise ConfigError(text)
     raise StoreError(text)
+
+
+def launch_count() -> int:
+    """Kernels launched by libinfigrid_b200 so far in this process."""
+    return int(lib().ig_launch_count())
 
 
 def call(name: str, *args):

@@ -12,6 +12,9 @@ namespace ig {
 // thread-local error message behind ig_last_error()
 void set_error(const char* fmt, ...);
 
+// process-wide count of kernels this library launched (ig_launch_count)
+void note_launch();
+
 inline int cuda_check(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

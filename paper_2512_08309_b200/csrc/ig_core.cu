@@ -6,6 +6,7 @@
 // reference's numpy expressions evaluate, and the file is compiled with
 // -fmad=false as a second guard.  Reference citations are per kernel.
 #include <cstdarg>
+#include <atomic>
 #include <cstring>
 
 #include "ig_common.cuh"
@@ -21,6 +22,9 @@ void set_error(const char* fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
 }
+
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -492,6 +496,7 @@ extern "C" {
 
 const char* ig_last_error(void) { return g_err; }
 int ig_abi_version(void) { return 1; }
+long long ig_launch_count(void) { return g_launches.load(); }
 
 int ig_noise_region(uint64_t seed, uint32_t stream, int64_t x0, int64_t y0, int32_t width,
                     int32_t height, int32_t ch0, int32_t nch, int32_t out_dtype, void* out,
@@ -503,11 +508,11 @@ int ig_noise_region(uint64_t seed, uint32_t stream, int64_t x0, int64_t y0, int3
   const int64_t quads = (int64_t)((width + 3) / 4) * height * nch;
   const int grid = grid_for(quads, 256, 32);
   if (out_dtype == IG_DTYPE_F32)
-    noise_region_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        prefix, x0, y0, width, height, ch0, nch, (float*)out, slow_count);
+    { noise_region_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        prefix, x0, y0, width, height, ch0, nch, (float*)out, slow_count); note_launch(); }
   else
-    noise_region_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        prefix, x0, y0, width, height, ch0, nch, (double*)out, slow_count);
+    { noise_region_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        prefix, x0, y0, width, height, ch0, nch, (double*)out, slow_count); note_launch(); }
   return cuda_check("ig_noise_region");
 }
 
@@ -529,12 +534,12 @@ int ig_phi_analytic(int32_t kind, int32_t radius, double lam, int32_t dtype, con
   const int grid = grid_for(total, 256);
   const int lam_zero = (lam == 0.0);
   if (dtype == IG_DTYPE_F32)
-    phi_analytic_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+    { phi_analytic_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
         kind, radius, (float)(1.0 - lam), (float)lam, lam_zero, s, wxy, n, window, c,
-        (float*)out);
+        (float*)out); note_launch(); }
   else
-    phi_analytic_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        kind, radius, 1.0 - lam, lam, lam_zero, s, wxy, n, window, c, (double*)out);
+    { phi_analytic_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        kind, radius, 1.0 - lam, lam, lam_zero, s, wxy, n, window, c, (double*)out); note_launch(); }
   return cuda_check("ig_phi_analytic");
 }
 
@@ -549,13 +554,13 @@ int ig_blend(const void* const* win_data, int64_t i0, int64_t j0, int32_t ni, in
   IG_REQUIRE(mode == 0 || weight != nullptr, "blend: weighted mode needs a weight table");
   const int grid = grid_for((int64_t)rw * rh, 256);
   if (dtype == IG_DTYPE_F32)
-    blend_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+    { blend_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
         (const float* const*)win_data, i0, j0, ni, nj, window, stride, off_x, off_y, channels,
-        mode, (const float*)weight, rx0, ry0, rw, rh, divide, (float*)out);
+        mode, (const float*)weight, rx0, ry0, rw, rh, divide, (float*)out); note_launch(); }
   else
-    blend_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+    { blend_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
         (const double* const*)win_data, i0, j0, ni, nj, window, stride, off_x, off_y, channels,
-        mode, (const double*)weight, rx0, ry0, rw, rh, divide, (double*)out);
+        mode, (const double*)weight, rx0, ry0, rw, rh, divide, (double*)out); note_launch(); }
   return cuda_check("ig_blend");
 }
 
@@ -564,11 +569,11 @@ int ig_divide_weighted(const void* raw, int32_t channels, int64_t npix, int32_t 
   if (npix <= 0) return IG_OK;
   const int grid = grid_for(npix, 256);
   if (dtype == IG_DTYPE_F32)
-    divide_weighted_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        (const float*)raw, channels, npix, (float*)out);
+    { divide_weighted_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const float*)raw, channels, npix, (float*)out); note_launch(); }
   else
-    divide_weighted_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        (const double*)raw, channels, npix, (double*)out);
+    { divide_weighted_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const double*)raw, channels, npix, (double*)out); note_launch(); }
   return cuda_check("ig_divide_weighted");
 }
 
@@ -579,11 +584,11 @@ int ig_box_mean(const void* in, int32_t planes, int32_t h, int32_t w, int32_t ra
   if (total == 0) return IG_OK;
   const int grid = grid_for(total, 256);
   if (dtype == IG_DTYPE_F32)
-    box_mean_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>((const float*)in, planes, h,
-                                                                     w, radius, (float*)out);
+    { box_mean_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>((const float*)in, planes, h,
+                                                                     w, radius, (float*)out); note_launch(); }
   else
-    box_mean_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        (const double*)in, planes, h, w, radius, (double*)out);
+    { box_mean_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const double*)in, planes, h, w, radius, (double*)out); note_launch(); }
   return cuda_check("ig_box_mean");
 }
 
@@ -598,15 +603,15 @@ int ig_blur_block_mean_f64(const void* in, int32_t in_dtype, int32_t planes, int
   double* a = scratch;
   double* b = scratch + total;
   if (in_dtype == IG_DTYPE_F32)
-    widen_kernel<float><<<grid, 256, 0, st>>>((const float*)in, total, a);
+    { widen_kernel<float><<<grid, 256, 0, st>>>((const float*)in, total, a); note_launch(); }
   else
-    widen_kernel<double><<<grid, 256, 0, st>>>((const double*)in, total, a);
+    { widen_kernel<double><<<grid, 256, 0, st>>>((const double*)in, total, a); note_launch(); }
   for (int it = 0; it < blur_iters; ++it) {
-    box_mean_kernel<double><<<grid, 256, 0, st>>>(a, planes, h, w, 1, b);
+    { box_mean_kernel<double><<<grid, 256, 0, st>>>(a, planes, h, w, 1, b); note_launch(); }
     double* t = a; a = b; b = t;
   }
   const int64_t lt = total / ((int64_t)factor * factor);
-  block_mean_f64_kernel<<<grid_for(lt, 256), 256, 0, st>>>(a, planes, h, w, factor, low);
+  { block_mean_f64_kernel<<<grid_for(lt, 256), 256, 0, st>>>(a, planes, h, w, factor, low); note_launch(); }
   return cuda_check("ig_blur_block_mean_f64");
 }
 
@@ -615,11 +620,11 @@ int ig_laplacian_residual(const void* x, int32_t x_dtype, const double* low, int
   const int64_t total = (int64_t)planes * h * w;
   const int grid = grid_for(total, 256);
   if (x_dtype == IG_DTYPE_F32)
-    laplacian_residual_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        (const float*)x, low, planes, h, w, factor, high);
+    { laplacian_residual_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const float*)x, low, planes, h, w, factor, high); note_launch(); }
   else
-    laplacian_residual_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        (const double*)x, low, planes, h, w, factor, high);
+    { laplacian_residual_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const double*)x, low, planes, h, w, factor, high); note_launch(); }
   return cuda_check("ig_laplacian_residual");
 }
 
@@ -629,11 +634,11 @@ int ig_laplacian_merge(const double* low, const double* high, int32_t planes, in
   const int64_t total = (int64_t)planes * h * w;
   const int grid = grid_for(total, 256);
   if (out_dtype == IG_DTYPE_F32)
-    laplacian_merge_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        low, high, planes, h, w, factor, square_out, (float*)out);
+    { laplacian_merge_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        low, high, planes, h, w, factor, square_out, (float*)out); note_launch(); }
   else
-    laplacian_merge_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        low, high, planes, h, w, factor, square_out, (double*)out);
+    { laplacian_merge_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        low, high, planes, h, w, factor, square_out, (double*)out); note_launch(); }
   return cuda_check("ig_laplacian_merge");
 }
 
@@ -642,11 +647,11 @@ int ig_signed_pow(const void* in, int64_t n, int32_t op, int32_t dtype, void* ou
   if (n <= 0) return IG_OK;
   const int grid = grid_for(n, 256);
   if (dtype == IG_DTYPE_F32)
-    signed_pow_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>((const float*)in, n, op,
-                                                                       (float*)out);
+    { signed_pow_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>((const float*)in, n, op,
+                                                                       (float*)out); note_launch(); }
   else
-    signed_pow_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>((const double*)in, n, op,
-                                                                        (double*)out);
+    { signed_pow_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>((const double*)in, n, op,
+                                                                        (double*)out); note_launch(); }
   return cuda_check("ig_signed_pow");
 }
 
@@ -659,11 +664,11 @@ int ig_patch_features(const void* in, int64_t tile_stride, int32_t n, int32_t h,
   if (total == 0) return IG_OK;
   const int grid = grid_for(total, 128);
   if (dtype == IG_DTYPE_F32)
-    patch_features_kernel<float><<<grid, 128, 0, as_stream(cuda_stream)>>>(
-        (const float*)in, tile_stride, n, h, w, patch, rank, (float*)out);
+    { patch_features_kernel<float><<<grid, 128, 0, as_stream(cuda_stream)>>>(
+        (const float*)in, tile_stride, n, h, w, patch, rank, (float*)out); note_launch(); }
   else
-    patch_features_kernel<double><<<grid, 128, 0, as_stream(cuda_stream)>>>(
-        (const double*)in, tile_stride, n, h, w, patch, rank, (double*)out);
+    { patch_features_kernel<double><<<grid, 128, 0, as_stream(cuda_stream)>>>(
+        (const double*)in, tile_stride, n, h, w, patch, rank, (double*)out); note_launch(); }
   return cuda_check("ig_patch_features");
 }
 
@@ -676,13 +681,13 @@ int ig_condition_window(const void* parent, int64_t px0, int64_t py0, int32_t pw
   const uint64_t prefix = noise_prefix(seed, 101u);
   const int grid = grid_for((int64_t)n * window * window, 256);
   if (dtype == IG_DTYPE_F32)
-    condition_window_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+    { condition_window_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
         (const float*)parent, px0, py0, pw, ph, pc, scale, mask_channel, prefix, wxy, n, window,
-        (float*)out, (float*)mask_out);
+        (float*)out, (float*)mask_out); note_launch(); }
   else
-    condition_window_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+    { condition_window_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
         (const double*)parent, px0, py0, pw, ph, pc, scale, mask_channel, prefix, wxy, n, window,
-        (double*)out, (double*)mask_out);
+        (double*)out, (double*)mask_out); note_launch(); }
   return cuda_check("ig_condition_window");
 }
 
@@ -691,8 +696,8 @@ int ig_procedural_map(uint64_t seed, uint32_t stream, int32_t cell, int64_t x0, 
   IG_REQUIRE(cell >= 1, "cell must be >= 1");
   const int64_t total = (int64_t)channels * w * h;
   if (total == 0) return IG_OK;
-  procedural_map_kernel<<<grid_for(total, 256), 256, 0, as_stream(cuda_stream)>>>(
-      noise_prefix(seed, stream), cell, x0, y0, w, h, channels, out);
+  { procedural_map_kernel<<<grid_for(total, 256), 256, 0, as_stream(cuda_stream)>>>(
+      noise_prefix(seed, stream), cell, x0, y0, w, h, channels, out); note_launch(); }
   return cuda_check("ig_procedural_map");
 }
 
@@ -709,9 +714,9 @@ int ig_corrupt(const float* in, const double* levels_host, int32_t channels, uin
                         cudaMemcpyDeviceToDevice, st);
       continue;
     }
-    corrupt_kernel<<<grid_for(plane, 256), 256, 0, st>>>(
+    { corrupt_kernel<<<grid_for(plane, 256), 256, 0, st>>>(
         in + c * plane, noise_prefix(seed, 201u + (uint32_t)c), (float)lv, x0, y0, w, h,
-        out + c * plane);
+        out + c * plane); note_launch(); }
   }
   return cuda_check("ig_corrupt");
 }
@@ -722,8 +727,8 @@ int ig_raster_map(const float* raster, int32_t rc, int32_t rh, int32_t rw, int32
   IG_REQUIRE(channels <= rc, "user map has %d channels, %d requested", rc, channels);
   const int64_t total = (int64_t)channels * w * h;
   if (total == 0) return IG_OK;
-  raster_map_kernel<<<grid_for(total, 256), 256, 0, as_stream(cuda_stream)>>>(
-      raster, rc, rh, rw, mode, x0, y0, w, h, channels, out);
+  { raster_map_kernel<<<grid_for(total, 256), 256, 0, as_stream(cuda_stream)>>>(
+      raster, rc, rh, rw, mode, x0, y0, w, h, channels, out); note_launch(); }
   return cuda_check("ig_raster_map");
 }
 

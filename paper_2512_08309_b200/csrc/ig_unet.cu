@@ -565,7 +565,7 @@ static int launch_conv_tc(const ig_conv_params_t* p, const ConvArgs& a, cudaStre
     attr_set = true;
   }
   const int grid = a.num_tiles < kNumSMs ? a.num_tiles : kNumSMs;
-  conv_tc_kernel<N><<<grid, 192, Cfg::SMEM, st>>>(ma, mb, mw, a);
+  { conv_tc_kernel<N><<<grid, 192, Cfg::SMEM, st>>>(ma, mb, mw, a); note_launch(); }
   return cuda_check("ig_conv_tc");
 }
 
@@ -630,10 +630,10 @@ int ig_conv_simt(const ig_conv_params_t* p, void* cuda_stream) {
   int rc = conv_args(p, &a, false);
   if (rc) return rc;
   const int64_t total = (int64_t)p->n * p->h * p->w * (p->cout / 16);
-  conv_simt_kernel<<<grid_for(total, 128, 64), 128, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+  { conv_simt_kernel<<<grid_for(total, 128, 64), 128, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       a, reinterpret_cast<const __nv_bfloat16*>(p->act_a),
       reinterpret_cast<const __nv_bfloat16*>(p->act_b),
-      reinterpret_cast<const __nv_bfloat16*>(p->wgt));
+      reinterpret_cast<const __nv_bfloat16*>(p->wgt)); note_launch(); }
   return cuda_check("ig_conv_simt");
 }
 
@@ -650,11 +650,11 @@ int ig_unet_gather_input(const float* src, int32_t src_batched, int64_t src_x0, 
              in_planes, cin_pad);
   if (n == 0) return IG_OK;
   const int64_t total = (int64_t)n * window * window;
-  unet_gather_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+  { unet_gather_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       src, src_batched, src_x0, src_y0, src_w, src_h, channels, wxy, n, cond_parent, cond_x0,
       cond_y0, cond_w, cond_h, cond_c, cond_scale < 1 ? 1 : cond_scale, cond_mask_channel,
       noise_prefix(cond_seed, 101u), noise_prefix(renoise_seed, renoise_stream), sigma, c_in,
-      first_step, reinterpret_cast<__nv_bfloat16*>(x_in), window, cin_pad, in_planes, x_noisy);
+      first_step, reinterpret_cast<__nv_bfloat16*>(x_in), window, cin_pad, in_planes, x_noisy); note_launch(); }
   return cuda_check("ig_unet_gather_input");
 }
 
@@ -664,9 +664,9 @@ int ig_unet_output(const void* f, int32_t n, int32_t h, int32_t w, int32_t fc,
   (void)flags;
   const int64_t total = (int64_t)n * channels * h * w;
   if (total == 0) return IG_OK;
-  unet_output_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+  { unet_output_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(f), n, h, w, fc, x_noisy, channels, c_skip, c_out,
-      out);
+      out); note_launch(); }
   return cuda_check("ig_unet_output");
 }
 
@@ -674,9 +674,9 @@ int ig_avgpool2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c,
                      void* out_act, void* cuda_stream) {
   IG_REQUIRE(h % 2 == 0 && w % 2 == 0 && c % 8 == 0, "avgpool2: bad shape");
   const int64_t total = (int64_t)n * (h / 2) * (w / 2) * (c / 8);
-  avgpool2_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+  { avgpool2_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(in), n, h, w, c, 1.0f / 0.596f,
-      reinterpret_cast<__nv_bfloat16*>(out), reinterpret_cast<__nv_bfloat16*>(out_act));
+      reinterpret_cast<__nv_bfloat16*>(out), reinterpret_cast<__nv_bfloat16*>(out_act)); note_launch(); }
   return cuda_check("ig_avgpool2_bf16");
 }
 
@@ -684,9 +684,9 @@ int ig_upsample2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c
                       void* cuda_stream) {
   IG_REQUIRE(c % 8 == 0, "upsample2: channels must be a multiple of 8");
   const int64_t total = (int64_t)n * (2 * h) * (2 * w) * (c / 8);
-  upsample2_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+  { upsample2_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(in), n, h, w, c,
-      reinterpret_cast<__nv_bfloat16*>(out));
+      reinterpret_cast<__nv_bfloat16*>(out)); note_launch(); }
   return cuda_check("ig_upsample2_bf16");
 }
 

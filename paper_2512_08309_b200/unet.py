@@ -301,12 +301,42 @@ def model_for(cfg: UNetConfig) -> UNetDevice:
 _WS = None
 
 
+class _ConvTimer:
+    """Optional CUDA-event bracketing of every ig_conv_tc launch (bench.py's
+    roofline: per-launch device time on the launching stream)."""
+
+    def __init__(self):
+        self.on = False
+        self.events = []
+
+    def enable(self, stream=None):
+        self.on, self.events = True, []
+
+    def disable(self):
+        self.on, self.events = False, []
+
+    def collect(self):
+        torch.cuda.synchronize()
+        total = sum(a.elapsed_time(b) for a, b in self.events)
+        return total, len(self.events)
+
+
+TIMING = _ConvTimer()
+
+
 def conv_launch(p: ConvParams):
     global _WS
     nbytes = int(lib().ig_conv_workspace_bytes())
     if nbytes and (_WS is None or _WS.numel() < nbytes):
         _WS = torch.empty(nbytes, dtype=torch.uint8, device=dev.device())
+    if TIMING.on:
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
     check(lib().ig_conv_tc(p, dev.ptr(_WS) if nbytes else None, dev.stream_ptr()), "ig_conv_tc")
+    if TIMING.on:
+        b.record()
+        TIMING.events.append((a, b))
 
 
 def pool_launch(x: torch.Tensor):
