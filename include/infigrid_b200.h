@@ -168,6 +168,8 @@ typedef struct {
   void* out1;             /* bf16 or NULL */
 } ig_conv_params_t;
 size_t ig_conv_workspace_bytes(void);
+/* 1: force the per-tap (v1) kernel for every conv; 0: halo kernel where it applies */
+int ig_conv_set_variant(int force_per_tap);
 int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream);
 /* same contract on CUDA cores (fp32 accumulate, identical epilogue); used by
  * the tests as an independent device cross-check of the tensor-core kernel */

@@ -33,14 +33,25 @@ class UNetRef:
         self.prog = build_program(cfg)
         self.host = make_weights(cfg)
         self.w = {}
+        self.pad = {}
         for name, cs in self.prog.convs.items():
+            if name == "stem":
+                # the device runs the stem tap-packed; the oracle keeps the 3x3 form
+                w = round_bf16(self.host["stem.3x3"])       # [cout][9][P]
+                P = w.shape[2]
+                full = torch.zeros(cs.cout_pad, 3, 3, cfg.cin_pad)
+                full[:w.shape[0], :, :, :P] = w.reshape(w.shape[0], 3, 3, P)
+                self.w[name] = full.permute(0, 3, 1, 2).contiguous()
+                self.pad[name] = 1
+                continue
             w = round_bf16(self.host[name])                  # [cout_pad][taps][cin]
             k = 3 if cs.taps == 9 else 1
             self.w[name] = w.reshape(cs.cout_pad, k, k, cs.cin).permute(0, 3, 1, 2).contiguous()
+            self.pad[name] = k // 2
 
     def conv(self, name, x, sigma):
         cs = self.prog.convs[name]
-        y = F.conv2d(x, self.w[name], padding=1 if cs.taps == 9 else 0)
+        y = F.conv2d(x, self.w[name], padding=self.pad[name])
         if cs.modulated:
             y = y * modulation(self.cfg, self.host, name, sigma)[None, :, None, None]
         return y

@@ -54,6 +54,7 @@ SIGNATURES = {
     "ig_corrupt": [V, V, I32, U64, I64, I64, I32, I32, V, V],
     "ig_raster_map": [V, I32, I32, I32, I32, I64, I64, I32, I32, I32, V, V],
     "ig_conv_workspace_bytes": [],
+    "ig_conv_set_variant": [I32],
     "ig_conv_tc": [POINTER(ConvParams), V, V],
     "ig_conv_simt": [POINTER(ConvParams), V],
     "ig_unet_gather_input": [V, I32, I64, I64, I32, I32, I32, V, I32, V, I64, I64, I32, I32,

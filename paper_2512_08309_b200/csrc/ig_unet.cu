@@ -338,6 +338,217 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ---------------------------------------------------------------------------
+// ig_conv_tc, halo variant (3x3, width a multiple of 128).
+//
+// A tile is ROWS image rows x 128 pixels.  Per 64-channel chunk ONE TMA box
+// of (ROWS+2) x 130 pixels (the tile plus its 1-pixel halo, zero fill at the
+// image border) lands in SMEM; the 9 taps x ROWS MMAs read it through
+// descriptors whose start address is shifted by (r+dy)*130+dx rows of 128 B
+// (the SWIZZLE_128B pattern is a function of the absolute SMEM address, so a
+// row-shifted view of a TMA-written tile is itself a valid K-major operand).
+// Compared with per-tap loads this cuts activation traffic from L2 ~9x /
+// (1 + 2/ROWS), and each weight tile feeds ROWS MMAs.  When all weights of the
+// layer fit next to the halo ring they are loaded once per CTA and stay
+// resident.  8 epilogue warps: warp group g drains accumulator row g (or half
+// of the columns when ROWS == 1).
+template <int N, int ROWS>
+struct HaloCfg {
+  static constexpr int HALO_ROWS = (ROWS + 2) * 130;
+  static constexpr int HALO_TX = HALO_ROWS * 128;
+  static constexpr int HALO_BYTES = (HALO_TX + 1023) / 1024 * 1024;
+  static constexpr int B_BYTES = N * 128;
+  static constexpr int TMEM_COLS = (2 * ROWS * N <= 128) ? 128 : (2 * ROWS * N <= 256) ? 256 : 512;
+  static constexpr int BUDGET = 220 * 1024;
+  static constexpr int THREADS = 320;
+};
+
+struct HaloArgs {
+  ConvArgs c;
+  int resident;      // weights resident in SMEM
+  int b_stages;      // streamed weight ring depth (when !resident)
+  int tiles_x, tiles_y;
+};
+
+template <int N, int ROWS>
+__global__ void __launch_bounds__(320, 1)
+    conv_halo_kernel(const __grid_constant__ CUtensorMap map_a,
+                     const __grid_constant__ CUtensorMap map_b,
+                     const __grid_constant__ CUtensorMap map_w, const HaloArgs ha) {
+  using Cfg = HaloCfg<N, ROWS>;
+  const ConvArgs& args = ha.c;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int kchunks = args.kchunks_a + args.kchunks_b;
+  const int nb = ha.resident ? 9 * kchunks : ha.b_stages;   // weight tiles held in SMEM
+  uint8_t* sH = smem;                                         // 2 halo buffers
+  uint8_t* sB = smem + 2 * Cfg::HALO_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + nb * Cfg::B_BYTES);
+  uint64_t* hfull = bars;          // [2]
+  uint64_t* hempty = bars + 2;     // [2]
+  uint64_t* tfull = bars + 4;      // [2]
+  uint64_t* tempty = bars + 6;     // [2]
+  uint64_t* wfull = bars + 8;      // [1]
+  uint64_t* bfull = bars + 9;      // [b_stages]
+  uint64_t* bempty = bfull + ha.b_stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + ha.b_stages);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tiles_per_img = ha.tiles_x * ha.tiles_y;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_a);
+    if (args.kchunks_b) prefetch_map(&map_b);
+    prefetch_map(&map_w);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&hfull[s], 1);
+      mbar_init(&hempty[s], 1);
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 256);
+    }
+    mbar_init(wfull, 1);
+    for (int s = 0; s < ha.b_stages; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      if (ha.resident) {
+        mbar_expect_tx(wfull, (uint32_t)(9 * kchunks * Cfg::B_BYTES));
+        for (int t = 0; t < 9 * kchunks; ++t) {
+          const int tap = t / kchunks, kc = t - tap * kchunks;
+          tma_load_2d(sB + t * Cfg::B_BYTES, &map_w, wfull, tap * (args.ca + args.cb) + kc * 64, 0);
+        }
+      }
+      int hs = 0, bs = 0;
+      uint32_t hph = 0, bph = 0;
+      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+        const int img = tile / tiles_per_img;
+        const int r = tile - img * tiles_per_img;
+        const int ty = r / ha.tiles_x;
+        const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
+        for (int kc = 0; kc < kchunks; ++kc) {
+          mbar_wait(&hempty[hs], hph ^ 1);
+          mbar_expect_tx(&hfull[hs], Cfg::HALO_TX);
+          uint8_t* dst = sH + hs * Cfg::HALO_BYTES;
+          if (kc < args.kchunks_a)
+            tma_load_4d(dst, &map_a, &hfull[hs], kc * 64, x0 - 1, y0 - 1, img);
+          else
+            tma_load_4d(dst, &map_b, &hfull[hs], (kc - args.kchunks_a) * 64, x0 - 1, y0 - 1, img);
+          if (++hs == 2) { hs = 0; hph ^= 1; }
+          if (!ha.resident) {
+            for (int tap = 0; tap < 9; ++tap) {
+              mbar_wait(&bempty[bs], bph ^ 1);
+              mbar_expect_tx(&bfull[bs], Cfg::B_BYTES);
+              tma_load_2d(sB + bs * Cfg::B_BYTES, &map_w, &bfull[bs],
+                          tap * (args.ca + args.cb) + kc * 64, 0);
+              if (++bs == ha.b_stages) { bs = 0; bph ^= 1; }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc = idesc_bf16(128, N);
+      if (ha.resident) mbar_wait(wfull, 0);
+      int hs = 0, bs = 0;
+      uint32_t hph = 0, bph = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + acc * ROWS * N;
+        for (int kc = 0; kc < kchunks; ++kc) {
+          mbar_wait(&hfull[hs], hph);
+          tc_fence_after();
+          const uint32_t hbase = smem_u32(sH + hs * Cfg::HALO_BYTES);
+          for (int tap = 0; tap < 9; ++tap) {
+            const int dy = tap / 3, dx = tap % 3;
+            uint32_t baddr;
+            if (ha.resident) {
+              baddr = smem_u32(sB + (tap * kchunks + kc) * Cfg::B_BYTES);
+            } else {
+              mbar_wait(&bfull[bs], bph);
+              tc_fence_after();
+              baddr = smem_u32(sB + bs * Cfg::B_BYTES);
+            }
+            const uint64_t bdesc = smem_desc_sw128(baddr);
+#pragma unroll
+            for (int rr = 0; rr < ROWS; ++rr) {
+              const uint64_t adesc = smem_desc_sw128(hbase + ((rr + dy) * 130 + dx) * 128);
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                tc_mma(d0 + rr * N, adesc + 2 * k, bdesc + 2 * k, idesc,
+                       (kc | tap | k) ? 1u : 0u);
+            }
+            if (!ha.resident) {
+              tc_commit(&bempty[bs]);
+              if (++bs == ha.b_stages) { bs = 0; bph ^= 1; }
+            }
+          }
+          tc_commit(&hempty[hs]);
+          if (++hs == 2) { hs = 0; hph ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..9) ----------------
+    const int quarter = warp & 3;
+    const int grp = (warp - 2) >> 2;  // 0 or 1
+    const int m = quarter * 32 + lane;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int img = tile / tiles_per_img;
+      const int r = tile - img * tiles_per_img;
+      const int ty = r / ha.tiles_x;
+      const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
+      const int row = ROWS == 2 ? grp : 0;
+      const int cbeg = ROWS == 2 ? 0 : grp * (N / 2);
+      const int cend = ROWS == 2 ? N : cbeg + N / 2;
+      const int64_t p = ((int64_t)img * args.h + y0 + row) * args.w + x0 + m;
+      const uint32_t taddr =
+          tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N + row * N;
+#pragma unroll 1
+      for (int c0 = cbeg; c0 < cend; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + c0, v);
+        epi_chunk(args, p, c0, v);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(Cfg::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // CUDA-core reference convolution (same contract; test cross-check)
 __global__ void conv_simt_kernel(ConvArgs a, const __nv_bfloat16* __restrict__ act_a,
                                  const __nv_bfloat16* __restrict__ act_b,
@@ -373,60 +584,110 @@ __global__ void conv_simt_kernel(ConvArgs a, const __nv_bfloat16* __restrict__ a
 
 // ---------------------------------------------------------------------------
 // input gather: window crops of J (or unit noise), consistency renoise,
-// preconditioning, conditioning planes, constant plane -> NHWC bf16
-__global__ void unet_gather_kernel(const float* __restrict__ src, int src_batched, int64_t sx0,
-                                   int64_t sy0, int sw, int sh, int C,
-                                   const int64_t* __restrict__ wxy, int n,
-                                   const float* __restrict__ cpar, int64_t cx0, int64_t cy0,
-                                   int cw, int ch, int cc, int cscale, int cmask,
-                                   uint64_t cprefix, uint64_t rprefix, float sigma, float c_in,
-                                   int first_step, __nv_bfloat16* __restrict__ x_in, int win,
-                                   int cin_pad, int in_planes, float* __restrict__ x_noisy) {
-  const int64_t total = (int64_t)n * win * win;
+// preconditioning, conditioning planes, constant plane, then TAP PACKING:
+// the stem 3x3 conv over P <= 7 input planes is rewritten as a 1x1 GEMM over
+// 9*P <= 64 packed channels (channel tap*P + p = plane p of the neighbour at
+// tap (dy, dx), zero outside the window = the conv's zero padding), so the
+// stem costs K = 64 instead of 9 x 64 padded K.
+// One CTA computes the P planes of a (TY+2) x (TX+2) halo tile into SMEM,
+// then every thread packs one output pixel with 8 x 16-byte stores.
+constexpr int GTX = 32, GTY = 8, GPL = 8;
+
+__device__ __forceinline__ void gather_planes(
+    const float* __restrict__ src, int src_batched, int64_t sx0, int64_t sy0, int sw, int sh,
+    int C, int k, int win, int y, int x, int64_t X, int64_t Y, const float* __restrict__ cpar,
+    int64_t cx0, int64_t cy0, int cw, int ch, int cc, int cscale, int cmask, uint64_t cprefix,
+    uint64_t rprefix, float sigma, float c_in, int first_step, float* out_planes,
+    float* x_noisy_store, int* slow) {
+  for (int c = 0; c < C; ++c) {
+    float v;
+    if (src_batched)
+      v = src[(((int64_t)k * C + c) * win + y) * win + x];
+    else
+      v = src[((int64_t)c * sh + (Y - sy0)) * sw + (X - sx0)];
+    float xn;
+    if (first_step) {
+      xn = __fmul_rn(sigma, v);
+    } else {
+      const float z = noise_value(rprefix, X, Y, (uint32_t)c, slow);
+      xn = __fadd_rn(v, __fmul_rn(sigma, z));
+    }
+    if (x_noisy_store) x_noisy_store[c] = xn;
+    out_planes[c] = __fmul_rn(c_in, xn);
+  }
+  int plane = C;
+  if (cc > 0) {
+    float mval = 0.f;
+    if (cpar) {
+      const int64_t px = floordiv(X, cscale) - cx0, py = floordiv(Y, cscale) - cy0;
+      const int64_t pl = (int64_t)cw * ch;
+      mval = cmask >= 0 ? cpar[cmask * pl + py * cw + px] : 1.f;
+      for (int j = 0; j < cc; ++j) {
+        float v = cpar[j * pl + py * cw + px];
+        if (mval < 1.f) v = noise_value(cprefix, X, Y, (uint32_t)j, slow);
+        out_planes[plane + j] = v;
+      }
+    } else {
+      for (int j = 0; j < cc; ++j) out_planes[plane + j] = 0.f;
+    }
+    plane += cc;
+    out_planes[plane++] = mval;
+  }
+  out_planes[plane++] = 1.f;
+}
+
+__global__ void __launch_bounds__(GTX * GTY) unet_gather_kernel(
+    const float* __restrict__ src, int src_batched, int64_t sx0, int64_t sy0, int sw, int sh,
+    int C, const int64_t* __restrict__ wxy, int n, const float* __restrict__ cpar, int64_t cx0,
+    int64_t cy0, int cw, int ch, int cc, int cscale, int cmask, uint64_t cprefix,
+    uint64_t rprefix, float sigma, float c_in, int first_step, __nv_bfloat16* __restrict__ x_in,
+    int win, int cin_pad, int P, float* __restrict__ x_noisy) {
+  __shared__ __nv_bfloat16 tile[(GTY + 2) * (GTX + 2)][GPL];
+  const int tiles_x = (win + GTX - 1) / GTX, tiles_y = (win + GTY - 1) / GTY;
+  const int64_t ntiles = (int64_t)n * tiles_x * tiles_y;
   int slow = 0;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(idx / ((int64_t)win * win));
-    const int rem = (int)(idx - (int64_t)k * win * win);
-    const int y = rem / win, x = rem - (rem / win) * win;
-    const int64_t X = wxy[2 * k] + x, Y = wxy[2 * k + 1] + y;
-    __nv_bfloat16* dst = x_in + idx * cin_pad;
-    for (int c = 0; c < C; ++c) {
-      float v;
-      if (src_batched)
-        v = src[(((int64_t)k * C + c) * win + y) * win + x];
-      else
-        v = src[((int64_t)c * sh + (Y - sy0)) * sw + (X - sx0)];
-      float xn;
-      if (first_step) {
-        xn = __fmul_rn(sigma, v);
-      } else {
-        const float z = noise_value(rprefix, X, Y, (uint32_t)c, &slow);
-        xn = __fadd_rn(v, __fmul_rn(sigma, z));
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int k = (int)(t / (tiles_x * tiles_y));
+    const int r = (int)(t - (int64_t)k * tiles_x * tiles_y);
+    const int ty0 = (r / tiles_x) * GTY, tx0 = (r % tiles_x) * GTX;
+    const int64_t WX = wxy[2 * k], WY = wxy[2 * k + 1];
+    // phase 1: planes of the halo tile (zero outside the window)
+    for (int q = threadIdx.x; q < (GTY + 2) * (GTX + 2); q += blockDim.x) {
+      const int hy = q / (GTX + 2), hx = q - hy * (GTX + 2);
+      const int y = ty0 + hy - 1, x = tx0 + hx - 1;
+      float pl[GPL];
+#pragma unroll
+      for (int i = 0; i < GPL; ++i) pl[i] = 0.f;
+      if (y >= 0 && y < win && x >= 0 && x < win) {
+        const bool interior = hy >= 1 && hy <= GTY && hx >= 1 && hx <= GTX;
+        float xn[GPL];
+        gather_planes(src, src_batched, sx0, sy0, sw, sh, C, k, win, y, x, WX + x, WY + y, cpar,
+                      cx0, cy0, cw, ch, cc, cscale, cmask, cprefix, rprefix, sigma, c_in,
+                      first_step, pl, interior ? xn : nullptr, &slow);
+        if (interior)
+          for (int c = 0; c < C; ++c) x_noisy[(((int64_t)k * C + c) * win + y) * win + x] = xn[c];
       }
-      x_noisy[(((int64_t)k * C + c) * win + y) * win + x] = xn;
-      dst[c] = __float2bfloat16_rn(__fmul_rn(c_in, xn));
+#pragma unroll
+      for (int i = 0; i < GPL; ++i) tile[q][i] = __float2bfloat16_rn(pl[i]);
     }
-    int plane = C;
-    if (cc > 0) {
-      float mval = 0.f;
-      if (cpar) {
-        const int64_t px = floordiv(X, cscale) - cx0, py = floordiv(Y, cscale) - cy0;
-        const int64_t pl = (int64_t)cw * ch;
-        mval = cmask >= 0 ? cpar[cmask * pl + py * cw + px] : 1.f;
-        for (int j = 0; j < cc; ++j) {
-          float v = cpar[j * pl + py * cw + px];
-          if (mval < 1.f) v = noise_value(cprefix, X, Y, (uint32_t)j, &slow);
-          dst[plane + j] = __float2bfloat16_rn(v);
-        }
-      } else {
-        for (int j = 0; j < cc; ++j) dst[plane + j] = __float2bfloat16_rn(0.f);
+    __syncthreads();
+    // phase 2: pack the 3x3 neighbourhood of each output pixel
+    const int ly = threadIdx.x / GTX, lx = threadIdx.x % GTX;
+    const int y = ty0 + ly, x = tx0 + lx;
+    if (y < win && x < win) {
+      __align__(16) __nv_bfloat16 packed[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) packed[i] = __float2bfloat16_rn(0.f);
+      for (int tap = 0; tap < 9; ++tap) {
+        const int q = (ly + tap / 3) * (GTX + 2) + lx + tap % 3;
+        for (int p = 0; p < P; ++p) packed[tap * P + p] = tile[q][p];
       }
-      plane += cc;
-      dst[plane++] = __float2bfloat16_rn(mval);
+      uint4* dst = reinterpret_cast<uint4*>(x_in + (((int64_t)k * win + y) * win + x) * cin_pad);
+      const uint4* srcv = reinterpret_cast<const uint4*>(packed);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[i] = srcv[i];
     }
-    dst[plane++] = __float2bfloat16_rn(1.f);
-    for (; plane < cin_pad; ++plane) dst[plane] = __float2bfloat16_rn(0.f);
+    __syncthreads();
   }
 }
 
@@ -514,8 +775,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-static int make_act_map(CUtensorMap* m, const void* base, int n, int h, int w, int c, int bw,
-                        int bh) {
+static int make_act_map_box(CUtensorMap* m, const void* base, int n, int h, int w, int c, int bw,
+                            int bh) {
   cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
   cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)w * c * 2, (cuuint64_t)h * w * c * 2};
   cuuint32_t box[4] = {64, (cuuint32_t)bw, (cuuint32_t)bh, 1};
@@ -525,6 +786,11 @@ static int make_act_map(CUtensorMap* m, const void* base, int n, int h, int w, i
                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? IG_OK : IG_ERR_CUDA;
+}
+
+static int make_act_map(CUtensorMap* m, const void* base, int n, int h, int w, int c, int bw,
+                        int bh) {
+  return make_act_map_box(m, base, n, h, w, c, bw, bh);
 }
 
 static int make_w_map(CUtensorMap* m, const void* base, int ktot, int cout) {
@@ -569,6 +835,54 @@ static int launch_conv_tc(const ig_conv_params_t* p, const ConvArgs& a, cudaStre
   return cuda_check("ig_conv_tc");
 }
 
+template <int N, int ROWS>
+static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaStream_t st) {
+  using Cfg = HaloCfg<N, ROWS>;
+  CUtensorMap ma, mb, mw;
+  if (make_act_map_box(&ma, p->act_a, p->n, p->h, p->w, p->ca, 130, ROWS + 2) != IG_OK ||
+      (p->cb > 0 && make_act_map_box(&mb, p->act_b, p->n, p->h, p->w, p->cb, 130, ROWS + 2) != IG_OK) ||
+      make_w_map(&mw, p->wgt, p->taps * (p->ca + p->cb), p->cout) != IG_OK) {
+    set_error("ig_conv_tc(halo): cuTensorMapEncodeTiled failed");
+    return IG_ERR_CUDA;
+  }
+  if (p->cb == 0) mb = ma;
+  HaloArgs ha;
+  ha.c = a;
+  ha.tiles_x = p->w / 128;
+  ha.tiles_y = p->h / ROWS;
+  ha.c.num_tiles = p->n * ha.tiles_x * ha.tiles_y;
+  const int kchunks = a.kchunks_a + a.kchunks_b;
+  const int wbytes = 9 * kchunks * Cfg::B_BYTES;
+  const int fixed = 1024 + 2 * Cfg::HALO_BYTES + 512;
+  int smem;
+  if (fixed + wbytes <= Cfg::BUDGET) {
+    ha.resident = 1;
+    ha.b_stages = 1;
+    smem = fixed + wbytes;
+  } else {
+    ha.resident = 0;
+    int stages = (Cfg::BUDGET - fixed) / Cfg::B_BYTES;
+    if (stages > 8) stages = 8;
+    if (stages < 2) {
+      set_error("ig_conv_tc(halo): no room for the weight ring");
+      return IG_ERR_UNSUPPORTED;
+    }
+    ha.b_stages = stages;
+    smem = fixed + stages * Cfg::B_BYTES;
+  }
+  static int attr_smem = 0;
+  if (attr_smem < smem) {
+    cudaFuncSetAttribute(conv_halo_kernel<N, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    attr_smem = 227 * 1024;
+  }
+  const int grid = ha.c.num_tiles < kNumSMs ? ha.c.num_tiles : kNumSMs;
+  { conv_halo_kernel<N, ROWS><<<grid, Cfg::THREADS, smem, st>>>(ma, mb, mw, ha); note_launch(); }
+  return cuda_check("ig_conv_tc(halo)");
+}
+
+static bool g_force_v1 = false;
+
 static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   IG_REQUIRE(p && p->n > 0 && p->h > 0 && p->w > 0, "conv: empty problem");
   IG_REQUIRE(p->taps == 9 || p->taps == 1, "conv: taps must be 9 or 1");
@@ -602,6 +916,12 @@ extern "C" {
 
 size_t ig_conv_workspace_bytes(void) { return 0; }
 
+// 1: route every convolution through the per-tap kernel (tests / A-B timing)
+int ig_conv_set_variant(int force_per_tap) {
+  g_force_v1 = force_per_tap != 0;
+  return IG_OK;
+}
+
 int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
   (void)workspace;
   ConvArgs a;
@@ -612,6 +932,22 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
     return IG_ERR_CUDA;
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  const bool halo = p->taps == 9 && p->w % 128 == 0 && !g_force_v1;
+  if (halo && p->cout <= 128 && p->h % 2 == 0) {
+    switch (p->cout) {
+      case 16: return launch_conv_halo<16, 2>(p, a, st);
+      case 32: return launch_conv_halo<32, 2>(p, a, st);
+      case 64: return launch_conv_halo<64, 2>(p, a, st);
+      case 128: return launch_conv_halo<128, 2>(p, a, st);
+      default: break;
+    }
+  } else if (halo) {
+    switch (p->cout) {
+      case 192: return launch_conv_halo<192, 1>(p, a, st);
+      case 256: return launch_conv_halo<256, 1>(p, a, st);
+      default: break;
+    }
+  }
   switch (p->cout) {
     case 16: return launch_conv_tc<16>(p, a, st);
     case 32: return launch_conv_tc<32>(p, a, st);
@@ -646,11 +982,13 @@ int ig_unet_gather_input(const float* src, int32_t src_batched, int64_t src_x0, 
                          void* x_in, int32_t window, int32_t cin_pad, int32_t in_planes,
                          float* x_noisy, void* cuda_stream) {
   IG_REQUIRE(n >= 0 && window > 0, "gather: bad batch");
-  IG_REQUIRE(in_planes <= cin_pad, "gather: %d input planes exceed the %d padded planes",
-             in_planes, cin_pad);
+  IG_REQUIRE(cin_pad == 64, "gather: the packed stem input has 64 channels");
+  IG_REQUIRE(in_planes <= 7 && 9 * in_planes <= cin_pad,
+             "gather: %d input planes do not tap-pack into %d channels", in_planes, cin_pad);
   if (n == 0) return IG_OK;
-  const int64_t total = (int64_t)n * window * window;
-  { unet_gather_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+  const int64_t tiles = (int64_t)n * ((window + GTX - 1) / GTX) * ((window + GTY - 1) / GTY);
+  const int grid = (int)(tiles < (int64_t)kNumSMs * 16 ? tiles : (int64_t)kNumSMs * 16);
+  { unet_gather_kernel<<<grid, GTX * GTY, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       src, src_batched, src_x0, src_y0, src_w, src_h, channels, wxy, n, cond_parent, cond_x0,
       cond_y0, cond_w, cond_h, cond_c, cond_scale < 1 ? 1 : cond_scale, cond_mask_channel,
       noise_prefix(cond_seed, 101u), noise_prefix(renoise_seed, renoise_stream), sigma, c_in,

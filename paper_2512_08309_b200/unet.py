@@ -103,8 +103,9 @@ def build_program(cfg: UNetConfig) -> Program:
     def conv(name, cin, cout, taps, modulated=False, cout_pad=0):
         prog.convs[name] = ConvSpec(name, cin, cout, taps, cout_pad or cout, modulated)
 
-    # encoder
-    conv("stem", cfg.cin_pad, ch[0], 9)
+    # encoder; the stem 3x3 conv over in_planes() planes runs tap-packed as a
+    # 1x1 GEMM over 9 * in_planes <= cin_pad channels (see ig_unet_gather_input)
+    conv("stem", cfg.cin_pad, ch[0], 1)
     prog.ops.append(("stem",))
     skips = [ch[0]]
     cur = ch[0]
@@ -156,9 +157,11 @@ def conv_flops(cfg: UNetConfig, h: int, w: int, padded: bool = False) -> float:
         else:
             lv = int(name[3:].split(".")[0])
             hh, ww = lv_res[lv]
-        cin = cs.cin if (padded or name != "stem") else cfg.in_planes()
         cout = cs.cout_pad if padded else cs.cout
-        total += 2.0 * hh * ww * cin * cout * cs.taps
+        if name == "stem" and not padded:
+            total += 2.0 * hh * ww * cfg.in_planes() * cout * 9    # the real 3x3 conv
+        else:
+            total += 2.0 * hh * ww * cs.cin * cout * cs.taps
     return total
 
 
@@ -175,13 +178,20 @@ def make_weights(cfg: UNetConfig) -> dict:
     g = torch.Generator().manual_seed(cfg.weight_seed)
     out = {}
     for name, cs in prog.convs.items():
-        cin_real = cfg.in_planes() if name == "stem" else cs.cin
-        wr = torch.randn(cs.cout, cs.taps, cin_real, generator=g, dtype=torch.float32)
+        stem = name == "stem"
+        cin_real = cfg.in_planes() if stem else cs.cin
+        taps = 9 if stem else cs.taps
+        wr = torch.randn(cs.cout, taps, cin_real, generator=g, dtype=torch.float32)
         rms = wr.pow(2).mean(dim=(1, 2), keepdim=True).sqrt()
-        fan_in = cs.taps * cin_real
+        fan_in = taps * cin_real
         weff = wr / (rms + 1e-4) / math.sqrt(fan_in)
-        full = torch.zeros(cs.cout_pad, cs.taps, cs.cin, dtype=torch.float32)
-        full[:cs.cout, :, :cin_real] = weff
+        if stem:
+            out["stem.3x3"] = weff                       # [cout][9][P] (oracle form)
+            full = torch.zeros(cs.cout_pad, 1, cs.cin, dtype=torch.float32)
+            full[:cs.cout, 0, :9 * cin_real] = weff.reshape(cs.cout, 9 * cin_real)
+        else:
+            full = torch.zeros(cs.cout_pad, cs.taps, cs.cin, dtype=torch.float32)
+            full[:cs.cout, :, :cin_real] = weff
         out[name] = full
         if cs.modulated:
             out[name + ".emb"] = torch.randn(cs.cout, cfg.emb_dim, generator=g) / math.sqrt(

@@ -49,8 +49,24 @@ def _conv_ref(a, b, w, cout, taps, scale, res, ra, rb, gain):
     (1, 64, 128, 192, 64, 128, 1),
     (2, 64, 64, 64, 0, 192, 9),
     (1, 128, 128, 64, 0, 32, 9),
+    # halo-kernel shapes (width a multiple of 128): resident / streamed weights,
+    # two-row and one-row tiles, two sources
+    (2, 64, 256, 64, 0, 64, 9),
+    (1, 32, 128, 128, 64, 128, 9),
+    (1, 16, 128, 64, 0, 256, 9),
+    (1, 8, 256, 128, 64, 64, 9),
+    (1, 4, 128, 64, 0, 16, 9),
 ])
-def test_conv_tc_matches_torch(n, h, w, ca, cb, cout, taps):
+@pytest.mark.parametrize("variant", ["auto", "per_tap"])
+def test_conv_tc_matches_torch(n, h, w, ca, cb, cout, taps, variant):
+    check(lib().ig_conv_set_variant(1 if variant == "per_tap" else 0))
+    try:
+        _run_conv_case(n, h, w, ca, cb, cout, taps)
+    finally:
+        check(lib().ig_conv_set_variant(0))
+
+
+def _run_conv_case(n, h, w, ca, cb, cout, taps):
     g = torch.Generator(device=DEV).manual_seed(n * 1000 + cout + taps)
     a = torch.randn(n, h, w, ca, device=DEV, generator=g).bfloat16()
     b = torch.randn(n, h, w, cb, device=DEV, generator=g).bfloat16() if cb else None
