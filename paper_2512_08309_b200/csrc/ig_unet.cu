@@ -128,7 +128,16 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
          ((uint32_t)(M >> 4) << 24);
 }
 
-__device__ __forceinline__ float silu_f(float y) { return y / (1.0f + __expf(-y)); }
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// gain * silu(y) = y * (0.5 g + 0.5 g tanh(y / 2))   (MUFU.TANH, |rel err| < 2^-10)
+__device__ __forceinline__ float gsilu(float y, float half_gain) {
+  return y * fmaf(half_gain, tanh_approx(0.5f * y), half_gain);
+}
+__device__ __forceinline__ float silu_f(float y) { return gsilu(y, 0.5f); }
 
 struct ConvArgs {
   int n, h, w, ca, cb, cout, taps;
@@ -150,14 +159,15 @@ struct ConvCfg {
   static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
   static constexpr int TMEM_COLS = (2 * N <= 32) ? 32 : (2 * N <= 64) ? 64 : (2 * N <= 128) ? 128
                                    : (2 * N <= 256) ? 256 : 512;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + 1024;
 };
 
 // epilogue of one 16-channel chunk for pixel p
 __device__ __forceinline__ void epi_chunk(const ConvArgs& a, int64_t p, int c0, const float* acc) {
   float y[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) y[i] = acc[i] * __ldg(a.scale + c0 + i) + __ldg(a.bias + c0 + i);
+  for (int i = 0; i < 16; ++i)
+    y[i] = acc[i] * (a.scale ? __ldg(a.scale + c0 + i) : 1.f) + (a.bias ? __ldg(a.bias + c0 + i) : 0.f);
   const int64_t off = p * a.cout + c0;
   if (a.res) {
     const uint4* rp = reinterpret_cast<const uint4*>(a.res + off);
@@ -182,18 +192,111 @@ __device__ __forceinline__ void epi_chunk(const ConvArgs& a, int64_t p, int c0, 
   if (a.out1) {
     uint4 o[2];
     __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(o);
+    const float hg = 0.5f * a.act_gain;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-      ob[i] = __floats2bfloat162_rn(a.act_gain * silu_f(y[2 * i]),
-                                    a.act_gain * silu_f(y[2 * i + 1]));
+      ob[i] = __floats2bfloat162_rn(gsilu(y[2 * i], hg), gsilu(y[2 * i + 1], hg));
     uint4* dp = reinterpret_cast<uint4*>(a.out1 + off);
     dp[0] = o[0];
     dp[1] = o[1];
   }
 }
 
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Epilogue of NC consecutive accumulator columns [c0, c0+NC) of one pixel p
+// (this thread's TMEM lane): residual prefetched for the whole span, TMEM read
+// in 32-column blocks (two x16 loads, one wait), scale from SMEM (nullptr:
+// identity), fused mp_sum / mp_silu, 16-byte stores.
+template <int NC>
+__device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale, int64_t p,
+                                         int c0, uint32_t taddr) {
+  constexpr int BC = NC < 32 ? NC : 32;
+  const int64_t off = p * a.cout + c0;
+  uint4 res[NC / 8];
+  if (a.res) {
+#pragma unroll
+    for (int i = 0; i < NC / 8; ++i) res[i] = ldg_nc_v4(a.res + off + 8 * i);
+  }
+  const float hg = 0.5f * a.act_gain;
+#pragma unroll
+  for (int b = 0; b < NC; b += BC) {
+    uint32_t r[BC];
+    if constexpr (BC == 32) {
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+            "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+            "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+            "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+            "=r"(r[31])
+          : "r"(taddr + c0 + b));
+    } else {
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+            "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(taddr + c0 + b));
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    float y[BC];
+#pragma unroll
+    for (int i = 0; i < BC; ++i) {
+      y[i] = __uint_as_float(r[i]);
+      if (s_scale) y[i] *= s_scale[c0 + b + i];
+    }
+    if (a.bias) {
+#pragma unroll
+      for (int i = 0; i < BC; ++i) y[i] += __ldg(a.bias + c0 + b + i);
+    }
+    if (a.res) {
+#pragma unroll
+      for (int i = 0; i < BC / 8; ++i) {
+        const __nv_bfloat162* rb = reinterpret_cast<const __nv_bfloat162*>(&res[b / 8 + i]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(rb[j]);
+          y[8 * i + 2 * j] = fmaf(a.res_a, f.x, a.res_b * y[8 * i + 2 * j]);
+          y[8 * i + 2 * j + 1] = fmaf(a.res_a, f.y, a.res_b * y[8 * i + 2 * j + 1]);
+        }
+      }
+    }
+    if (a.out0) {
+#pragma unroll
+      for (int i = 0; i < BC / 8; ++i) {
+        uint4 o;
+        __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ob[j] = __floats2bfloat162_rn(y[8 * i + 2 * j], y[8 * i + 2 * j + 1]);
+        *reinterpret_cast<uint4*>(a.out0 + off + b + 8 * i) = o;
+      }
+    }
+    if (a.out1) {
+#pragma unroll
+      for (int i = 0; i < BC / 8; ++i) {
+        uint4 o;
+        __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          ob[j] = __floats2bfloat162_rn(gsilu(y[8 * i + 2 * j], hg), gsilu(y[8 * i + 2 * j + 1], hg));
+        *reinterpret_cast<uint4*>(a.out1 + off + b + 8 * i) = o;
+      }
+    }
+  }
+}
+
 template <int N>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_w, const ConvArgs args) {
@@ -208,10 +311,13 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* s_scale = reinterpret_cast<float*>(tmem_slot + 4);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kchunks = args.kchunks_a + args.kchunks_b;
   const int kblocks = args.taps * kchunks;
+  if (args.scale && threadIdx.x >= 64)
+    for (int c = threadIdx.x - 64; c < N; c += 256) s_scale[c] = args.scale[c];
 
   if (warp == 0 && lane == 0) {
     prefetch_map(&map_a);
@@ -223,7 +329,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 128);
+      mbar_init(&tempty[s], 256);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -309,9 +415,12 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ---------------- epilogue (warps 2..5) ----------------
+    // ---------------- epilogue (warps 2..9) ----------------
     const int quarter = warp & 3;  // TMEM lanes [32*quarter, +32) belong to this warp
+    const int half = (warp - 2) >> 2;
     const int m = quarter * 32 + lane;
+    constexpr int NC = N >= 64 ? N / 2 : N;
+    const float* sc = args.scale ? s_scale : nullptr;
     int it = 0;
     for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
@@ -319,12 +428,7 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const int64_t p = (int64_t)tile * 128 + m;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * N;
-#pragma unroll 1
-      for (int c0 = 0; c0 < N; c0 += 16) {
-        float v[16];
-        tmem_ld16(taddr + c0, v);
-        epi_chunk(args, p, c0, v);
-      }
+      if (N >= 64 || half == 0) epi_span<NC>(args, sc, p, half * NC, taddr);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
@@ -392,9 +496,12 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* bfull = bars + 9;      // [b_stages]
   uint64_t* bempty = bfull + ha.b_stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + ha.b_stages);
+  float* s_scale = reinterpret_cast<float*>(tmem_slot + 4);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles_per_img = ha.tiles_x * ha.tiles_y;
+  if (args.scale && threadIdx.x >= 64)
+    for (int c = threadIdx.x - 64; c < N; c += 256) s_scale[c] = args.scale[c];
 
   if (warp == 0 && lane == 0) {
     prefetch_map(&map_a);
@@ -525,17 +632,12 @@ __global__ void __launch_bounds__(320, 1)
       const int ty = r / ha.tiles_x;
       const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
       const int row = ROWS == 2 ? grp : 0;
-      const int cbeg = ROWS == 2 ? 0 : grp * (N / 2);
-      const int cend = ROWS == 2 ? N : cbeg + N / 2;
+      constexpr int NC = ROWS == 2 ? N : N / 2;
+      const int cbeg = ROWS == 2 ? 0 : grp * NC;
       const int64_t p = ((int64_t)img * args.h + y0 + row) * args.w + x0 + m;
       const uint32_t taddr =
           tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N + row * N;
-#pragma unroll 1
-      for (int c0 = cbeg; c0 < cend; c0 += 16) {
-        float v[16];
-        tmem_ld16(taddr + c0, v);
-        epi_chunk(args, p, c0, v);
-      }
+      epi_span<NC>(args, args.scale ? s_scale : nullptr, p, cbeg, taddr);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
@@ -831,7 +933,7 @@ static int launch_conv_tc(const ig_conv_params_t* p, const ConvArgs& a, cudaStre
     attr_set = true;
   }
   const int grid = a.num_tiles < kNumSMs ? a.num_tiles : kNumSMs;
-  { conv_tc_kernel<N><<<grid, 192, Cfg::SMEM, st>>>(ma, mb, mw, a); note_launch(); }
+  { conv_tc_kernel<N><<<grid, 320, Cfg::SMEM, st>>>(ma, mb, mw, a); note_launch(); }
   return cuda_check("ig_conv_tc");
 }
 
@@ -853,7 +955,7 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
   ha.c.num_tiles = p->n * ha.tiles_x * ha.tiles_y;
   const int kchunks = a.kchunks_a + a.kchunks_b;
   const int wbytes = 9 * kchunks * Cfg::B_BYTES;
-  const int fixed = 1024 + 2 * Cfg::HALO_BYTES + 512;
+  const int fixed = 1024 + 2 * Cfg::HALO_BYTES + 512 + 1024;
   int smem;
   if (fixed + wbytes <= Cfg::BUDGET) {
     ha.resident = 1;

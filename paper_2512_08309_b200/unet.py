@@ -255,14 +255,13 @@ class UNetDevice:
         n, h, w, ca = a.shape
         cb = 0 if b is None else b.shape[3]
         assert ca + cb == cs.cin, (name, ca, cb, cs.cin)
-        one, zero = self._vec1(cs.cout_pad)
-        scale = self._scale(name, sigma) if cs.modulated else one
+        scale = self._scale(name, sigma) if cs.modulated else None   # None: identity
         o0 = torch.empty((n, h, w, cs.cout_pad), dtype=torch.bfloat16, device=a.device) \
             if out0 else None
         o1 = torch.empty((n, h, w, cs.cout_pad), dtype=torch.bfloat16, device=a.device) \
             if out1 else None
         p = ConvParams(n, h, w, ca, cb, cs.cout_pad, cs.taps, a.data_ptr(), dev.ptr(b),
-                       self.w[name].data_ptr(), scale.data_ptr(), zero.data_ptr(), dev.ptr(res),
+                       self.w[name].data_ptr(), dev.ptr(scale), None, dev.ptr(res),
                        res_ab[0], res_ab[1], MP_SILU_GAIN, dev.ptr(o0), dev.ptr(o1))
         conv_launch(p)
         return o0, o1
