@@ -651,6 +651,217 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ---------------------------------------------------------------------------
+// ig_conv_tc, row-ring variant (3x3, one 64-channel input chunk, width a
+// multiple of 128).  Each CTA walks a contiguous strip of tiles ordered
+// (image, column, row-pair), so consecutive tiles are vertically adjacent and
+// share ROWS+2-ROWS = 2 input rows.  Input rows (130 px x 64 ch, one TMA box
+// each, zero fill outside the image) stream through an RING-slot FIFO: every
+// input row is fetched once per CTA column pass and the producer runs up to
+// ~2 tiles ahead of the MMAs.  The A operand of (row r, tap dy,dx) is the
+// 128-row view of ring slot (window row r+dy) starting at pixel dx.
+template <int N, int ROWS>
+struct RowCfg {
+  static constexpr int ROW_TX = 130 * 128;
+  static constexpr int ROW_BYTES = (ROW_TX + 1023) / 1024 * 1024;
+  static constexpr int WIN = ROWS + 2;
+  static constexpr int RING = 8;
+  static constexpr int B_BYTES = N * 128;
+  static constexpr int TMEM_COLS = (2 * ROWS * N <= 128) ? 128 : (2 * ROWS * N <= 256) ? 256 : 512;
+  static constexpr int BUDGET = 220 * 1024;
+};
+
+struct RowArgs {
+  ConvArgs c;
+  int resident, b_stages, tiles_x, tiles_y;
+};
+
+struct TileCoord {
+  int img, x0, y0;
+  bool cont;  // vertically continues the previous tile of this CTA
+};
+
+__device__ __forceinline__ TileCoord tile_coord(int g, int first, int tx_n, int ty_n, int rows) {
+  const int per_img = tx_n * ty_n;
+  const int img = g / per_img;
+  const int rem = g - img * per_img;
+  const int tx = rem / ty_n, ty = rem - (rem / ty_n) * ty_n;
+  return {img, tx * 128, ty * rows, g > first && ty > 0};
+}
+
+template <int N, int ROWS>
+__global__ void __launch_bounds__(320, 1)
+    conv_rows_kernel(const __grid_constant__ CUtensorMap map_a,
+                     const __grid_constant__ CUtensorMap map_w, const RowArgs ra) {
+  using Cfg = RowCfg<N, ROWS>;
+  const ConvArgs args = ra.c;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int nb = ra.resident ? 9 : ra.b_stages;
+  uint8_t* sR = smem;
+  uint8_t* sB = smem + Cfg::RING * Cfg::ROW_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + nb * Cfg::B_BYTES);
+  uint64_t* rfull = bars;                  // [RING]
+  uint64_t* rempty = bars + Cfg::RING;     // [RING]
+  uint64_t* tfull = rempty + Cfg::RING;    // [2]
+  uint64_t* tempty = tfull + 2;            // [2]
+  uint64_t* wfull = tempty + 2;            // [1]
+  uint64_t* bfull = wfull + 1;             // [b_stages]
+  uint64_t* bempty = bfull + ra.b_stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + ra.b_stages);
+  float* s_scale = reinterpret_cast<float*>(tmem_slot + 4);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int T = args.num_tiles;
+  const int first = (int)((int64_t)blockIdx.x * T / gridDim.x);
+  const int last = (int)((int64_t)(blockIdx.x + 1) * T / gridDim.x);
+  if (args.scale && threadIdx.x >= 64)
+    for (int c = threadIdx.x - 64; c < N; c += 256) s_scale[c] = args.scale[c];
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_a);
+    prefetch_map(&map_w);
+    for (int s = 0; s < Cfg::RING; ++s) {
+      mbar_init(&rfull[s], 1);
+      mbar_init(&rempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 256);
+    }
+    mbar_init(wfull, 1);
+    for (int s = 0; s < ra.b_stages; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      if (ra.resident) {
+        mbar_expect_tx(wfull, (uint32_t)(9 * Cfg::B_BYTES));
+        for (int t = 0; t < 9; ++t)
+          tma_load_2d(sB + t * Cfg::B_BYTES, &map_w, wfull, t * args.ca, 0);
+      }
+      int seq = 0;   // row sequence number of the next row to load
+      int bs = 0;
+      uint32_t bph = 0;
+      for (int g = first; g < last; ++g) {
+        const TileCoord tc = tile_coord(g, first, ra.tiles_x, ra.tiles_y, ROWS);
+        const int r0 = tc.cont ? 2 : 0;           // window rows already resident
+        for (int wr = r0; wr < Cfg::WIN; ++wr, ++seq) {
+          const int slot = seq % Cfg::RING;
+          mbar_wait(&rempty[slot], ((seq / Cfg::RING) & 1) ^ 1);
+          mbar_expect_tx(&rfull[slot], Cfg::ROW_TX);
+          tma_load_4d(sR + slot * Cfg::ROW_BYTES, &map_a, &rfull[slot], 0, tc.x0 - 1,
+                      tc.y0 - 1 + wr, tc.img);
+        }
+        if (!ra.resident) {
+          for (int tap = 0; tap < 9; ++tap) {
+            mbar_wait(&bempty[bs], bph ^ 1);
+            mbar_expect_tx(&bfull[bs], Cfg::B_BYTES);
+            tma_load_2d(sB + bs * Cfg::B_BYTES, &map_w, &bfull[bs], tap * args.ca, 0);
+            if (++bs == ra.b_stages) { bs = 0; bph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc = idesc_bf16(128, N);
+      if (ra.resident) mbar_wait(wfull, 0);
+      int wbase = 0;     // row sequence number of the current window's first row
+      int loaded = 0;    // rows whose "full" barrier we have waited on
+      int bs = 0;
+      uint32_t bph = 0;
+      int it = 0;
+      for (int g = first; g < last; ++g, ++it) {
+        const TileCoord tc = tile_coord(g, first, ra.tiles_x, ra.tiles_y, ROWS);
+        if (g > first) wbase += tc.cont ? ROWS : Cfg::WIN;
+        for (; loaded < wbase + Cfg::WIN; ++loaded)
+          mbar_wait(&rfull[loaded % Cfg::RING], (loaded / Cfg::RING) & 1);
+        tc_fence_after();
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + acc * ROWS * N;
+        for (int tap = 0; tap < 9; ++tap) {
+          const int dy = tap / 3, dx = tap % 3;
+          uint32_t baddr;
+          if (ra.resident) {
+            baddr = smem_u32(sB + tap * Cfg::B_BYTES);
+          } else {
+            mbar_wait(&bfull[bs], bph);
+            tc_fence_after();
+            baddr = smem_u32(sB + bs * Cfg::B_BYTES);
+          }
+          const uint64_t bdesc = smem_desc_sw128(baddr);
+#pragma unroll
+          for (int rr = 0; rr < ROWS; ++rr) {
+            const int slot = (wbase + rr + dy) % Cfg::RING;
+            const uint64_t adesc = smem_desc_sw128(smem_u32(sR + slot * Cfg::ROW_BYTES) + dx * 128);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma(d0 + rr * N, adesc + 2 * k, bdesc + 2 * k, idesc, (tap | k) ? 1u : 0u);
+          }
+          if (!ra.resident) {
+            tc_commit(&bempty[bs]);
+            if (++bs == ra.b_stages) { bs = 0; bph ^= 1; }
+          }
+        }
+        tc_commit(&tfull[acc]);
+        // release the rows the next tile of this CTA does not reuse
+        bool next_cont = false;
+        if (g + 1 < last) next_cont = tile_coord(g + 1, first, ra.tiles_x, ra.tiles_y, ROWS).cont;
+        const int nrel = next_cont ? ROWS : Cfg::WIN;
+        for (int q = 0; q < nrel; ++q) tc_commit(&rempty[(wbase + q) % Cfg::RING]);
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..9) ----------------
+    const int quarter = warp & 3;
+    const int grp = (warp - 2) >> 2;
+    const int m = quarter * 32 + lane;
+    int it = 0;
+    for (int g = first; g < last; ++g, ++it) {
+      const int acc = it & 1;
+      const TileCoord tc = tile_coord(g, first, ra.tiles_x, ra.tiles_y, ROWS);
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int row = ROWS == 2 ? grp : 0;
+      constexpr int NC = ROWS == 2 ? N : N / 2;
+      const int cbeg = ROWS == 2 ? 0 : grp * NC;
+      const int64_t p = ((int64_t)tc.img * args.h + tc.y0 + row) * args.w + tc.x0 + m;
+      const uint32_t taddr =
+          tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N + row * N;
+      epi_span<NC>(args, args.scale ? s_scale : nullptr, p, cbeg, taddr);
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(Cfg::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // CUDA-core reference convolution (same contract; test cross-check)
 __global__ void conv_simt_kernel(ConvArgs a, const __nv_bfloat16* __restrict__ act_a,
                                  const __nv_bfloat16* __restrict__ act_b,
@@ -938,6 +1149,49 @@ static int launch_conv_tc(const ig_conv_params_t* p, const ConvArgs& a, cudaStre
 }
 
 template <int N, int ROWS>
+static int launch_conv_rows(const ig_conv_params_t* p, const ConvArgs& a, cudaStream_t st) {
+  using Cfg = RowCfg<N, ROWS>;
+  CUtensorMap ma, mw;
+  if (make_act_map_box(&ma, p->act_a, p->n, p->h, p->w, p->ca, 130, 1) != IG_OK ||
+      make_w_map(&mw, p->wgt, 9 * p->ca, p->cout) != IG_OK) {
+    set_error("ig_conv_tc(rows): cuTensorMapEncodeTiled failed");
+    return IG_ERR_CUDA;
+  }
+  RowArgs ra;
+  ra.c = a;
+  ra.tiles_x = p->w / 128;
+  ra.tiles_y = p->h / ROWS;
+  ra.c.num_tiles = p->n * ra.tiles_x * ra.tiles_y;
+  const int wbytes = 9 * Cfg::B_BYTES;
+  const int fixed = 1024 + Cfg::RING * Cfg::ROW_BYTES + 1024 + 512;
+  int smem;
+  if (fixed + wbytes <= Cfg::BUDGET) {
+    ra.resident = 1;
+    ra.b_stages = 1;
+    smem = fixed + wbytes;
+  } else {
+    ra.resident = 0;
+    int stages = (Cfg::BUDGET - fixed) / Cfg::B_BYTES;
+    if (stages > 8) stages = 8;
+    if (stages < 2) {
+      set_error("ig_conv_tc(rows): no room for the weight ring");
+      return IG_ERR_UNSUPPORTED;
+    }
+    ra.b_stages = stages;
+    smem = fixed + stages * Cfg::B_BYTES;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(conv_rows_kernel<N, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    attr = true;
+  }
+  const int grid = ra.c.num_tiles < kNumSMs ? ra.c.num_tiles : kNumSMs;
+  { conv_rows_kernel<N, ROWS><<<grid, 320, smem, st>>>(ma, mw, ra); note_launch(); }
+  return cuda_check("ig_conv_tc(rows)");
+}
+
+template <int N, int ROWS>
 static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaStream_t st) {
   using Cfg = HaloCfg<N, ROWS>;
   CUtensorMap ma, mb, mw;
@@ -983,7 +1237,7 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
   return cuda_check("ig_conv_tc(halo)");
 }
 
-static bool g_force_v1 = false;
+static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring
 
 static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   IG_REQUIRE(p && p->n > 0 && p->h > 0 && p->w > 0, "conv: empty problem");
@@ -1018,9 +1272,10 @@ extern "C" {
 
 size_t ig_conv_workspace_bytes(void) { return 0; }
 
-// 1: route every convolution through the per-tap kernel (tests / A-B timing)
-int ig_conv_set_variant(int force_per_tap) {
-  g_force_v1 = force_per_tap != 0;
+// 0: automatic; 1: per-tap kernel only; 2: halo kernel instead of the row
+// ring (tests / A-B timing)
+int ig_conv_set_variant(int variant) {
+  g_variant = variant;
   return IG_OK;
 }
 
@@ -1034,7 +1289,24 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
     return IG_ERR_CUDA;
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
-  const bool halo = p->taps == 9 && p->w % 128 == 0 && !g_force_v1;
+  const bool halo = p->taps == 9 && p->w % 128 == 0 && g_variant != 1;
+  if (halo && p->cb == 0 && p->ca == 64 && g_variant != 2) {
+    if (p->cout <= 128 && p->h % 2 == 0) {
+      switch (p->cout) {
+        case 16: return launch_conv_rows<16, 2>(p, a, st);
+        case 32: return launch_conv_rows<32, 2>(p, a, st);
+        case 64: return launch_conv_rows<64, 2>(p, a, st);
+        case 128: return launch_conv_rows<128, 2>(p, a, st);
+        default: break;
+      }
+    } else {
+      switch (p->cout) {
+        case 192: return launch_conv_rows<192, 1>(p, a, st);
+        case 256: return launch_conv_rows<256, 1>(p, a, st);
+        default: break;
+      }
+    }
+  }
   if (halo && p->cout <= 128 && p->h % 2 == 0) {
     switch (p->cout) {
       case 16: return launch_conv_halo<16, 2>(p, a, st);

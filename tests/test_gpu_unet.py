@@ -56,10 +56,14 @@ def _conv_ref(a, b, w, cout, taps, scale, res, ra, rb, gain):
     (1, 16, 128, 64, 0, 256, 9),
     (1, 8, 256, 128, 64, 64, 9),
     (1, 4, 128, 64, 0, 16, 9),
+    # row-ring shapes (one 64-channel input chunk): several CTAs per image column
+    (3, 96, 256, 64, 0, 64, 9),
+    (2, 34, 128, 64, 0, 128, 9),
+    (1, 40, 128, 64, 0, 256, 9),
 ])
-@pytest.mark.parametrize("variant", ["auto", "per_tap"])
+@pytest.mark.parametrize("variant", ["auto", "per_tap", "halo"])
 def test_conv_tc_matches_torch(n, h, w, ca, cb, cout, taps, variant):
-    check(lib().ig_conv_set_variant(1 if variant == "per_tap" else 0))
+    check(lib().ig_conv_set_variant({"auto": 0, "per_tap": 1, "halo": 2}[variant]))
     try:
         _run_conv_case(n, h, w, ca, cb, cout, taps)
     finally:
