@@ -72,6 +72,19 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
+// one elected lane of a converged warp (the MMA warp runs its loop with all
+// 32 lanes so descriptors stay warp-uniform; only the issue is elected)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.u32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -385,8 +398,8 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
+    {
+      // ---------------- MMA issuer: whole warp, elected issue ----------------
       constexpr uint32_t idesc = idesc_bf16(128, N);
       int stage = 0;
       uint32_t phase = 0;
@@ -402,16 +415,20 @@ __global__ void __launch_bounds__(320, 1)
           tc_fence_after();
           const uint64_t adesc = smem_desc_sw128(smem_u32(sA + stage * Cfg::A_BYTES));
           const uint64_t bdesc = smem_desc_sw128(smem_u32(sB + stage * Cfg::B_BYTES));
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)  // K = 16 per MMA: +32 B in the 128 B swizzled row
-            tc_mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) ? 1u : 0u);
-          tc_commit(&empty[stage]);
+            for (int k = 0; k < 4; ++k)  // K = 16 per MMA: +32 B in the 128 B swizzled row
+              tc_mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) ? 1u : 0u);
+            tc_commit(&empty[stage]);
+          }
+          __syncwarp();
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);
+        if (elect_one()) tc_commit(&tfull[acc]);
+        __syncwarp();
       }
     }
   } else {
@@ -571,8 +588,8 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
+    {
+      // ---------------- MMA issuer: whole warp, elected issue ----------------
       constexpr uint32_t idesc = idesc_bf16(128, N);
       if (ha.resident) mbar_wait(wfull, 0);
       int hs = 0, bs = 0;
@@ -598,23 +615,28 @@ __global__ void __launch_bounds__(320, 1)
               baddr = smem_u32(sB + bs * Cfg::B_BYTES);
             }
             const uint64_t bdesc = smem_desc_sw128(baddr);
+            if (elect_one()) {
 #pragma unroll
-            for (int rr = 0; rr < ROWS; ++rr) {
-              const uint64_t adesc = smem_desc_sw128(hbase + ((rr + dy) * 130 + dx) * 128);
+              for (int rr = 0; rr < ROWS; ++rr) {
+                const uint64_t adesc = smem_desc_sw128(hbase + ((rr + dy) * 130 + dx) * 128);
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                tc_mma(d0 + rr * N, adesc + 2 * k, bdesc + 2 * k, idesc,
-                       (kc | tap | k) ? 1u : 0u);
+                for (int k = 0; k < 4; ++k)
+                  tc_mma(d0 + rr * N, adesc + 2 * k, bdesc + 2 * k, idesc,
+                         (kc | tap | k) ? 1u : 0u);
+              }
+              if (!ha.resident) tc_commit(&bempty[bs]);
             }
+            __syncwarp();
             if (!ha.resident) {
-              tc_commit(&bempty[bs]);
               if (++bs == ha.b_stages) { bs = 0; bph ^= 1; }
             }
           }
-          tc_commit(&hempty[hs]);
+          if (elect_one()) tc_commit(&hempty[hs]);
+          __syncwarp();
           if (++hs == 2) { hs = 0; hph ^= 1; }
         }
-        tc_commit(&tfull[acc]);
+        if (elect_one()) tc_commit(&tfull[acc]);
+        __syncwarp();
       }
     }
   } else {
@@ -780,8 +802,8 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
+    {
+      // ---------------- MMA issuer: whole warp, elected issue ----------------
       constexpr uint32_t idesc = idesc_bf16(128, N);
       if (ra.resident) mbar_wait(wfull, 0);
       int wbase = 0;     // row sequence number of the current window's first row
@@ -793,7 +815,7 @@ __global__ void __launch_bounds__(320, 1)
         const TileCoord tc = tile_coord(g, first, ra.tiles_x, ra.tiles_y, ROWS);
         if (g > first) wbase += tc.cont ? ROWS : Cfg::WIN;
         for (; loaded < wbase + Cfg::WIN; ++loaded)
-          mbar_wait(&rfull[loaded % Cfg::RING], (loaded / Cfg::RING) & 1);
+          mbar_wait(&rfull[loaded & (Cfg::RING - 1)], (loaded / Cfg::RING) & 1);
         tc_fence_after();
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
@@ -810,25 +832,32 @@ __global__ void __launch_bounds__(320, 1)
             baddr = smem_u32(sB + bs * Cfg::B_BYTES);
           }
           const uint64_t bdesc = smem_desc_sw128(baddr);
+          if (elect_one()) {
 #pragma unroll
-          for (int rr = 0; rr < ROWS; ++rr) {
-            const int slot = (wbase + rr + dy) % Cfg::RING;
-            const uint64_t adesc = smem_desc_sw128(smem_u32(sR + slot * Cfg::ROW_BYTES) + dx * 128);
+            for (int rr = 0; rr < ROWS; ++rr) {
+              const int slot = (wbase + rr + dy) & (Cfg::RING - 1);
+              const uint64_t adesc =
+                  smem_desc_sw128(smem_u32(sR + slot * Cfg::ROW_BYTES) + dx * 128);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc_mma(d0 + rr * N, adesc + 2 * k, bdesc + 2 * k, idesc, (tap | k) ? 1u : 0u);
+              for (int k = 0; k < 4; ++k)
+                tc_mma(d0 + rr * N, adesc + 2 * k, bdesc + 2 * k, idesc, (tap | k) ? 1u : 0u);
+            }
+            if (!ra.resident) tc_commit(&bempty[bs]);
           }
+          __syncwarp();
           if (!ra.resident) {
-            tc_commit(&bempty[bs]);
             if (++bs == ra.b_stages) { bs = 0; bph ^= 1; }
           }
         }
-        tc_commit(&tfull[acc]);
         // release the rows the next tile of this CTA does not reuse
         bool next_cont = false;
         if (g + 1 < last) next_cont = tile_coord(g + 1, first, ra.tiles_x, ra.tiles_y, ROWS).cont;
         const int nrel = next_cont ? ROWS : Cfg::WIN;
-        for (int q = 0; q < nrel; ++q) tc_commit(&rempty[(wbase + q) % Cfg::RING]);
+        if (elect_one()) {
+          tc_commit(&tfull[acc]);
+          for (int q = 0; q < nrel; ++q) tc_commit(&rempty[(wbase + q) & (Cfg::RING - 1)]);
+        }
+        __syncwarp();
       }
     }
   } else {
