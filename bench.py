@@ -107,12 +107,12 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def _conv_flops_per_step(ucfg):
+def _conv_flops_per_step(ucfg, side=REGION):
     from paper_2512_08309_b200.unet import conv_flops
     from paper_2512_08309_b200.grid import Region, WindowLayout, region_union_cover, \
         windows_overlapping
     lay = WindowLayout(WINDOW, STRIDE)
-    r0 = Region(0, 0, REGION, REGION)
+    r0 = Region(0, 0, side, side)
     n0 = len(windows_overlapping(lay, r0))
     n1 = len(windows_overlapping(lay, region_union_cover(lay, r0)))
     per_win = conv_flops(ucfg, WINDOW, WINDOW)
@@ -146,8 +146,23 @@ def run_gpu(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    sharded = args.workload == "cfg5"
+    if sharded:
+        from paper_2512_08309_b200 import shard
+        big = args.region if args.region else 16384
+
     def one_step(step, e2e):
         st = ig.SamplerState(scfg, ig.TileStore())
+        if sharded:
+            # one big region split in strips over the ranks, owner-computes
+            # windows + NCCL halo exchange of boundary Phi (bitwise = 1 GPU)
+            R = ig.Region(big * step - 10 ** 6, 10 ** 5, big, big)
+            p = shard.plan([WindowLayout(WINDOW, STRIDE)] * T, R, world)
+            xch = shard.p2p_exchange(dist, torch.device("cuda", local), (1, WINDOW, WINDOW),
+                                     torch.float32) if world > 1 else \
+                (lambda t, out, exp: {})
+            out = shard.run(p, rank, shard.StoreExecutor(st), xch)
+            return out.cpu().numpy() if e2e else out
         r = _region(step, rank, world)
         if e2e:
             return st.query(0, r)           # public API: numpy result (D2H inside)
@@ -203,10 +218,12 @@ def run_gpu(args):
         if world > 1:
             dist.destroy_process_group()
         return
-    px_total = REGION * REGION * world * args.steps
+    px_total = (big * big if sharded else REGION * REGION * world) * args.steps
     value = px_total * KM2_PER_PX / (ms_max / 1e3)
     e2e_value = px_total * KM2_PER_PX / (e2e_ms / 1e3)
-    calls, f_win, f_win_pad = _conv_flops_per_step(ucfg)
+    calls, f_win, f_win_pad = _conv_flops_per_step(ucfg, big if sharded else REGION)
+    if sharded:
+        calls = calls / world            # rank 0's share of the owner-computed windows
     peak_tf, peak_hbm, peak_src = _peaks()
     conv_flops_total = f_win * calls * args.steps
     achieved = conv_flops_total / (conv_ms / 1e3) / 1e12 if conv_ms else None
@@ -224,7 +241,7 @@ def run_gpu(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms_max / args.steps, 3),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (seed-0 coordinate noise; random-init UNet weights, torch.manual_seed(0))",
@@ -367,6 +384,10 @@ def main():
     ap.add_argument("--base", type=int, default=64)
     ap.add_argument("--mults", type=int, nargs="+", default=[1, 2, 2, 4])
     ap.add_argument("--blocks", type=int, default=1)
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5"],
+                    help="cfg2: one 2048^2 region per GPU per step (weak scaling); cfg5: one "
+                         "16384^2 region per step sharded over all GPUs (strong scaling)")
+    ap.add_argument("--region", type=int, default=0, help="cfg5 region side override")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--ref-region", type=int, default=128)

@@ -1,0 +1,218 @@
+"""Spatial sharding of one large region query over ranks.
+
+The world plane partitions naturally: every pixel of every step image is a
+pure function of (seed, coordinates), and its value is the canonical (j, i)
+ordered sum over the windows covering it.  A region R is split into
+horizontal output strips, one per rank.  Each step's window *rows* are then
+owned by exactly one rank (owner-computes: no window is evaluated twice), and
+before a step's blend every rank receives, from its neighbours, the Phi
+outputs of the boundary window rows it needs but does not own (the halo
+exchange, NCCL send/recv over NVLink).  Each rank then blends its strip with
+the full canonical window set, so the gathered result is bitwise equal to the
+single-GPU query -- no all-reduce (partial sums would change the float order).
+
+The planner is pure host logic; execution goes through an executor with
+three operations (``generate``, ``inject``, ``query``) so the same plan runs
+on the device tile store (``StoreExecutor``) and, in the CPU tests, on the
+numpy oracle.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .grid import Region, WindowLayout, index_box, region_union_cover
+
+
+@dataclass
+class StepPlan:
+    rows_needed: dict[int, tuple[int, int]]      # rank -> inclusive window-row range
+    owner: dict[int, int]                          # window row j -> owning rank
+    cols: tuple[int, int]                          # inclusive window-column range (all ranks)
+    sends: dict[tuple[int, int], list[int]] = field(default_factory=dict)  # (src, dst) -> rows
+
+
+@dataclass
+class ShardPlan:
+    region: Region
+    world: int
+    strips: list[Region]
+    steps: list[StepPlan]                          # index t = sampler step (0 = final)
+
+    def owned(self, t: int, rank: int) -> list[int]:
+        return sorted(j for j, r in self.steps[t].owner.items() if r == rank)
+
+    def windows(self, t: int, rows) -> list[tuple[int, int]]:
+        i_lo, i_hi = self.steps[t].cols
+        return [(i, j) for j in sorted(rows) for i in range(i_lo, i_hi + 1)]
+
+
+def split_rows(r: Region, world: int, align: int = 1) -> list[Region]:
+    """Balanced horizontal strips of r (boundaries on multiples of `align` rows
+    relative to r.y0 where possible)."""
+    h = r.height
+    cuts = [r.y0]
+    for k in range(1, world):
+        y = r.y0 + (h * k) // world
+        y = r.y0 + ((y - r.y0) // align) * align
+        cuts.append(max(y, cuts[-1] + 1))
+    cuts.append(r.y1)
+    return [Region(r.x0, cuts[k], r.width, cuts[k + 1] - cuts[k]) for k in range(world)]
+
+
+def plan(layouts: list[WindowLayout], r: Region, world: int) -> ShardPlan:
+    """Owner-computes plan for query(0, r) of a `len(layouts)`-step sampler."""
+    T = len(layouts)
+    strips = split_rows(r, world, align=layouts[0].stride)
+    steps: list[StepPlan] = []
+    need = {k: strips[k] for k in range(world)}   # region each rank needs at step t
+    full = r
+    for t in range(T):
+        lay = layouts[t]
+        fi_lo, fi_hi, _, _ = index_box(lay, full)
+        rows_needed = {}
+        for k in range(world):
+            _, _, j_lo, j_hi = index_box(lay, need[k])
+            rows_needed[k] = (j_lo, j_hi)
+        # owner of a row: the lowest-numbered rank whose strip interior the
+        # row's first output line falls into; rows outside all strips go to
+        # the nearest rank.  Every needed row gets exactly one owner.
+        owner = {}
+        all_rows = sorted({j for k in range(world)
+                           for j in range(rows_needed[k][0], rows_needed[k][1] + 1)})
+        for j in all_rows:
+            y_mid = j * lay.stride + lay.offset[1] + lay.window // 2
+            cand = [k for k in range(world) if rows_needed[k][0] <= j <= rows_needed[k][1]]
+            best = min(cand, key=lambda k: (0 if strips[k].y0 <= y_mid < strips[k].y1 else 1,
+                                            abs(strips[k].y0 + strips[k].height // 2 - y_mid),
+                                            k))
+            owner[j] = best
+        sp = StepPlan(rows_needed=rows_needed, owner=owner, cols=(fi_lo, fi_hi))
+        for dst in range(world):
+            lo, hi = rows_needed[dst]
+            for j in range(lo, hi + 1):
+                src = owner[j]
+                if src != dst:
+                    sp.sends.setdefault((src, dst), []).append(j)
+        steps.append(sp)
+        # next step: each rank needs the union cover of its needed windows
+        nxt = {}
+        for k in range(world):
+            lo, hi = rows_needed[k]
+            box = Region(fi_lo * lay.stride + lay.offset[0], lo * lay.stride + lay.offset[1],
+                         (fi_hi - fi_lo) * lay.stride + lay.window,
+                         (hi - lo) * lay.stride + lay.window)
+            nxt[k] = box
+        need = nxt
+        full = region_union_cover(lay, full)
+    return ShardPlan(region=r, world=world, strips=strips, steps=steps)
+
+
+def run(plan_: ShardPlan, rank: int, executor, exchange):
+    """Execute the plan on one rank.
+
+    executor.generate(t, idxs) -> {idx: data}  (Phi of step-t windows, batched)
+    executor.inject(t, {idx: data})             (make received windows resident)
+    executor.query(region) -> step-0 image of the rank's strip
+    exchange(t, {dst: [data, ...]}, {src: n}) -> {src: [data, ...]}
+        moves packed window data; both sides derive the window order from the
+        plan, so only tensors travel.
+    Steps run deepest first (t = T-1 .. 0), as plan_rounds does.
+    """
+    T = len(plan_.steps)
+    for t in reversed(range(T)):
+        sp = plan_.steps[t]
+        mine = plan_.owned(t, rank)
+        produced = executor.generate(t, plan_.windows(t, mine)) if mine else {}
+        outgoing, expect = {}, {}
+        for (src, dst), rows in sorted(sp.sends.items()):
+            if src == rank:
+                outgoing[dst] = [produced[idx] for idx in plan_.windows(t, rows)]
+            if dst == rank:
+                expect[src] = plan_.windows(t, rows)
+        incoming = exchange(t, outgoing, {src: len(v) for src, v in expect.items()})
+        got = {}
+        for src, idxs in expect.items():
+            for idx, data in zip(idxs, incoming[src]):
+                got[idx] = data
+        if got:
+            executor.inject(t, got)
+    return executor.query(plan_.strips[rank])
+
+
+class StoreExecutor:
+    """Executor over a SamplerState on the device tile store."""
+
+    def __init__(self, state):
+        self.state = state
+        self.store = state.store
+
+    def generate(self, t, idxs):
+        return self.store.generate_windows(self.state.handles[t], idxs)
+
+    def inject(self, t, windows):
+        for idx, data in windows.items():
+            self.store.inject_window(self.state.handles[t], idx, data)
+
+    def query(self, region):
+        return self.state.query_device(0, region)
+
+
+def p2p_exchange(dist, device, window_shape, dtype):
+    """Halo exchange with torch.distributed point-to-point ops (NCCL over
+    NVLink on B200, gloo in the CPU tests): one packed (n, *window_shape)
+    tensor per (src, dst) pair, all sends/recvs of a step in one batch."""
+    import torch
+
+    def exchange(t, outgoing, expect):
+        ops, bufs = [], {}
+        for dst, items in sorted(outgoing.items()):
+            if items:
+                buf = torch.stack(list(items)).contiguous().to(device)
+                ops.append(dist.P2POp(dist.isend, buf, dst))
+        for src, n in sorted(expect.items()):
+            if n:
+                buf = torch.empty((n,) + tuple(window_shape), dtype=dtype, device=device)
+                bufs[src] = buf
+                ops.append(dist.P2POp(dist.irecv, buf, src))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return {src: list(buf.unbind(0)) for src, buf in bufs.items()}
+
+    return exchange
+
+
+def local_exchange(mailbox: dict, rank: int):
+    """In-process exchange used to emulate ranks sequentially (one GPU):
+    senders deposit, receivers collect (ranks must run in dependency order
+    per step -- run_emulated drives that)."""
+
+    def exchange(t, outgoing, expect):
+        for dst, items in outgoing.items():
+            mailbox[(t, rank, dst)] = items
+        return {src: mailbox[(t, src, rank)] for src in expect}
+
+    return exchange
+
+
+def run_emulated(plan_: ShardPlan, executors):
+    """Run every rank of a plan inside one process: per step, all ranks
+    generate their owned windows first, then exchange, then (after the last
+    step) query.  Returns the per-rank strip images."""
+    mailbox = {}
+    T = len(plan_.steps)
+    world = plan_.world
+    for t in reversed(range(T)):
+        sp = plan_.steps[t]
+        produced = {k: (executors[k].generate(t, plan_.windows(t, plan_.owned(t, k)))
+                        if plan_.owned(t, k) else {}) for k in range(world)}
+        for k in range(world):
+            got = {}
+            for (src, dst), rows in sp.sends.items():
+                if dst == k:
+                    for idx in plan_.windows(t, rows):
+                        got[idx] = produced[src][idx]
+            if got:
+                executors[k].inject(t, got)
+    return [executors[k].query(plan_.strips[k]) for k in range(world)]

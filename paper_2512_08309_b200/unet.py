@@ -374,8 +374,6 @@ def unet_phi_batch(cfg: UNetConfig, src: torch.Tensor, src_region: Region | None
     C = cfg.data_channels
     sigma = cfg.sigma_for(outer_step, steps)
     c_skip, c_out, c_in, _ = precond(cfg, sigma)
-    x_in = torch.empty((n, win, win, cfg.cin_pad), dtype=torch.bfloat16, device=src.device)
-    x_noisy = torch.empty((n, C, win, win), dtype=torch.float32, device=src.device)
     src32 = src if src.dtype == torch.float32 else src.to(torch.float32)
     batched = src_region is None
     sx0, sy0 = (0, 0) if batched else (src_region.x0, src_region.y0)
@@ -386,13 +384,27 @@ def unet_phi_batch(cfg: UNetConfig, src: torch.Tensor, src_region: Region | None
                  -1 if cond.mask_channel is None else cond.mask_channel, cond.seed)
     else:
         cargs = (None, 0, 0, 0, 0, 0, 1, -1, 0)
-    call("ig_unet_gather_input", src32.data_ptr(), int(batched), sx0, sy0, src32.shape[-1],
-         src32.shape[-2], C, wxy.data_ptr(), n, *cargs[:-1], cargs[-1] & ((1 << 64) - 1),
-         seed & ((1 << 64) - 1), STREAM_RENOISE + outer_step, float(sigma), float(c_in),
-         int(outer_step == steps), x_in.data_ptr(), win, cfg.cin_pad, cfg.in_planes(),
-         x_noisy.data_ptr(), dev.stream_ptr())
-    f = model.forward(x_in, sigma)
     phi = torch.empty((n, C, win, win), dtype=torch.float32, device=src.device)
-    call("ig_unet_output", f.data_ptr(), n, win, win, 16, x_noisy.data_ptr(), C, float(c_skip),
-         float(c_out), 0, phi.data_ptr(), dev.stream_ptr())
+    # windows are processed in chunks so activation memory stays bounded
+    # (~8 MB per window per live 64-channel tensor at 256^2); Phi of a window
+    # does not depend on its chunk (the kernels are batch invariant)
+    chunk = max(1, min(n, max_windows_per_forward(win)))
+    for k0 in range(0, n, chunk):
+        m = min(chunk, n - k0)
+        x_in = torch.empty((m, win, win, cfg.cin_pad), dtype=torch.bfloat16, device=src.device)
+        x_noisy = torch.empty((m, C, win, win), dtype=torch.float32, device=src.device)
+        sptr = src32[k0:k0 + m].data_ptr() if batched else src32.data_ptr()
+        call("ig_unet_gather_input", sptr, int(batched), sx0, sy0, src32.shape[-1],
+             src32.shape[-2], C, wxy[k0:k0 + m].data_ptr(), m, *cargs[:-1],
+             cargs[-1] & ((1 << 64) - 1), seed & ((1 << 64) - 1), STREAM_RENOISE + outer_step,
+             float(sigma), float(c_in), int(outer_step == steps), x_in.data_ptr(), win,
+             cfg.cin_pad, cfg.in_planes(), x_noisy.data_ptr(), dev.stream_ptr())
+        f = model.forward(x_in, sigma)
+        call("ig_unet_output", f.data_ptr(), m, win, win, 16, x_noisy.data_ptr(), C,
+             float(c_skip), float(c_out), 0, phi[k0:k0 + m].data_ptr(), dev.stream_ptr())
     return phi
+
+
+def max_windows_per_forward(win: int) -> int:
+    """Windows per UNet forward: ~3 GB per 64-channel activation tensor."""
+    return max(16, int(3.2e9 // (win * win * 64 * 2)))

@@ -1,0 +1,98 @@
+"""Multi-rank sharded query on CPU: the owner-computes plan and
+the halo-exchange protocol over torch.distributed (gloo, world size 2/3), with
+the numpy oracle as the compute backend.  Result must be bitwise equal to the
+single-process query and every window evaluated exactly once."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import port
+from paper_2512_08309_b200 import shard
+from paper_2512_08309_b200.grid import Region, WindowLayout, region_union_cover, \
+    windows_overlapping
+
+SPEC = dict(kind="shrink_smooth", radius=1, lambdas=[0.6, 0.4])
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _reference(steps, H, s, region, seed):
+    out, _ = port.Stage(steps, (H, s), SPEC, seed).run(
+        port.Box(region.x0, region.y0, region.width, region.height))
+    return out
+
+
+@pytest.mark.parametrize("steps,world", [(2, 2), (2, 3), (3, 4), (1, 2)])
+def test_plan_partitions_windows(steps, world):
+    lay = WindowLayout(16, 8)
+    r = Region(-37, 11, 70, 90)
+    p = shard.plan([lay] * steps, r, world)
+    need = r
+    for t in range(steps):
+        full = set(windows_overlapping(lay, need))
+        owned = [set(p.windows(t, p.owned(t, k))) for k in range(world)]
+        union = set().union(*owned)
+        assert union == full                               # same windows as 1 GPU
+        assert sum(len(o) for o in owned) == len(full)     # each exactly once
+        need = region_union_cover(lay, need)
+
+
+@pytest.mark.parametrize("steps,world", [(2, 2), (2, 4), (3, 3)])
+def test_emulated_ranks_bitwise(steps, world):
+    from tests.shard_helpers import PortExecutor
+    H, s, seed = 16, 8, 5
+    r = Region(-37, 11, 70, 90)
+    p = shard.plan([WindowLayout(H, s)] * steps, r, world)
+    ex = [PortExecutor(steps, H, s, SPEC, seed) for _ in range(world)]
+    strips = shard.run_emulated(p, ex)
+    got = np.concatenate(strips, axis=1)
+    want = _reference(steps, H, s, r, seed)
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def _worker(rank, world, port_, steps, H, s, seed, region, q):
+    from tests.shard_helpers import PortExecutor
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = shard.plan([WindowLayout(H, s)] * steps, region, world)
+        ex = PortExecutor(steps, H, s, SPEC, seed)
+        xch = shard.p2p_exchange(dist, torch.device("cpu"), (1, H, H), torch.float32)
+        strip = shard.run(p, rank, ex, xch)
+        q.put((rank, strip, ex.generated))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_ranks_bitwise(world):
+    steps, H, s, seed = 2, 16, 8, 9
+    region = Region(5, -20, 64, 72)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_worker, args=(k, world, port_, steps, H, s, seed, region, q))
+             for k in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda x: x[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    got = np.concatenate([r[1] for r in res], axis=1)
+    want = _reference(steps, H, s, region, seed)
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+    lay = WindowLayout(H, s)
+    n1 = len(windows_overlapping(lay, region)) + len(
+        windows_overlapping(lay, region_union_cover(lay, region)))
+    assert sum(r[2] for r in res) == n1          # owner-computes: no redundant Phi
