@@ -54,7 +54,10 @@ def empty(shape, dtype) -> torch.Tensor:
 
 def upload(arr: np.ndarray) -> torch.Tensor:
     """Host array -> device tensor via pinned staging (async on the current stream)."""
-    t = torch.from_numpy(np.array(arr, copy=False, order="C"))
+    a = np.ascontiguousarray(arr)
+    if not a.flags.writeable:
+        a = a.copy()
+    t = torch.from_numpy(a)
     traffic["h2d"] += t.numel() * t.element_size()
     if t.numel() * t.element_size() >= 1 << 16:
         t = t.pin_memory()
