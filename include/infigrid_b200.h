@@ -166,6 +166,14 @@ typedef struct {
   float res_a, res_b, act_gain;
   void* out0;             /* bf16 or NULL */
   void* out1;             /* bf16 or NULL */
+  /* fused 1x1 skip GEMM accumulated into the same fp32 accumulator before the
+   * epilogue:  acc += sum_ci concat(skip_a, skip_b)[p][ci] * wskip[co][ci]
+   * (csa, csb multiples of 64; csa = 0 disables it).  Replaces a separate skip
+   * convolution + residual read for mp_sum blocks. */
+  int32_t csa, csb;
+  const void* skip_a;     /* [n][h][w][csa] bf16 */
+  const void* skip_b;     /* [n][h][w][csb] bf16 or NULL */
+  const void* wskip;      /* [cout][csa+csb] bf16 */
 } ig_conv_params_t;
 size_t ig_conv_workspace_bytes(void);
 /* 1: force the per-tap (v1) kernel for every conv; 0: halo kernel where it applies */

@@ -29,7 +29,8 @@ class ConvParams(ctypes.Structure):
     _fields_ = [("n", I32), ("h", I32), ("w", I32), ("ca", I32), ("cb", I32), ("cout", I32),
                 ("taps", I32), ("act_a", V), ("act_b", V), ("wgt", V), ("scale", V),
                 ("bias", V), ("res", V), ("res_a", F32), ("res_b", F32), ("act_gain", F32),
-                ("out0", V), ("out1", V)]
+                ("out0", V), ("out1", V), ("csa", I32), ("csb", I32), ("skip_a", V),
+                ("skip_b", V), ("wskip", V)]
 
 
 # name -> argtypes (every function returns int32 status unless listed in _RESTYPES)

@@ -155,6 +155,10 @@ __device__ __forceinline__ float silu_f(float y) { return gsilu(y, 0.5f); }
 struct ConvArgs {
   int n, h, w, ca, cb, cout, taps;
   int bw, bh, tiles_per_img, num_tiles, kchunks_a, kchunks_b;
+  int kskip_a, kskip_b;   // 64-channel chunks of the fused 1x1 skip GEMM
+  const __nv_bfloat16* skip_a;
+  const __nv_bfloat16* skip_b;
+  const __nv_bfloat16* wskip;
   const float* scale;
   const float* bias;
   const __nv_bfloat16* res;
@@ -312,7 +316,10 @@ template <int N>
 __global__ void __launch_bounds__(320, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
-                   const __grid_constant__ CUtensorMap map_w, const ConvArgs args) {
+                   const __grid_constant__ CUtensorMap map_w,
+                   const __grid_constant__ CUtensorMap map_sa,
+                   const __grid_constant__ CUtensorMap map_sb,
+                   const __grid_constant__ CUtensorMap map_ws, const ConvArgs args) {
   using Cfg = ConvCfg<N>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -328,7 +335,8 @@ __global__ void __launch_bounds__(320, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kchunks = args.kchunks_a + args.kchunks_b;
-  const int kblocks = args.taps * kchunks;
+  const int kmain = args.taps * kchunks;
+  const int kblocks = kmain + args.kskip_a + args.kskip_b;  // + fused 1x1 skip GEMM
   if (args.scale && threadIdx.x >= 64)
     for (int c = threadIdx.x - 64; c < N; c += 256) s_scale[c] = args.scale[c];
 
@@ -376,20 +384,29 @@ __global__ void __launch_bounds__(320, 1)
           x0 = 0;
         }
         for (int kb = 0; kb < kblocks; ++kb) {
-          const int tap = kb / kchunks;
-          const int kc = kb - tap * kchunks;
-          const int dy = args.taps == 9 ? tap / 3 - 1 : 0;
-          const int dx = args.taps == 9 ? tap % 3 - 1 : 0;
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], Cfg::STAGE);
           uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
-          if (kc < args.kchunks_a)
-            tma_load_4d(a_dst, &map_a, &full[stage], kc * 64, x0 + dx, y0 + dy, img);
-          else
-            tma_load_4d(a_dst, &map_b, &full[stage], (kc - args.kchunks_a) * 64, x0 + dx,
-                        y0 + dy, img);
-          const int kglob = tap * (args.ca + args.cb) + kc * 64;
-          tma_load_2d(sB + stage * Cfg::B_BYTES, &map_w, &full[stage], kglob, 0);
+          if (kb < kmain) {
+            const int tap = kb / kchunks;
+            const int kc = kb - tap * kchunks;
+            const int dy = args.taps == 9 ? tap / 3 - 1 : 0;
+            const int dx = args.taps == 9 ? tap % 3 - 1 : 0;
+            if (kc < args.kchunks_a)
+              tma_load_4d(a_dst, &map_a, &full[stage], kc * 64, x0 + dx, y0 + dy, img);
+            else
+              tma_load_4d(a_dst, &map_b, &full[stage], (kc - args.kchunks_a) * 64, x0 + dx,
+                          y0 + dy, img);
+            const int kglob = tap * (args.ca + args.cb) + kc * 64;
+            tma_load_2d(sB + stage * Cfg::B_BYTES, &map_w, &full[stage], kglob, 0);
+          } else {
+            const int ks = kb - kmain;   // skip chunk: centre tap of the skip sources
+            if (ks < args.kskip_a)
+              tma_load_4d(a_dst, &map_sa, &full[stage], ks * 64, x0, y0, img);
+            else
+              tma_load_4d(a_dst, &map_sb, &full[stage], (ks - args.kskip_a) * 64, x0, y0, img);
+            tma_load_2d(sB + stage * Cfg::B_BYTES, &map_ws, &full[stage], ks * 64, 0);
+          }
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -494,14 +511,22 @@ template <int N, int ROWS>
 __global__ void __launch_bounds__(320, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap map_a,
                      const __grid_constant__ CUtensorMap map_b,
-                     const __grid_constant__ CUtensorMap map_w, const HaloArgs ha) {
+                     const __grid_constant__ CUtensorMap map_w,
+                     const __grid_constant__ CUtensorMap map_sa,
+                     const __grid_constant__ CUtensorMap map_sb,
+                     const __grid_constant__ CUtensorMap map_ws, const HaloArgs ha) {
   using Cfg = HaloCfg<N, ROWS>;
-  const ConvArgs& args = ha.c;
+  const ConvArgs args = ha.c;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int kchunks = args.kchunks_a + args.kchunks_b;
-  const int nb = ha.resident ? 9 * kchunks : ha.b_stages;   // weight tiles held in SMEM
+  // skip chunks ride through the halo ring as ROWS x 128-pixel boxes (no halo)
+  // and use one weight tile each (fused 1x1 skip GEMM)
+  const int kskip = args.kskip_a + args.kskip_b;
+  const int nchunks = kchunks + kskip;
+  constexpr uint32_t SKIP_TX = ROWS * 128 * 128;
+  const int nb = ha.resident ? 9 * kchunks + kskip : ha.b_stages;   // weight tiles in SMEM
   uint8_t* sH = smem;                                         // 2 halo buffers
   uint8_t* sB = smem + 2 * Cfg::HALO_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + nb * Cfg::B_BYTES);
@@ -553,11 +578,13 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       if (ha.resident) {
-        mbar_expect_tx(wfull, (uint32_t)(9 * kchunks * Cfg::B_BYTES));
+        mbar_expect_tx(wfull, (uint32_t)((9 * kchunks + kskip) * Cfg::B_BYTES));
         for (int t = 0; t < 9 * kchunks; ++t) {
           const int tap = t / kchunks, kc = t - tap * kchunks;
           tma_load_2d(sB + t * Cfg::B_BYTES, &map_w, wfull, tap * (args.ca + args.cb) + kc * 64, 0);
         }
+        for (int ks = 0; ks < kskip; ++ks)
+          tma_load_2d(sB + (9 * kchunks + ks) * Cfg::B_BYTES, &map_ws, wfull, ks * 64, 0);
       }
       int hs = 0, bs = 0;
       uint32_t hph = 0, bph = 0;
@@ -566,21 +593,35 @@ __global__ void __launch_bounds__(320, 1)
         const int r = tile - img * tiles_per_img;
         const int ty = r / ha.tiles_x;
         const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
-        for (int kc = 0; kc < kchunks; ++kc) {
+        for (int kc = 0; kc < nchunks; ++kc) {
           mbar_wait(&hempty[hs], hph ^ 1);
-          mbar_expect_tx(&hfull[hs], Cfg::HALO_TX);
           uint8_t* dst = sH + hs * Cfg::HALO_BYTES;
-          if (kc < args.kchunks_a)
-            tma_load_4d(dst, &map_a, &hfull[hs], kc * 64, x0 - 1, y0 - 1, img);
-          else
-            tma_load_4d(dst, &map_b, &hfull[hs], (kc - args.kchunks_a) * 64, x0 - 1, y0 - 1, img);
+          if (kc < kchunks) {
+            mbar_expect_tx(&hfull[hs], Cfg::HALO_TX);
+            if (kc < args.kchunks_a)
+              tma_load_4d(dst, &map_a, &hfull[hs], kc * 64, x0 - 1, y0 - 1, img);
+            else
+              tma_load_4d(dst, &map_b, &hfull[hs], (kc - args.kchunks_a) * 64, x0 - 1, y0 - 1,
+                          img);
+          } else {
+            const int ks = kc - kchunks;
+            mbar_expect_tx(&hfull[hs], SKIP_TX);
+            if (ks < args.kskip_a)
+              tma_load_4d(dst, &map_sa, &hfull[hs], ks * 64, x0, y0, img);
+            else
+              tma_load_4d(dst, &map_sb, &hfull[hs], (ks - args.kskip_a) * 64, x0, y0, img);
+          }
           if (++hs == 2) { hs = 0; hph ^= 1; }
           if (!ha.resident) {
-            for (int tap = 0; tap < 9; ++tap) {
+            const int ntaps = kc < kchunks ? 9 : 1;
+            for (int tap = 0; tap < ntaps; ++tap) {
               mbar_wait(&bempty[bs], bph ^ 1);
               mbar_expect_tx(&bfull[bs], Cfg::B_BYTES);
-              tma_load_2d(sB + bs * Cfg::B_BYTES, &map_w, &bfull[bs],
-                          tap * (args.ca + args.cb) + kc * 64, 0);
+              if (kc < kchunks)
+                tma_load_2d(sB + bs * Cfg::B_BYTES, &map_w, &bfull[bs],
+                            tap * (args.ca + args.cb) + kc * 64, 0);
+              else
+                tma_load_2d(sB + bs * Cfg::B_BYTES, &map_ws, &bfull[bs], (kc - kchunks) * 64, 0);
               if (++bs == ha.b_stages) { bs = 0; bph ^= 1; }
             }
           }
@@ -600,15 +641,18 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d0 = tmem_base + acc * ROWS * N;
-        for (int kc = 0; kc < kchunks; ++kc) {
+        for (int kc = 0; kc < nchunks; ++kc) {
           mbar_wait(&hfull[hs], hph);
           tc_fence_after();
           const uint32_t hbase = smem_u32(sH + hs * Cfg::HALO_BYTES);
-          for (int tap = 0; tap < 9; ++tap) {
+          const bool skipc = kc >= kchunks;
+          const int ntaps = skipc ? 1 : 9;
+          for (int tap = 0; tap < ntaps; ++tap) {
             const int dy = tap / 3, dx = tap % 3;
             uint32_t baddr;
             if (ha.resident) {
-              baddr = smem_u32(sB + (tap * kchunks + kc) * Cfg::B_BYTES);
+              baddr = smem_u32(sB + (skipc ? 9 * kchunks + (kc - kchunks) : tap * kchunks + kc) *
+                                        Cfg::B_BYTES);
             } else {
               mbar_wait(&bfull[bs], bph);
               tc_fence_after();
@@ -618,7 +662,10 @@ __global__ void __launch_bounds__(320, 1)
             if (elect_one()) {
 #pragma unroll
               for (int rr = 0; rr < ROWS; ++rr) {
-                const uint64_t adesc = smem_desc_sw128(hbase + ((rr + dy) * 130 + dx) * 128);
+                // halo chunk: (ROWS+2) x 130 box, tap view shifted by (dy, dx);
+                // skip chunk: ROWS x 128 box, row rr
+                const uint64_t adesc = smem_desc_sw128(
+                    hbase + (skipc ? rr * 128 : (rr + dy) * 130 + dx) * 128);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                   tc_mma(d0 + rr * N, adesc + 2 * k, bdesc + 2 * k, idesc,
@@ -920,6 +967,13 @@ __global__ void conv_simt_kernel(ConvArgs a, const __nv_bfloat16* __restrict__ a
         }
       }
     }
+    const int csa = a.kskip_a * 64, csb = a.kskip_b * 64;
+    for (int ci = 0; ci < csa + csb; ++ci) {     // fused 1x1 skip GEMM
+      const float xv = ci < csa ? __bfloat162float(a.skip_a[p * csa + ci])
+                                : __bfloat162float(a.skip_b[p * csb + (ci - csa)]);
+      for (int i = 0; i < 16; ++i)
+        acc[i] += xv * __bfloat162float(a.wskip[(int64_t)(chunk * 16 + i) * (csa + csb) + ci]);
+    }
     epi_chunk(a, p, chunk * 16, acc);
   }
 }
@@ -1167,13 +1221,22 @@ static int launch_conv_tc(const ig_conv_params_t* p, const ConvArgs& a, cudaStre
     set_error("ig_conv_tc: cuTensorMapEncodeTiled(weights) failed");
     return IG_ERR_CUDA;
   }
+  CUtensorMap msa = ma, msb = ma, mws = mw;
+  if (p->csa > 0) {
+    if (make_act_map(&msa, p->skip_a, p->n, p->h, p->w, p->csa, a.bw, a.bh) != IG_OK ||
+        (p->csb > 0 && make_act_map(&msb, p->skip_b, p->n, p->h, p->w, p->csb, a.bw, a.bh) != IG_OK) ||
+        make_w_map(&mws, p->wskip, p->csa + p->csb, p->cout) != IG_OK) {
+      set_error("ig_conv_tc: cuTensorMapEncodeTiled(skip) failed");
+      return IG_ERR_CUDA;
+    }
+  }
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(conv_tc_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr_set = true;
   }
   const int grid = a.num_tiles < kNumSMs ? a.num_tiles : kNumSMs;
-  { conv_tc_kernel<N><<<grid, 320, Cfg::SMEM, st>>>(ma, mb, mw, a); note_launch(); }
+  { conv_tc_kernel<N><<<grid, 320, Cfg::SMEM, st>>>(ma, mb, mw, msa, msb, mws, a); note_launch(); }
   return cuda_check("ig_conv_tc");
 }
 
@@ -1231,13 +1294,22 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
     return IG_ERR_CUDA;
   }
   if (p->cb == 0) mb = ma;
+  CUtensorMap msa = ma, msb = ma, mws = mw;
+  if (p->csa > 0) {
+    if (make_act_map_box(&msa, p->skip_a, p->n, p->h, p->w, p->csa, 128, ROWS) != IG_OK ||
+        (p->csb > 0 && make_act_map_box(&msb, p->skip_b, p->n, p->h, p->w, p->csb, 128, ROWS) != IG_OK) ||
+        make_w_map(&mws, p->wskip, p->csa + p->csb, p->cout) != IG_OK) {
+      set_error("ig_conv_tc(halo): cuTensorMapEncodeTiled(skip) failed");
+      return IG_ERR_CUDA;
+    }
+  }
   HaloArgs ha;
   ha.c = a;
   ha.tiles_x = p->w / 128;
   ha.tiles_y = p->h / ROWS;
   ha.c.num_tiles = p->n * ha.tiles_x * ha.tiles_y;
   const int kchunks = a.kchunks_a + a.kchunks_b;
-  const int wbytes = 9 * kchunks * Cfg::B_BYTES;
+  const int wbytes = (9 * kchunks + a.kskip_a + a.kskip_b) * Cfg::B_BYTES;
   const int fixed = 1024 + 2 * Cfg::HALO_BYTES + 512 + 1024;
   int smem;
   if (fixed + wbytes <= Cfg::BUDGET) {
@@ -1262,7 +1334,7 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
     attr_smem = 227 * 1024;
   }
   const int grid = ha.c.num_tiles < kNumSMs ? ha.c.num_tiles : kNumSMs;
-  { conv_halo_kernel<N, ROWS><<<grid, Cfg::THREADS, smem, st>>>(ma, mb, mw, ha); note_launch(); }
+  { conv_halo_kernel<N, ROWS><<<grid, Cfg::THREADS, smem, st>>>(ma, mb, mw, msa, msb, mws, ha); note_launch(); }
   return cuda_check("ig_conv_tc(halo)");
 }
 
@@ -1289,6 +1361,16 @@ static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   a->res_a = p->res_a; a->res_b = p->res_b; a->act_gain = p->act_gain;
   a->out0 = reinterpret_cast<__nv_bfloat16*>(p->out0);
   a->out1 = reinterpret_cast<__nv_bfloat16*>(p->out1);
+  IG_REQUIRE(p->csa % 64 == 0 && p->csb % 64 == 0 && p->csa >= 0 && p->csb >= 0,
+             "conv: skip channels must be multiples of 64");
+  IG_REQUIRE(p->csa > 0 || p->csb == 0, "conv: skip_b without skip_a");
+  IG_REQUIRE(p->csa == 0 || (p->skip_a && p->wskip && (p->csb == 0 || p->skip_b)),
+             "conv: skip operands missing");
+  a->kskip_a = p->csa / 64;
+  a->kskip_b = p->csb / 64;
+  a->skip_a = reinterpret_cast<const __nv_bfloat16*>(p->skip_a);
+  a->skip_b = reinterpret_cast<const __nv_bfloat16*>(p->skip_b);
+  a->wskip = reinterpret_cast<const __nv_bfloat16*>(p->wskip);
   (void)tc;
   return IG_OK;
 }
@@ -1319,7 +1401,7 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
   const bool halo = p->taps == 9 && p->w % 128 == 0 && g_variant != 1;
-  if (halo && p->cb == 0 && p->ca == 64 && g_variant != 2) {
+  if (halo && p->cb == 0 && p->ca == 64 && p->csa == 0 && g_variant != 2) {
     if (p->cout <= 128 && p->h % 2 == 0) {
       switch (p->cout) {
         case 16: return launch_conv_rows<16, 2>(p, a, st);

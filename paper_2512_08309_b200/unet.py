@@ -33,7 +33,11 @@ from .grid import Region
 from .noise import STREAM_RENOISE
 
 MP_SILU_GAIN = 1.0 / 0.596   # EDM2 mp_silu: silu(x) / 0.596
-RES_T = 0.3                  # EDM2 mp_sum blend of residual branch
+RES_T = 1.0 / 3.0            # mp_sum blend of the residual branch (EDM2 uses 0.3;
+#                              1/3 makes ra/rb = 2 exactly, see UNetDevice.forward)
+RES_RA = (1 - RES_T) / math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
+RES_RB = RES_T / math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
+RES_Q = 2.0                  # ra / rb
 
 
 @dataclass(frozen=True)
@@ -249,36 +253,67 @@ class UNetDevice:
             self._mod_cache[key] = modulation(self.cfg, self.host, name, sigma).to(dev.device())
         return self._mod_cache[key]
 
+    def _skip_weights(self, name, cin, cout):
+        """q * W_skip (bf16) for the fused skip GEMM of block `name`; the
+        identity when the block keeps its channel count.  q = ra / rb = 2
+        (RES_T = 1/3), so the scaling is exact in bf16."""
+        key = name + ".wskip"
+        if key not in self.w:
+            q = RES_Q
+            if name + ".skip" in self.prog.convs:
+                wsk = self.w[name + ".skip"].float() * q
+            else:
+                wsk = torch.eye(cout, cin, device=dev.device()) * q
+            self.w[key] = wsk.to(torch.bfloat16).contiguous()
+        return self.w[key]
+
+    def _rb(self, n):
+        key = ("rb", n)
+        if key not in self._mod_cache:
+            self._mod_cache[key] = torch.full((n,), RES_RB, dtype=torch.float32,
+                                              device=dev.device())
+        return self._mod_cache[key]
+
     # -- primitive launches -------------------------------------------------
-    def conv(self, name, a, b, sigma, res=None, out0=True, out1=True, res_ab=(0.0, 1.0)):
+    def conv(self, name, a, b, sigma, out0=True, out1=True, skip=None, wskip=None,
+             scale=None):
         cs = self.prog.convs[name]
         n, h, w, ca = a.shape
         cb = 0 if b is None else b.shape[3]
         assert ca + cb == cs.cin, (name, ca, cb, cs.cin)
-        scale = self._scale(name, sigma) if cs.modulated else None   # None: identity
+        if scale is None and cs.modulated:
+            scale = self._scale(name, sigma)      # None: identity
         o0 = torch.empty((n, h, w, cs.cout_pad), dtype=torch.bfloat16, device=a.device) \
             if out0 else None
         o1 = torch.empty((n, h, w, cs.cout_pad), dtype=torch.bfloat16, device=a.device) \
             if out1 else None
+        sa = skip[0] if skip else None
+        sb = skip[1] if skip and len(skip) > 1 else None
         p = ConvParams(n, h, w, ca, cb, cs.cout_pad, cs.taps, a.data_ptr(), dev.ptr(b),
-                       self.w[name].data_ptr(), dev.ptr(scale), None, dev.ptr(res),
-                       res_ab[0], res_ab[1], MP_SILU_GAIN, dev.ptr(o0), dev.ptr(o1))
+                       self.w[name].data_ptr(), dev.ptr(scale), None, None, 0.0, 1.0,
+                       MP_SILU_GAIN, dev.ptr(o0), dev.ptr(o1),
+                       0 if sa is None else sa.shape[3], 0 if sb is None else sb.shape[3],
+                       dev.ptr(sa), dev.ptr(sb), dev.ptr(wskip))
         conv_launch(p)
         return o0, o1
 
     def forward(self, x_in: torch.Tensor, sigma: float) -> torch.Tensor:
-        """x_in: (n, H, W, cin_pad) bf16 -> F (n, H, W, 16) bf16."""
-        cfg = self.cfg
-        nrm = math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
-        ra, rb = (1 - RES_T) / nrm, RES_T / nrm
+        """x_in: (n, H, W, cin_pad) bf16 -> F (n, H, W, 16) bf16.
+
+        Residual blocks: x' = rb * (conv2(h) + q * skip(x)) = ra*skip + rb*conv2
+        (mp_sum).  The skip branch (1x1 conv, or identity) is accumulated into
+        conv2's TMEM accumulator as extra K blocks (no separate launch, no
+        residual read), and the epilogue scales by rb."""
         x, xa = self.conv("stem", x_in, None, sigma)
         skips = [(x, xa)]
         for op in self.prog.ops[1:]:
             if op[0] == "enc":
-                nm, has_skip = op[1], op[2]
+                nm = op[1]
                 _, h1 = self.conv(nm + ".c1", xa, None, sigma, out0=False)
-                res = self.conv(nm + ".skip", x, None, sigma, out1=False)[0] if has_skip else x
-                x, xa = self.conv(nm + ".c2", h1, None, sigma, res=res, res_ab=(ra, rb))
+                c2 = self.prog.convs[nm + ".c2"]
+                wsk = self._skip_weights(nm, x.shape[3], c2.cout)
+                x, xa = self.conv(nm + ".c2", h1, None, sigma, skip=(x,), wskip=wsk,
+                                  scale=self._rb(c2.cout_pad))
                 skips.append((x, xa))
             elif op[0] == "down":
                 x, xa = pool_launch(x)
@@ -287,8 +322,10 @@ class UNetDevice:
                 nm = op[1]
                 s, sa = skips.pop()
                 _, h1 = self.conv(nm + ".c1", xa, sa, sigma, out0=False)
-                res = self.conv(nm + ".skip", x, s, sigma, out1=False)[0]
-                x, xa = self.conv(nm + ".c2", h1, None, sigma, res=res, res_ab=(ra, rb))
+                c2 = self.prog.convs[nm + ".c2"]
+                wsk = self._skip_weights(nm, x.shape[3] + s.shape[3], c2.cout)
+                x, xa = self.conv(nm + ".c2", h1, None, sigma, skip=(x, s), wskip=wsk,
+                                  scale=self._rb(c2.cout_pad))
             elif op[0] == "up":
                 x, xa = upsample_launch(x), upsample_launch(xa)
             elif op[0] == "out":

@@ -104,6 +104,51 @@ def _run_conv_case(n, h, w, ca, cb, cout, taps):
     assert d <= 0.01 * y.abs().max().item() + 1e-2
 
 
+@pytest.mark.parametrize("n,h,w,ca,cout,csa,csb", [
+    (2, 64, 256, 64, 64, 64, 0),       # halo kernel, identity-style skip
+    (1, 32, 128, 64, 128, 128, 64),    # halo kernel, two skip sources
+    (2, 32, 64, 128, 128, 64, 64),     # per-tap kernel (width < 128)
+    (1, 16, 128, 128, 256, 128, 128),  # halo, one-row tiles
+])
+@pytest.mark.parametrize("variant", ["auto", "per_tap"])
+def test_conv_fused_skip_gemm(n, h, w, ca, cout, csa, csb, variant):
+    """acc = conv3x3(a) + [skip_a, skip_b] @ wskip^T, then the epilogue."""
+    check(lib().ig_conv_set_variant(1 if variant == "per_tap" else 0))
+    try:
+        g = torch.Generator(device=DEV).manual_seed(h * w + cout + csa)
+        a = torch.randn(n, h, w, ca, device=DEV, generator=g).bfloat16()
+        wgt = (torch.randn(cout, 9 * ca, device=DEV, generator=g) / math.sqrt(9 * ca)).bfloat16()
+        sa = torch.randn(n, h, w, csa, device=DEV, generator=g).bfloat16()
+        sb = torch.randn(n, h, w, csb, device=DEV, generator=g).bfloat16() if csb else None
+        wsk = (torch.randn(cout, csa + csb, device=DEV, generator=g) /
+               math.sqrt(csa + csb)).bfloat16()
+        scale = torch.full((cout,), 0.45, device=DEV)
+        outs = {}
+        for kind in ("tc", "simt"):
+            o0 = torch.empty(n, h, w, cout, device=DEV, dtype=torch.bfloat16)
+            o1 = torch.empty_like(o0)
+            p = ConvParams(n, h, w, ca, 0, cout, 9, a.data_ptr(), 0, wgt.data_ptr(),
+                           scale.data_ptr(), 0, 0, 0.0, 1.0, 1.5, o0.data_ptr(), o1.data_ptr(),
+                           csa, csb, sa.data_ptr(), 0 if sb is None else sb.data_ptr(),
+                           wsk.data_ptr())
+            fn = lib().ig_conv_tc if kind == "tc" else None
+            if kind == "tc":
+                check(lib().ig_conv_tc(p, None, torch.cuda.current_stream().cuda_stream))
+            else:
+                check(lib().ig_conv_simt(p, torch.cuda.current_stream().cuda_stream))
+            torch.cuda.synchronize()
+            outs[kind] = (o0.float(), o1.float())
+        y, _ = _conv_ref(a, None, wgt, cout, 9, torch.ones(cout, device=DEV), None, 0, 1, 1)
+        skp = (sa if sb is None else torch.cat([sa, sb], -1)).float() @ wsk.float().t()
+        y = (y + skp) * 0.45
+        ya = 1.5 * F.silu(y)
+        for kind, (o0, o1) in outs.items():
+            assert (o0 - y).abs().max().item() < 0.02 * y.abs().max().item() + 0.02, kind
+            assert (o1 - ya).abs().max().item() < 0.02 * ya.abs().max().item() + 0.02, kind
+    finally:
+        check(lib().ig_conv_set_variant(0))
+
+
 SMALL = unet.UNetConfig(base=64, mults=(1, 2), blocks=1, sigmas=(80.0, 1.0))
 
 

@@ -1,0 +1,106 @@
+"""Per-layer roofline table from an ncu launch list of tools/prof_step.py.
+
+python tools/layer_table.py launches.csv [--windows 64]
+
+Matches the launches of the LAST UNet forward to the layer program and prints,
+per launch: time, algorithmic TFLOP/s, minimal HBM bytes (activations in/out,
+residual), and the max(tensor, HBM) bound time using MEASURED_PEAKS.json.
+"""
+import csv
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2512_08309_b200.unet import UNetConfig, build_program  # noqa: E402
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr, out = None, []
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            if d["Metric Name"] != "gpu__time_duration.sum":
+                continue
+            v = float(d["Metric Value"].replace(",", ""))
+            v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(d["Metric Unit"], 1.0)
+            out.append((d["Kernel Name"].split("(")[0], v))
+    return out
+
+
+def layer_ops(cfg, win):
+    """Expected launch sequence of one forward: (kind, name, h, cin, cout, taps, outs, res)."""
+    prog = build_program(cfg)
+    ch = cfg.channels()
+    seq = [("gather", "gather", win, 0, cfg.cin_pad, 0, 1, 0)]
+    lv = 0
+    h = win
+    for op in prog.ops:
+        if op[0] == "stem":
+            seq.append(("conv", "stem", h, cfg.cin_pad, ch[0], 1, 2, 0))
+        elif op[0] == "enc":
+            nm, has_skip = op[1], op[2]
+            c1 = prog.convs[nm + ".c1"]
+            seq.append(("conv", nm + ".c1", h, c1.cin, c1.cout, 9, 1, 0))
+            if has_skip:
+                sk = prog.convs[nm + ".skip"]
+                seq.append(("conv", nm + ".skip", h, sk.cin, sk.cout, 1, 1, 0))
+            c2 = prog.convs[nm + ".c2"]
+            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, 2, 1))
+        elif op[0] == "down":
+            seq.append(("pool", "down", h, 0, 0, 0, 0, 0))
+            h //= 2
+        elif op[0] == "dec":
+            nm = op[1]
+            c1 = prog.convs[nm + ".c1"]
+            seq.append(("conv", nm + ".c1", h, c1.cin, c1.cout, 9, 1, 0))
+            sk = prog.convs[nm + ".skip"]
+            seq.append(("conv", nm + ".skip", h, sk.cin, sk.cout, 1, 1, 0))
+            c2 = prog.convs[nm + ".c2"]
+            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, 2, 1))
+        elif op[0] == "up":
+            seq.append(("up", "up.x", h, 0, 0, 0, 0, 0))
+            seq.append(("up", "up.xa", h, 0, 0, 0, 0, 0))
+            h *= 2
+        elif op[0] == "out":
+            seq.append(("conv", "out", h, ch[0], 16, 9, 1, 0))
+            seq.append(("output", "output", h, 0, 0, 0, 0, 0))
+    return seq
+
+
+def main():
+    path = sys.argv[1]
+    n = int(sys.argv[sys.argv.index("--windows") + 1]) if "--windows" in sys.argv else 64
+    cfg = UNetConfig()
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    tf, bw = peaks["bf16_tflops_sustained"] * 1e12, peaks["hbm_gbs"] * 1e9
+    L = [x for x in launches(path) if not x[0].startswith("void at::")]
+    seq = layer_ops(cfg, 256)
+    last = L[-len(seq):]
+    tot_t = tot_b = 0.0
+    print(f"{'layer':14s} {'kernel':28s} {'us':>8s} {'TF/s':>7s} {'GB/s':>7s} {'bound_us':>8s} {'eff':>5s}")
+    for (kind, name, h, cin, cout, taps, outs, res), (kname, us) in zip(seq, last):
+        px = n * h * h
+        fl = 2.0 * px * cin * cout * taps if kind == "conv" else 0.0
+        if kind == "conv":
+            by = px * 2 * (cin + cout * (outs + res))
+        elif kind == "up":
+            by = px * 2 * 64 * 1.25
+        else:
+            by = 0.0
+        bound = max(fl / tf, by / bw) * 1e6
+        tot_t += us
+        tot_b += bound
+        print(f"{name:14s} {kname[-28:]:28s} {us:8.1f} {fl / us / 1e6:7.1f} {by / us / 1e3:7.0f} "
+              f"{bound:8.1f} {bound / us if us else 0:5.2f}")
+    print(f"total {tot_t:.1f} us, sum of per-layer bounds {tot_b:.1f} us ({tot_b / tot_t:.2f})")
+
+
+if __name__ == "__main__":
+    main()
