@@ -1106,53 +1106,69 @@ __global__ void unet_output_kernel(const __nv_bfloat16* __restrict__ f, int n, i
 __global__ void avgpool2_kernel(const __nv_bfloat16* __restrict__ in, int n, int h, int w, int c,
                                 float gain, __nv_bfloat16* __restrict__ out,
                                 __nv_bfloat16* __restrict__ out_act) {
+  // one output row per CTA iteration: no 64-bit divisions in the inner loop
   const int oh = h / 2, ow = w / 2;
   const int c8 = c / 8;
-  const int64_t total = (int64_t)n * oh * ow * c8;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int cv = (int)(idx % c8);
-    const int64_t pix = idx / c8;
-    const int img = (int)(pix / ((int64_t)oh * ow));
-    const int rem = (int)(pix - (int64_t)img * oh * ow);
-    const int oy = rem / ow, ox = rem - (rem / ow) * ow;
-    float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int d = 0; d < 4; ++d) {
-      const int yy = 2 * oy + (d >> 1), xx = 2 * ox + (d & 1);
-      const uint4 v = *reinterpret_cast<const uint4*>(
-          in + (((int64_t)img * h + yy) * w + xx) * c + cv * 8);
-      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&v);
-      for (int i = 0; i < 8; ++i) s[i] += __bfloat162float(b[i]);
+  const int row_items = ow * c8;
+  const int rows = n * oh;
+  for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int img = row / oh, oy = row - (row / oh) * oh;
+    const __nv_bfloat16* r0 = in + ((int64_t)img * h + 2 * oy) * w * c;
+    const __nv_bfloat16* r1 = r0 + (int64_t)w * c;
+    __nv_bfloat16* o0 = out + (int64_t)row * ow * c;
+    __nv_bfloat16* o1 = out_act + (int64_t)row * ow * c;
+    for (int q = threadIdx.x; q < row_items; q += blockDim.x) {
+      const int ox = q / c8, cv = q - ox * c8;
+      const int64_t off = (int64_t)(2 * ox) * c + cv * 8;
+      const uint4 va = __ldg(reinterpret_cast<const uint4*>(r0 + off));
+      const uint4 vb = __ldg(reinterpret_cast<const uint4*>(r0 + off + c));
+      const uint4 vc = __ldg(reinterpret_cast<const uint4*>(r1 + off));
+      const uint4 vd = __ldg(reinterpret_cast<const uint4*>(r1 + off + c));
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&va);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&vb);
+      const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&vc);
+      const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&vd);
+      uint4 o, oa;
+      __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+      __nv_bfloat162* oab = reinterpret_cast<__nv_bfloat162*>(&oa);
+      const float hg = 0.5f * gain;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 fa = __bfloat1622float2(a2[i]), fb = __bfloat1622float2(b2[i]);
+        const float2 fc = __bfloat1622float2(c2[i]), fd = __bfloat1622float2(d2[i]);
+        const float mx = ((fa.x + fb.x) + (fc.x + fd.x)) * 0.25f;
+        const float my = ((fa.y + fb.y) + (fc.y + fd.y)) * 0.25f;
+        ob[i] = __floats2bfloat162_rn(mx, my);
+        oab[i] = __floats2bfloat162_rn(gsilu(mx, hg), gsilu(my, hg));
+      }
+      *reinterpret_cast<uint4*>(o0 + (int64_t)ox * c + cv * 8) = o;
+      *reinterpret_cast<uint4*>(o1 + (int64_t)ox * c + cv * 8) = oa;
     }
-    uint4 o, oa;
-    __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
-    __nv_bfloat16* oab = reinterpret_cast<__nv_bfloat16*>(&oa);
-    for (int i = 0; i < 8; ++i) {
-      const float m = s[i] * 0.25f;
-      ob[i] = __float2bfloat16_rn(m);
-      oab[i] = __float2bfloat16_rn(gain * silu_f(m));
-    }
-    const int64_t o_off = pix * c + cv * 8;
-    *reinterpret_cast<uint4*>(out + o_off) = o;
-    *reinterpret_cast<uint4*>(out_act + o_off) = oa;
   }
 }
 
 __global__ void upsample2_kernel(const __nv_bfloat16* __restrict__ in, int n, int h, int w, int c,
                                  __nv_bfloat16* __restrict__ out) {
+  // one INPUT row per CTA iteration; each 16-byte chunk is written to the
+  // 2x2 output pixels it covers (two output rows, two adjacent pixels)
   const int c8 = c / 8;
-  const int oh = 2 * h, ow = 2 * w;
-  const int64_t total = (int64_t)n * oh * ow * c8;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int cv = (int)(idx % c8);
-    const int64_t pix = idx / c8;
-    const int img = (int)(pix / ((int64_t)oh * ow));
-    const int rem = (int)(pix - (int64_t)img * oh * ow);
-    const int oy = rem / ow, ox = rem - (rem / ow) * ow;
-    const uint4 v = *reinterpret_cast<const uint4*>(
-        in + (((int64_t)img * h + oy / 2) * w + ox / 2) * c + cv * 8);
-    *reinterpret_cast<uint4*>(out + pix * c + cv * 8) = v;
+  const int ow = 2 * w;
+  const int row_items = w * c8;
+  const int rows = n * h;
+  for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int img = row / h, y = row - (row / h) * h;
+    const __nv_bfloat16* src = in + (int64_t)row * w * c;
+    __nv_bfloat16* d0 = out + ((int64_t)img * 2 * h + 2 * y) * ow * c;
+    __nv_bfloat16* d1 = d0 + (int64_t)ow * c;
+    for (int q = threadIdx.x; q < row_items; q += blockDim.x) {
+      const int x = q / c8, cv = q - x * c8;
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + (int64_t)x * c + cv * 8));
+      const int64_t o = (int64_t)(2 * x) * c + cv * 8;
+      *reinterpret_cast<uint4*>(d0 + o) = v;
+      *reinterpret_cast<uint4*>(d0 + o + c) = v;
+      *reinterpret_cast<uint4*>(d1 + o) = v;
+      *reinterpret_cast<uint4*>(d1 + o + c) = v;
+    }
   }
 }
 
@@ -1496,8 +1512,8 @@ int ig_unet_output(const void* f, int32_t n, int32_t h, int32_t w, int32_t fc,
 int ig_avgpool2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,
                      void* out_act, void* cuda_stream) {
   IG_REQUIRE(h % 2 == 0 && w % 2 == 0 && c % 8 == 0, "avgpool2: bad shape");
-  const int64_t total = (int64_t)n * (h / 2) * (w / 2) * (c / 8);
-  { avgpool2_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+  const int64_t total = (int64_t)n * (h / 2);
+  { avgpool2_kernel<<<grid_for(total, 1, 16), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(in), n, h, w, c, 1.0f / 0.596f,
       reinterpret_cast<__nv_bfloat16*>(out), reinterpret_cast<__nv_bfloat16*>(out_act)); note_launch(); }
   return cuda_check("ig_avgpool2_bf16");
@@ -1506,8 +1522,8 @@ int ig_avgpool2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c,
 int ig_upsample2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,
                       void* cuda_stream) {
   IG_REQUIRE(c % 8 == 0, "upsample2: channels must be a multiple of 8");
-  const int64_t total = (int64_t)n * (2 * h) * (2 * w) * (c / 8);
-  { upsample2_kernel<<<grid_for(total, 256), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+  const int64_t total = (int64_t)n * h;
+  { upsample2_kernel<<<grid_for(total, 1, 16), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(in), n, h, w, c,
       reinterpret_cast<__nv_bfloat16*>(out)); note_launch(); }
   return cuda_check("ig_upsample2_bf16");

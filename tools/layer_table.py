@@ -48,11 +48,9 @@ def layer_ops(cfg, win):
             nm, has_skip = op[1], op[2]
             c1 = prog.convs[nm + ".c1"]
             seq.append(("conv", nm + ".c1", h, c1.cin, c1.cout, 9, 1, 0))
-            if has_skip:
-                sk = prog.convs[nm + ".skip"]
-                seq.append(("conv", nm + ".skip", h, sk.cin, sk.cout, 1, 1, 0))
             c2 = prog.convs[nm + ".c2"]
-            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, 2, 1))
+            # c2 with the fused skip GEMM: reads the block input (c1.cin) once more
+            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, 2, c1.cin / c2.cout))
         elif op[0] == "down":
             seq.append(("pool", "down", h, 0, 0, 0, 0, 0))
             h //= 2
@@ -60,10 +58,8 @@ def layer_ops(cfg, win):
             nm = op[1]
             c1 = prog.convs[nm + ".c1"]
             seq.append(("conv", nm + ".c1", h, c1.cin, c1.cout, 9, 1, 0))
-            sk = prog.convs[nm + ".skip"]
-            seq.append(("conv", nm + ".skip", h, sk.cin, sk.cout, 1, 1, 0))
             c2 = prog.convs[nm + ".c2"]
-            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, 2, 1))
+            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, 2, c1.cin / c2.cout))
         elif op[0] == "up":
             seq.append(("up", "up.x", h, 0, 0, 0, 0, 0))
             seq.append(("up", "up.xa", h, 0, 0, 0, 0, 0))
