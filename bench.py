@@ -375,6 +375,106 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _timed(fn, reps):
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for k in range(reps):
+        fn(k)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def run_cfg3(args):
+    """BASELINE configs[2]: coarse planetary UNet -> conditioned base UNet ->
+    Laplacian stabilize + decode + signed_square, 4096^2, fresh store per step."""
+    import torch
+    import paper_2512_08309_b200 as ig
+    from paper_2512_08309_b200 import transforms
+    from paper_2512_08309_b200.unet import UNetConfig
+    side = args.region if args.region else 4096
+    coarse = UNetConfig(base=64, mults=(1,), blocks=1, sigmas=(80.0,))
+    basecfg = UNetConfig(data_channels=2, cond_channels=3, base=args.base,
+                         mults=tuple(args.mults), blocks=args.blocks, sigmas=(80.0, 1.0))
+    pcfg = ig.PipelineConfig(stages=(
+        ig.StageConfig(steps=1, window=64, stride=32, corruption=(0.1,), patch=4,
+                       denoiser=ig.DenoiserSpec(kind="unet", unet=coarse)),
+        ig.StageConfig(steps=2, window=WINDOW, stride=STRIDE, scale=16, channels=2,
+                       denoiser=ig.DenoiserSpec(kind="unet", unet=basecfg)),
+    ))
+    counts = {}
+
+    def step(k):
+        store = ig.TileStore()
+        h = ig.build_pipeline(store, pcfg, seed=0, user_map=ig.ProceduralMap(0, cell=16))
+        r = ig.Region(side * k - 10 ** 6, 10 ** 5, side, side)
+        j0 = store.read_values_device(h, r)
+        low = transforms.block_mean(j0[0].to(torch.float64), 8)
+        pair = transforms.LaplacianPair(low=low, high=j0[1].to(torch.float64), factor=8,
+                                        dtype=torch.float32)
+        elev = transforms.laplacian_decode_signed_square(transforms.laplacian_stabilize(pair, 1))
+        counts.update({n: store.generator_calls(n) for n in store.tensor_names()})
+        return elev
+
+    for k in range(args.warmup):
+        step(100 + k)
+    ms = _timed(step, args.steps)
+    print(json.dumps({
+        "metric": METRIC, "value": round(side * side * KM2_PER_PX / (ms / 1e3), 3),
+        "unit": "km^2/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"cfg3: hierarchy (coarse UNet w64/s32 T=1 -> base UNet "
+                               f"w256/s128 T=2 scale 16, C=2, conditioned) + Laplacian "
+                               f"stabilize/decode/signed_square, {side}x{side}",
+                   "generator_calls": counts}}), flush=True)
+
+
+def run_cfg4(args):
+    """BASELINE configs[3]: random-access 512^2 queries through ONE persistent
+    device store (UNet Phi, T=2), origins from random.Random(0 ^ 0xB1E55ED) in
+    [-1e6, 1e6); per-query device latency p50/p99 (synchronised per query)."""
+    import random
+    import statistics as stats
+    import torch
+    import paper_2512_08309_b200 as ig
+    from paper_2512_08309_b200.grid import WindowLayout
+    ucfg = _workload(args)
+    scfg = ig.SamplerConfig(steps=T, layout=WindowLayout(WINDOW, STRIDE), seed=0,
+                            denoiser=ig.DenoiserSpec(kind="unet", unet=ucfg), name="stream",
+                            cache_limit=args.cache_gb * (1 << 30))
+    state = ig.SamplerState(scfg, ig.TileStore())
+    rng = random.Random(0 ^ 0xB1E55ED)
+    n = args.queries
+    origins = [(rng.randrange(-10 ** 6, 10 ** 6), rng.randrange(-10 ** 6, 10 ** 6))
+               for _ in range(n + args.warmup)]
+    if args.snap:
+        origins = [(x - x % STRIDE, y - y % STRIDE) for x, y in origins]
+    lat, calls = [], []
+    for k, (x, y) in enumerate(origins):
+        c0 = state.total_denoiser_calls()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        state.query_device(0, ig.Region(x, y, 512, 512))
+        torch.cuda.synchronize()
+        if k >= args.warmup:
+            lat.append((time.perf_counter() - t0) * 1e3)
+            calls.append(state.total_denoiser_calls() - c0)
+    lat.sort()
+    p50, p99 = lat[len(lat) // 2], lat[min(len(lat) - 1, int(0.99 * len(lat)))]
+    print(json.dumps({
+        "metric": "cfg4 random-access 512^2 query latency", "value": round(p50, 3),
+        "unit": "ms (p50)", "p99_ms": round(p99, 3), "mean_ms": round(stats.mean(lat), 3),
+        "queries": n, "phi_per_query_mean": round(stats.mean(calls), 2),
+        "phi_per_query_max": max(calls), "higher_is_better": False,
+        "config": {"workload": "cfg4: scattered 512x512 queries, one persistent DIRECT "
+                               f"store (cache_limit {args.cache_gb} GiB), UNet Phi T=2, "
+                               f"origins {'snapped to the stride lattice' if args.snap else 'unsnapped'}"}
+    }), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -384,16 +484,24 @@ def main():
     ap.add_argument("--base", type=int, default=64)
     ap.add_argument("--mults", type=int, nargs="+", default=[1, 2, 2, 4])
     ap.add_argument("--blocks", type=int, default=1)
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5"],
-                    help="cfg2: one 2048^2 region per GPU per step (weak scaling); cfg5: one "
-                         "16384^2 region per step sharded over all GPUs (strong scaling)")
-    ap.add_argument("--region", type=int, default=0, help="cfg5 region side override")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="cfg2: one 2048^2 region per GPU per step (weak scaling); cfg3: "
+                         "hierarchy + Laplacian decode; cfg4: streaming 512^2 queries; cfg5: "
+                         "one 16384^2 region per step sharded over all GPUs (strong scaling)")
+    ap.add_argument("--region", type=int, default=0, help="cfg3/cfg5 region side override")
+    ap.add_argument("--queries", type=int, default=300, help="cfg4 measured queries")
+    ap.add_argument("--cache-gb", type=int, default=8, help="cfg4 device cache budget")
+    ap.add_argument("--snap", action="store_true", help="cfg4: snap origins to the stride")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--ref-region", type=int, default=128)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "cfg3":
+        run_cfg3(args)
+    elif args.workload == "cfg4":
+        run_cfg4(args)
     else:
         run_gpu(args)
 

@@ -1,0 +1,68 @@
+"""Hierarchy with learned Phi (cfg3 shape, scaled down): a coarse UNet without
+down/upsampling samples the planetary stage from a corrupted
+procedural map; a conditioned UNet (features of the stage above as input
+planes) samples the base stage; the result goes through the Laplacian
+stabilize/decode.  GPU vs the fp32 CPU oracle under the stated tolerance."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import paper_2512_08309_b200 as ig  # noqa: E402
+from paper_2512_08309_b200 import transforms  # noqa: E402
+from paper_2512_08309_b200.grid import Region  # noqa: E402
+from paper_2512_08309_b200.unet import UNetConfig  # noqa: E402
+
+RMS_TOL, MAX_TOL = 0.03, 0.25
+
+COARSE = UNetConfig(base=64, mults=(1,), blocks=1, sigmas=(80.0,))
+BASE = UNetConfig(data_channels=2, cond_channels=3, base=64, mults=(1, 2), blocks=1,
+                  sigmas=(80.0, 1.0))
+
+
+def _gpu_pipeline():
+    cfg = ig.PipelineConfig(stages=(
+        ig.StageConfig(steps=1, window=64, stride=32,
+                       denoiser=ig.DenoiserSpec(kind="unet", unet=COARSE),
+                       corruption=(0.1,), patch=4),
+        ig.StageConfig(steps=2, window=64, stride=32, scale=2, channels=2,
+                       denoiser=ig.DenoiserSpec(kind="unet", unet=BASE)),
+    ))
+    store = ig.TileStore()
+    h = ig.build_pipeline(store, cfg, seed=0, user_map=ig.ProceduralMap(0, cell=16))
+    return store, h
+
+
+def _oracle(region):
+    from oracle import port
+    from oracle.unet_ref import unet_phi
+    stages = [dict(steps=1, window=64, stride=32, phi=unet_phi(COARSE, 1, 0),
+                   corruption=(0.1,), patch=4),
+              dict(steps=2, window=64, stride=32, scale=2, channels=2,
+                   phi=unet_phi(BASE, 2, 1))]
+    return port.pipeline_dense(stages, 0, lambda b, c: port.procedural(0, 16, b, c),
+                               port.Box(region.x0, region.y0, region.width, region.height))
+
+
+def test_unet_hierarchy_vs_oracle():
+    r = Region(0, 0, 128, 128)
+    store, h = _gpu_pipeline()
+    got = store.read_values(h, r)
+    want = _oracle(r)
+    assert got.shape == want.shape == (2, 128, 128)
+    for c in range(2):
+        std = float(want[c].std())
+        rms = float(np.sqrt(np.mean((got[c] - want[c]) ** 2))) / std
+        mx = float(np.abs(got[c] - want[c]).max()) / std
+        assert rms < RMS_TOL and mx < MAX_TOL, (c, rms, mx)
+    # Laplacian decode of the base stage's (low source, residual) channels
+    low = transforms.block_mean(got[0].astype(np.float64), 8)
+    pair = transforms.LaplacianPair(low=low, high=got[1].astype(np.float64), factor=8,
+                                    dtype=np.dtype(np.float32))
+    elev = transforms.laplacian_decode_signed_square(transforms.laplacian_stabilize(pair, 1))
+    assert elev.shape == (128, 128) and np.isfinite(elev).all()
+    # seed consistency through the whole hierarchy: a sub-region from a fresh store
+    store2, h2 = _gpu_pipeline()
+    sub = store2.read_values(h2, Region(32, 64, 64, 32))
+    np.testing.assert_array_equal(sub, got[:, 64:96, 32:96])
