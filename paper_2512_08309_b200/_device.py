@@ -33,6 +33,10 @@ def stream_ptr() -> int:
 
 
 def torch_dtype(dtype) -> torch.dtype:
+    if isinstance(dtype, torch.dtype):
+        if dtype in (torch.float32, torch.float64):
+            return dtype
+        raise ValueError(f"unsupported dtype {dtype} (float32 or float64)")
     dt = np.dtype(dtype)
     if dt == np.float32:
         return torch.float32
