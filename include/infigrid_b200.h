@@ -174,6 +174,9 @@ typedef struct {
   const void* skip_a;     /* [n][h][w][csa] bf16 */
   const void* skip_b;     /* [n][h][w][csb] bf16 or NULL */
   const void* wskip;      /* [cout][csa+csb] bf16 */
+  /* up2 != 0: out0/out1 are [n][2h][2w][cout] and every result is written to
+   * its 2x2 block (nearest-neighbour upsample fused into the epilogue) */
+  int32_t up2;
 } ig_conv_params_t;
 size_t ig_conv_workspace_bytes(void);
 /* 1: force the per-tap (v1) kernel for every conv; 0: halo kernel where it applies */

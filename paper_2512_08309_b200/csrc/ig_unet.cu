@@ -156,6 +156,7 @@ struct ConvArgs {
   int n, h, w, ca, cb, cout, taps;
   int bw, bh, tiles_per_img, num_tiles, kchunks_a, kchunks_b;
   int kskip_a, kskip_b;   // 64-channel chunks of the fused 1x1 skip GEMM
+  int up2;                // outputs replicated onto a 2x finer grid
   const __nv_bfloat16* skip_a;
   const __nv_bfloat16* skip_b;
   const __nv_bfloat16* wskip;
@@ -178,6 +179,28 @@ struct ConvCfg {
                                    : (2 * N <= 256) ? 256 : 512;
   static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + 1024;
 };
+
+// Output element offset of pixel p.  With up2 the outputs live on a 2x finer
+// grid and every result is replicated to its 2x2 block (the nearest-neighbour
+// upsample of the UNet decoder, fused into the producing convolution).
+__device__ __forceinline__ int64_t out_base(const ConvArgs& a, int64_t p) {
+  if (!a.up2) return p * a.cout;
+  const int64_t hw = (int64_t)a.h * a.w;
+  const int64_t img = p / hw;
+  const int rem = (int)(p - img * hw);
+  const int y = rem / a.w, x = rem - (rem / a.w) * a.w;
+  return ((img * 2 * a.h + 2 * y) * (2 * (int64_t)a.w) + 2 * x) * a.cout;
+}
+__device__ __forceinline__ void store_out(const ConvArgs& a, __nv_bfloat16* base, int64_t o,
+                                          uint4 v) {
+  *reinterpret_cast<uint4*>(base + o) = v;
+  if (a.up2) {
+    const int64_t rs = (int64_t)2 * a.w * a.cout;
+    *reinterpret_cast<uint4*>(base + o + a.cout) = v;
+    *reinterpret_cast<uint4*>(base + o + rs) = v;
+    *reinterpret_cast<uint4*>(base + o + rs + a.cout) = v;
+  }
+}
 
 // epilogue of one 16-channel chunk for pixel p
 __device__ __forceinline__ void epi_chunk(const ConvArgs& a, int64_t p, int c0, const float* acc) {
@@ -202,9 +225,9 @@ __device__ __forceinline__ void epi_chunk(const ConvArgs& a, int64_t p, int c0, 
     __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(o);
 #pragma unroll
     for (int i = 0; i < 8; ++i) ob[i] = __floats2bfloat162_rn(y[2 * i], y[2 * i + 1]);
-    uint4* dp = reinterpret_cast<uint4*>(a.out0 + off);
-    dp[0] = o[0];
-    dp[1] = o[1];
+    const int64_t o0 = out_base(a, p) + c0;
+    store_out(a, a.out0, o0, o[0]);
+    store_out(a, a.out0, o0 + 8, o[1]);
   }
   if (a.out1) {
     uint4 o[2];
@@ -213,9 +236,9 @@ __device__ __forceinline__ void epi_chunk(const ConvArgs& a, int64_t p, int c0, 
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       ob[i] = __floats2bfloat162_rn(gsilu(y[2 * i], hg), gsilu(y[2 * i + 1], hg));
-    uint4* dp = reinterpret_cast<uint4*>(a.out1 + off);
-    dp[0] = o[0];
-    dp[1] = o[1];
+    const int64_t o1 = out_base(a, p) + c0;
+    store_out(a, a.out1, o1, o[0]);
+    store_out(a, a.out1, o1 + 8, o[1]);
   }
 }
 
@@ -236,6 +259,7 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
                                          int c0, uint32_t taddr) {
   constexpr int BC = NC < 32 ? NC : 32;
   const int64_t off = p * a.cout + c0;
+  const int64_t ob0 = out_base(a, p) + c0;
   uint4 res[NC / 8];
   if (a.res) {
 #pragma unroll
@@ -295,7 +319,7 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
         __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
         for (int j = 0; j < 4; ++j) ob[j] = __floats2bfloat162_rn(y[8 * i + 2 * j], y[8 * i + 2 * j + 1]);
-        *reinterpret_cast<uint4*>(a.out0 + off + b + 8 * i) = o;
+        store_out(a, a.out0, ob0 + b + 8 * i, o);
       }
     }
     if (a.out1) {
@@ -306,7 +330,7 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           ob[j] = __floats2bfloat162_rn(gsilu(y[8 * i + 2 * j], hg), gsilu(y[8 * i + 2 * j + 1], hg));
-        *reinterpret_cast<uint4*>(a.out1 + off + b + 8 * i) = o;
+        store_out(a, a.out1, ob0 + b + 8 * i, o);
       }
     }
   }
@@ -1387,6 +1411,7 @@ static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   a->skip_a = reinterpret_cast<const __nv_bfloat16*>(p->skip_a);
   a->skip_b = reinterpret_cast<const __nv_bfloat16*>(p->skip_b);
   a->wskip = reinterpret_cast<const __nv_bfloat16*>(p->wskip);
+  a->up2 = p->up2 != 0;
   (void)tc;
   return IG_OK;
 }

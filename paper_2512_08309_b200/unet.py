@@ -276,16 +276,17 @@ class UNetDevice:
 
     # -- primitive launches -------------------------------------------------
     def conv(self, name, a, b, sigma, out0=True, out1=True, skip=None, wskip=None,
-             scale=None):
+             scale=None, up2=False):
         cs = self.prog.convs[name]
         n, h, w, ca = a.shape
         cb = 0 if b is None else b.shape[3]
         assert ca + cb == cs.cin, (name, ca, cb, cs.cin)
         if scale is None and cs.modulated:
             scale = self._scale(name, sigma)      # None: identity
-        o0 = torch.empty((n, h, w, cs.cout_pad), dtype=torch.bfloat16, device=a.device) \
+        oh, ow = (2 * h, 2 * w) if up2 else (h, w)
+        o0 = torch.empty((n, oh, ow, cs.cout_pad), dtype=torch.bfloat16, device=a.device) \
             if out0 else None
-        o1 = torch.empty((n, h, w, cs.cout_pad), dtype=torch.bfloat16, device=a.device) \
+        o1 = torch.empty((n, oh, ow, cs.cout_pad), dtype=torch.bfloat16, device=a.device) \
             if out1 else None
         sa = skip[0] if skip else None
         sb = skip[1] if skip and len(skip) > 1 else None
@@ -293,7 +294,7 @@ class UNetDevice:
                        self.w[name].data_ptr(), dev.ptr(scale), None, None, 0.0, 1.0,
                        MP_SILU_GAIN, dev.ptr(o0), dev.ptr(o1),
                        0 if sa is None else sa.shape[3], 0 if sb is None else sb.shape[3],
-                       dev.ptr(sa), dev.ptr(sb), dev.ptr(wskip))
+                       dev.ptr(sa), dev.ptr(sb), dev.ptr(wskip), int(up2))
         conv_launch(p)
         return o0, o1
 
@@ -306,7 +307,9 @@ class UNetDevice:
         residual read), and the epilogue scales by rb."""
         x, xa = self.conv("stem", x_in, None, sigma)
         skips = [(x, xa)]
-        for op in self.prog.ops[1:]:
+        ops = self.prog.ops
+        for k in range(1, len(ops)):
+            op = ops[k]
             if op[0] == "enc":
                 nm = op[1]
                 _, h1 = self.conv(nm + ".c1", xa, None, sigma, out0=False)
@@ -324,10 +327,13 @@ class UNetDevice:
                 _, h1 = self.conv(nm + ".c1", xa, sa, sigma, out0=False)
                 c2 = self.prog.convs[nm + ".c2"]
                 wsk = self._skip_weights(nm, x.shape[3] + s.shape[3], c2.cout)
+                # the last block of a level writes its outputs directly on the
+                # next (2x finer) level's grid: the upsample is fused
+                up_next = k + 1 < len(ops) and ops[k + 1][0] == "up"
                 x, xa = self.conv(nm + ".c2", h1, None, sigma, skip=(x, s), wskip=wsk,
-                                  scale=self._rb(c2.cout_pad))
+                                  scale=self._rb(c2.cout_pad), up2=up_next)
             elif op[0] == "up":
-                x, xa = upsample_launch(x), upsample_launch(xa)
+                pass            # fused into the preceding conv's epilogue
             elif op[0] == "out":
                 f, _ = self.conv("out", xa, None, sigma, out1=False)
                 return f

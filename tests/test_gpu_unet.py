@@ -149,6 +149,29 @@ def test_conv_fused_skip_gemm(n, h, w, ca, cout, csa, csb, variant):
         check(lib().ig_conv_set_variant(0))
 
 
+@pytest.mark.parametrize("n,h,w,ca,cout", [(2, 32, 64, 64, 128), (1, 16, 128, 128, 64),
+                                           (1, 8, 32, 256, 256)])
+def test_conv_fused_upsample_epilogue(n, h, w, ca, cout):
+    """up2: the epilogue writes the 2x nearest-upsampled outputs directly; they
+    must equal upsampling the ordinary outputs (bit for bit)."""
+    g = torch.Generator(device=DEV).manual_seed(7 * h + cout)
+    a = torch.randn(n, h, w, ca, device=DEV, generator=g).bfloat16()
+    wgt = (torch.randn(cout, 9 * ca, device=DEV, generator=g) / math.sqrt(9 * ca)).bfloat16()
+    res = {}
+    for up2 in (0, 1):
+        f = 2 if up2 else 1
+        o0 = torch.empty(n, f * h, f * w, cout, device=DEV, dtype=torch.bfloat16)
+        o1 = torch.empty_like(o0)
+        p = ConvParams(n, h, w, ca, 0, cout, 9, a.data_ptr(), 0, wgt.data_ptr(), 0, 0, 0, 0.0,
+                       1.0, 1.5, o0.data_ptr(), o1.data_ptr(), 0, 0, 0, 0, 0, up2)
+        check(lib().ig_conv_tc(p, None, torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        res[up2] = (o0, o1)
+    for k in range(2):
+        up = res[0][k].repeat_interleave(2, dim=1).repeat_interleave(2, dim=2)
+        assert torch.equal(res[1][k], up)
+
+
 SMALL = unet.UNetConfig(base=64, mults=(1, 2), blocks=1, sigmas=(80.0, 1.0))
 
 
