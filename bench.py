@@ -136,7 +136,11 @@ def run_gpu(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ucfg = _workload(args)
-    spec = ig.DenoiserSpec(kind="unet", unet=ucfg)
+    if args.phi == "analytic":
+        # the reference's own analytic Phi: the bit-exact parity leg
+        spec = ig.DenoiserSpec(kind="shrink_smooth", radius=1, lambdas=(0.6, 0.4))
+    else:
+        spec = ig.DenoiserSpec(kind="unet", unet=ucfg)
     scfg = ig.SamplerConfig(steps=T, layout=WindowLayout(WINDOW, STRIDE), denoiser=spec, seed=0,
                             name="bench")
     stream = torch.cuda.current_stream()
@@ -246,10 +250,14 @@ def run_gpu(args):
         "dtype": "bf16",
         "data": "synthetic (seed-0 coordinate noise; random-init UNet weights, torch.manual_seed(0))",
         "config": {
-            "workload": "cfg2: InfiniteDiffusion 2048x2048 region, 256-px windows stride 128, "
-                        "2-step consistency sampler, UNet Phi (EDM2-style, base %d, mults %s, "
-                        "%d block/level), 1 region per GPU per step" % (
-                            ucfg.base, list(ucfg.mults), ucfg.blocks),
+            "workload": ("cfg2: InfiniteDiffusion 2048x2048 region, 256-px windows stride 128, "
+                         "2-step consistency sampler, UNet Phi (EDM2-style, base %d, mults %s, "
+                         "%d block/level), 1 region per GPU per step" % (
+                             ucfg.base, list(ucfg.mults), ucfg.blocks))
+                        if args.phi == "unet" else
+                        "cfg2 geometry with the reference's analytic shrink_smooth Phi "
+                        "(bit-exact leg), 1 region per GPU per step",
+            "phi": args.phi,
             "region_px": REGION, "window": WINDOW, "stride": STRIDE, "sampler_steps": T,
             "phi_calls_per_region": calls,
             "mpx_per_s": round(px_total / (ms_max / 1e3) / 1e6, 3),
@@ -489,6 +497,9 @@ def main():
                          "hierarchy + Laplacian decode; cfg4: streaming 512^2 queries; cfg5: "
                          "one 16384^2 region per step sharded over all GPUs (strong scaling)")
     ap.add_argument("--region", type=int, default=0, help="cfg3/cfg5 region side override")
+    ap.add_argument("--phi", default="unet", choices=["unet", "analytic"],
+                    help="Phi of the sampler: the UNet (headline) or the reference's analytic "
+                         "shrink_smooth (bit-exact leg)")
     ap.add_argument("--queries", type=int, default=300, help="cfg4 measured queries")
     ap.add_argument("--cache-gb", type=int, default=8, help="cfg4 device cache budget")
     ap.add_argument("--snap", action="store_true", help="cfg4: snap origins to the stride")
