@@ -182,6 +182,41 @@ size_t ig_conv_workspace_bytes(void);
 /* 1: force the per-tap (v1) kernel for every conv; 0: halo kernel where it applies */
 int ig_conv_set_variant(int force_per_tap);
 int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream);
+/* UNet helpers (NHWC bf16 activations):
+ * ig_unet_gather_input: tap-packed stem input [n][w][w][cin_pad] from window
+ *   crops (+ renoise, conditioning planes, mask, constant plane) and x_noisy;
+ * ig_unet_output: Phi[n][C][h][w] = c_skip * x_noisy + c_out * F[..., c];
+ * ig_avgpool2_bf16: 2x2 mean -> out and mp_silu(out);
+ * ig_upsample2_bf16: nearest 2x. */
+int ig_unet_gather_input(const float* src, int32_t src_batched, int64_t src_x0, int64_t src_y0,
+                         int32_t src_w, int32_t src_h, int32_t channels, const int64_t* wxy,
+                         int32_t n, const float* cond_parent, int64_t cond_x0, int64_t cond_y0,
+                         int32_t cond_w, int32_t cond_h, int32_t cond_c, int32_t cond_scale,
+                         int32_t cond_mask_channel, uint64_t cond_seed, uint64_t renoise_seed,
+                         uint32_t renoise_stream, float sigma, float c_in, int32_t first_step,
+                         void* x_in, int32_t window, int32_t cin_pad, int32_t in_planes,
+                         float* x_noisy, void* cuda_stream);
+int ig_unet_output(const void* f, int32_t n, int32_t h, int32_t w, int32_t fc,
+                   const float* x_noisy, int32_t channels, float c_skip, float c_out,
+                   int32_t flags, float* out, void* cuda_stream);
+int ig_avgpool2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,
+                     void* out_act, void* cuda_stream);
+int ig_upsample2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,
+                      void* cuda_stream);
+/* Fused UNet input gather + stem convolution (64 output channels): builds the
+ * tap-packed input planes of each 128-pixel tile in SMEM (window crops of the
+ * source canvas/batch, consistency renoise, conditioning + mask, constant
+ * plane), runs the stem GEMM on the tensor cores and writes x and mp_silu(x)
+ * (bf16 NHWC [n][window][window][64]) plus x_noisy (f32 [n][channels][w][w]).
+ * Same input-plane contract as ig_unet_gather_input. */
+int ig_unet_stem(const float* src, int32_t src_batched, int64_t src_x0, int64_t src_y0,
+                 int32_t src_w, int32_t src_h, int32_t channels, const int64_t* wxy, int32_t n,
+                 const float* cond_parent, int64_t cond_x0, int64_t cond_y0, int32_t cond_w,
+                 int32_t cond_h, int32_t cond_c, int32_t cond_scale, int32_t cond_mask_channel,
+                 uint64_t cond_seed, uint64_t renoise_seed, uint32_t renoise_stream, float sigma,
+                 float c_in, int32_t first_step, int32_t window, int32_t in_planes,
+                 const void* w_stem, float act_gain, void* out_x, void* out_xa, float* x_noisy,
+                 void* cuda_stream);
 /* same contract on CUDA cores (fp32 accumulate, identical epilogue); used by
  * the tests as an independent device cross-check of the tensor-core kernel */
 int ig_conv_simt(const ig_conv_params_t* p, void* cuda_stream);

@@ -1111,6 +1111,153 @@ __global__ void __launch_bounds__(GTX * GTY) unet_gather_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused input gather + stem: one CTA per 128-pixel tile of a window.
+//   1. the P input planes (c_in*x_noisy with the consistency renoise,
+//      conditioning planes + mask, constant plane) of the tile and its 1-pixel
+//      halo are evaluated into SMEM (f32);
+//   2. every thread packs its pixel's 3x3 neighbourhood (9*P <= 64 channels,
+//      zero outside the window) straight into the SWIZZLE_128B K-major layout
+//      the tensor core reads (chunk c of row m at m*128 + ((c ^ (m&7)) * 16));
+//   3. one elected thread issues 4 x tcgen05.mma (M=128, N=64, K=16) against
+//      the SMEM-resident stem weights, commit -> mbarrier;
+//   4. all 4 warps drain TMEM (warp w owns lanes 32w..32w+31) and store
+//      x and mp_silu(x) (bf16 NHWC).
+// The packed input never touches HBM (the unfused path wrote and re-read
+// 128 B per pixel).
+constexpr int STEM_N = 64;
+
+__global__ void __launch_bounds__(128) unet_stem_kernel(
+    const float* __restrict__ src, int src_batched, int64_t sx0, int64_t sy0, int sw, int sh,
+    int C, const int64_t* __restrict__ wxy, int n, const float* __restrict__ cpar, int64_t cx0,
+    int64_t cy0, int cw, int ch, int cc, int cscale, int cmask, uint64_t cprefix,
+    uint64_t rprefix, float sigma, float c_in, int first_step, int win, int P,
+    const __nv_bfloat16* __restrict__ wstem, float act_gain, __nv_bfloat16* __restrict__ out_x,
+    __nv_bfloat16* __restrict__ out_xa, float* __restrict__ x_noisy) {
+  __shared__ __align__(1024) uint8_t sA[128 * 128];       // packed A tile (SW128)
+  __shared__ __align__(1024) uint8_t sB[STEM_N * 128];    // stem weights (SW128)
+  __shared__ float planes[390 * GPL];   // (rows+2) x (cols+2) x P; max 3 x 130 (w >= 128)
+  __shared__ uint64_t mma_bar;
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int tw = win < 128 ? win : 128;           // tile width in pixels
+  const int trows = 128 / tw;                     // image rows per tile
+  const int tiles_per_win = win * win / 128;
+  const int k = blockIdx.x / tiles_per_win;
+  const int tr = blockIdx.x - k * tiles_per_win;
+  const int y0 = (tr * 128) / win, x0 = (tr * 128) % win;
+  const int hw = tw + 2;
+  const int64_t WX = wxy[2 * k], WY = wxy[2 * k + 1];
+  int slow = 0;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "r"(STEM_N));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&mma_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // stem weights -> SW128 K-major tile (row co = 128 B)
+  for (int q = tid; q < STEM_N * 8; q += 128) {
+    const int row = q / 8, c = q % 8;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(wstem + row * 64 + c * 8));
+    *reinterpret_cast<uint4*>(sB + row * 128 + ((c ^ (row & 7)) * 16)) = v;
+  }
+  // 1. planes of the tile + halo
+  const int npos = (trows + 2) * hw;
+  for (int q = tid; q < npos; q += 128) {
+    const int hy = q / hw, hx = q - hy * hw;
+    const int y = y0 + hy - 1, x = x0 + hx - 1;
+    float pl[GPL];
+#pragma unroll
+    for (int i = 0; i < GPL; ++i) pl[i] = 0.f;
+    if (y >= 0 && y < win && x >= 0 && x < win) {
+      const bool interior = hy >= 1 && hy <= trows && hx >= 1 && hx <= tw;
+      float xn[GPL];
+      gather_planes(src, src_batched, sx0, sy0, sw, sh, C, k, win, y, x, WX + x, WY + y, cpar,
+                    cx0, cy0, cw, ch, cc, cscale, cmask, cprefix, rprefix, sigma, c_in,
+                    first_step, pl, interior ? xn : nullptr, &slow);
+      if (interior)
+        for (int c = 0; c < C; ++c) x_noisy[(((int64_t)k * C + c) * win + y) * win + x] = xn[c];
+    }
+    for (int i = 0; i < P; ++i) planes[q * GPL + i] = pl[i];
+  }
+  __syncthreads();
+  // 2. pack pixel m's 3x3 x P neighbourhood into row m of the A tile
+  {
+    const int m = tid;
+    const int ly = m / tw, lx = m - ly * tw;
+    __align__(16) __nv_bfloat16 row[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) row[i] = __float2bfloat16_rn(0.f);
+    for (int tap = 0; tap < 9; ++tap) {
+      const int q = (ly + tap / 3) * hw + lx + tap % 3;
+      for (int p = 0; p < P; ++p) row[tap * P + p] = __float2bfloat16_rn(planes[q * GPL + p]);
+    }
+    const uint4* rv = reinterpret_cast<const uint4*>(row);
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      *reinterpret_cast<uint4*>(sA + m * 128 + ((c ^ (m & 7)) * 16)) = rv[c];
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  // 3. one GEMM: [128 x 64] x [64 x 64]^T
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint64_t adesc = smem_desc_sw128(smem_u32(sA));
+      const uint64_t bdesc = smem_desc_sw128(smem_u32(sB));
+      constexpr uint32_t idesc = idesc_bf16(128, STEM_N);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        tc_mma(tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, kk ? 1u : 0u);
+      tc_commit(&mma_bar);
+    }
+    __syncwarp();
+  }
+  mbar_wait(&mma_bar, 0);
+  tc_fence_after();
+  // 4. epilogue: thread m holds pixel m's 64 accumulators
+  {
+    const int m = warp * 32 + lane;
+    const int ly = m / tw, lx = m - ly * tw;
+    const int64_t p = ((int64_t)k * win + y0 + ly) * win + x0 + lx;
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+    const float hg = 0.5f * act_gain;
+#pragma unroll
+    for (int c0 = 0; c0 < STEM_N; c0 += 16) {
+      float v[16];
+      tmem_ld16(taddr + c0, v);
+      uint4 o[2], oa[2];
+      __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(o);
+      __nv_bfloat162* oab = reinterpret_cast<__nv_bfloat162*>(oa);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        ob[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+        oab[i] = __floats2bfloat162_rn(gsilu(v[2 * i], hg), gsilu(v[2 * i + 1], hg));
+      }
+      uint4* dx = reinterpret_cast<uint4*>(out_x + p * STEM_N + c0);
+      uint4* dxa = reinterpret_cast<uint4*>(out_xa + p * STEM_N + c0);
+      dx[0] = o[0];
+      dx[1] = o[1];
+      dxa[0] = oa[0];
+      dxa[1] = oa[1];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(STEM_N));
+  }
+}
+
 __global__ void unet_output_kernel(const __nv_bfloat16* __restrict__ f, int n, int h, int w,
                                    int fc, const float* __restrict__ x_noisy, int C,
                                    float c_skip, float c_out, float* __restrict__ out) {
@@ -1520,6 +1667,29 @@ int ig_unet_gather_input(const float* src, int32_t src_batched, int64_t src_x0, 
       noise_prefix(cond_seed, 101u), noise_prefix(renoise_seed, renoise_stream), sigma, c_in,
       first_step, reinterpret_cast<__nv_bfloat16*>(x_in), window, cin_pad, in_planes, x_noisy); note_launch(); }
   return cuda_check("ig_unet_gather_input");
+}
+
+int ig_unet_stem(const float* src, int32_t src_batched, int64_t src_x0, int64_t src_y0,
+                 int32_t src_w, int32_t src_h, int32_t channels, const int64_t* wxy, int32_t n,
+                 const float* cond_parent, int64_t cond_x0, int64_t cond_y0, int32_t cond_w,
+                 int32_t cond_h, int32_t cond_c, int32_t cond_scale, int32_t cond_mask_channel,
+                 uint64_t cond_seed, uint64_t renoise_seed, uint32_t renoise_stream, float sigma,
+                 float c_in, int32_t first_step, int32_t window, int32_t in_planes,
+                 const void* w_stem, float act_gain, void* out_x, void* out_xa, float* x_noisy,
+                 void* cuda_stream) {
+  IG_REQUIRE(n >= 0 && window > 0 && (window * window) % 128 == 0 && window <= 4096,
+             "stem: window side %d unsupported (window^2 must be a multiple of 128)", window);
+  IG_REQUIRE(window >= 128 || 128 % window == 0, "stem: window %d must divide 128", window);
+  IG_REQUIRE(in_planes <= 7, "stem: %d input planes do not tap-pack into 64 channels", in_planes);
+  if (n == 0) return IG_OK;
+  const int64_t tiles = (int64_t)n * window * window / 128;
+  { unet_stem_kernel<<<(unsigned)tiles, 128, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+      src, src_batched, src_x0, src_y0, src_w, src_h, channels, wxy, n, cond_parent, cond_x0,
+      cond_y0, cond_w, cond_h, cond_c, cond_scale < 1 ? 1 : cond_scale, cond_mask_channel,
+      noise_prefix(cond_seed, 101u), noise_prefix(renoise_seed, renoise_stream), sigma, c_in,
+      first_step, window, in_planes, reinterpret_cast<const __nv_bfloat16*>(w_stem), act_gain,
+      reinterpret_cast<__nv_bfloat16*>(out_x), reinterpret_cast<__nv_bfloat16*>(out_xa), x_noisy); note_launch(); }
+  return cuda_check("ig_unet_stem");
 }
 
 int ig_unet_output(const void* f, int32_t n, int32_t h, int32_t w, int32_t fc,

@@ -38,6 +38,7 @@ RES_T = 1.0 / 3.0            # mp_sum blend of the residual branch (EDM2 uses 0.
 RES_RA = (1 - RES_T) / math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
 RES_RB = RES_T / math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
 RES_Q = 2.0                  # ra / rb
+FUSED_STEM = True            # input gather fused into the stem GEMM (ig_unet_stem)
 
 
 @dataclass(frozen=True)
@@ -306,6 +307,10 @@ class UNetDevice:
         conv2's TMEM accumulator as extra K blocks (no separate launch, no
         residual read), and the epilogue scales by rb."""
         x, xa = self.conv("stem", x_in, None, sigma)
+        return self.forward_after_stem(x, xa, sigma)
+
+    def forward_after_stem(self, x: torch.Tensor, xa: torch.Tensor, sigma: float):
+        """The network after the stem: (x, mp_silu(x)) -> F."""
         skips = [(x, xa)]
         ops = self.prog.ops
         for k in range(1, len(ops)):
@@ -434,15 +439,26 @@ def unet_phi_batch(cfg: UNetConfig, src: torch.Tensor, src_region: Region | None
     chunk = max(1, min(n, max_windows_per_forward(win)))
     for k0 in range(0, n, chunk):
         m = min(chunk, n - k0)
-        x_in = torch.empty((m, win, win, cfg.cin_pad), dtype=torch.bfloat16, device=src.device)
         x_noisy = torch.empty((m, C, win, win), dtype=torch.float32, device=src.device)
         sptr = src32[k0:k0 + m].data_ptr() if batched else src32.data_ptr()
-        call("ig_unet_gather_input", sptr, int(batched), sx0, sy0, src32.shape[-1],
-             src32.shape[-2], C, wxy[k0:k0 + m].data_ptr(), m, *cargs[:-1],
-             cargs[-1] & ((1 << 64) - 1), seed & ((1 << 64) - 1), STREAM_RENOISE + outer_step,
-             float(sigma), float(c_in), int(outer_step == steps), x_in.data_ptr(), win,
-             cfg.cin_pad, cfg.in_planes(), x_noisy.data_ptr(), dev.stream_ptr())
-        f = model.forward(x_in, sigma)
+        common = (sptr, int(batched), sx0, sy0, src32.shape[-1], src32.shape[-2], C,
+                  wxy[k0:k0 + m].data_ptr(), m, *cargs[:-1], cargs[-1] & ((1 << 64) - 1),
+                  seed & ((1 << 64) - 1), STREAM_RENOISE + outer_step, float(sigma), float(c_in),
+                  int(outer_step == steps))
+        if FUSED_STEM and model.prog.convs["stem"].cout_pad == 64:
+            # gather + tap-packed stem GEMM in one kernel (input never hits HBM)
+            x = torch.empty((m, win, win, 64), dtype=torch.bfloat16, device=src.device)
+            xa = torch.empty_like(x)
+            call("ig_unet_stem", *common, win, cfg.in_planes(), model.w["stem"].data_ptr(),
+                 MP_SILU_GAIN, x.data_ptr(), xa.data_ptr(), x_noisy.data_ptr(),
+                 dev.stream_ptr())
+            f = model.forward_after_stem(x, xa, sigma)
+        else:
+            x_in = torch.empty((m, win, win, cfg.cin_pad), dtype=torch.bfloat16,
+                               device=src.device)
+            call("ig_unet_gather_input", *common, x_in.data_ptr(), win, cfg.cin_pad,
+                 cfg.in_planes(), x_noisy.data_ptr(), dev.stream_ptr())
+            f = model.forward(x_in, sigma)
         call("ig_unet_output", f.data_ptr(), m, win, win, 16, x_noisy.data_ptr(), C,
              float(c_skip), float(c_out), 0, phi[k0:k0 + m].data_ptr(), dev.stream_ptr())
     return phi

@@ -238,3 +238,23 @@ def test_unet_batch_invariance():
     one = unet.unet_phi_batch(cfg, src[2:3].contiguous(), None, wxy[2:3].contiguous(), win, 1,
                               None, seed=3, steps=2)
     assert torch.equal(full[2], one[0])
+
+
+@pytest.mark.parametrize("win,outer_step", [(64, 2), (64, 1), (256, 1)])
+def test_fused_stem_matches_unfused(win, outer_step):
+    """ig_unet_stem (gather + tap-packed stem GEMM in one kernel) == gather
+    kernel + stem conv: same x_noisy bits, x / mp_silu(x) to bf16 rounding."""
+    cfg = SMALL
+    wins, xs = _phi_inputs(cfg, 3, win, seed=2)
+    wxy = torch.tensor([[b.x0, b.y0] for b in wins], dtype=torch.int64, device=DEV)
+    src = torch.from_numpy(xs).to(DEV)
+    outs = {}
+    for fused in (False, True):
+        unet.FUSED_STEM = fused
+        try:
+            outs[fused] = unet.unet_phi_batch(cfg, src, None, wxy, win, outer_step, None,
+                                              seed=2, steps=2)
+        finally:
+            unet.FUSED_STEM = True
+    d = (outs[True] - outs[False]).abs().max().item()
+    assert d <= 0.02 * outs[False].abs().max().item() + 1e-3, d
