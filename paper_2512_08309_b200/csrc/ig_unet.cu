@@ -123,6 +123,22 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 consecutive fp32 columns of this thread's TMEM lane (no wait)
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // K-major operand tile in SMEM written by TMA with SWIZZLE_128B: rows of 128 B
 // (64 bf16), 8-row (1024 B) swizzle atoms stacked along M/N.
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
@@ -1013,27 +1029,30 @@ __global__ void conv_simt_kernel(ConvArgs a, const __nv_bfloat16* __restrict__ a
 // then every thread packs one output pixel with 8 x 16-byte stores.
 constexpr int GTX = 32, GTY = 8, GPL = 8;
 
+// Evaluates the P input planes of one pixel straight into SMEM (bf16; the
+// caller zero-fills the GPL slots first).  x_noisy (f32, channel stride
+// xn_cstride) is written when xn != nullptr.
 __device__ __forceinline__ void gather_planes(
     const float* __restrict__ src, int src_batched, int64_t sx0, int64_t sy0, int sw, int sh,
     int C, int k, int win, int y, int x, int64_t X, int64_t Y, const float* __restrict__ cpar,
     int64_t cx0, int64_t cy0, int cw, int ch, int cc, int cscale, int cmask, uint64_t cprefix,
-    uint64_t rprefix, float sigma, float c_in, int first_step, float* out_planes,
-    float* x_noisy_store, int* slow) {
+    uint64_t rprefix, float sigma, float c_in, int first_step, __nv_bfloat16* out,
+    float* __restrict__ xn, int64_t xn_cstride, int* slow) {
   for (int c = 0; c < C; ++c) {
     float v;
     if (src_batched)
       v = src[(((int64_t)k * C + c) * win + y) * win + x];
     else
       v = src[((int64_t)c * sh + (Y - sy0)) * sw + (X - sx0)];
-    float xn;
+    float xv;
     if (first_step) {
-      xn = __fmul_rn(sigma, v);
+      xv = __fmul_rn(sigma, v);
     } else {
       const float z = noise_value(rprefix, X, Y, (uint32_t)c, slow);
-      xn = __fadd_rn(v, __fmul_rn(sigma, z));
+      xv = __fadd_rn(v, __fmul_rn(sigma, z));
     }
-    if (x_noisy_store) x_noisy_store[c] = xn;
-    out_planes[c] = __fmul_rn(c_in, xn);
+    if (xn) xn[c * xn_cstride] = xv;
+    out[c] = __float2bfloat16_rn(__fmul_rn(c_in, xv));
   }
   int plane = C;
   if (cc > 0) {
@@ -1045,15 +1064,13 @@ __device__ __forceinline__ void gather_planes(
       for (int j = 0; j < cc; ++j) {
         float v = cpar[j * pl + py * cw + px];
         if (mval < 1.f) v = noise_value(cprefix, X, Y, (uint32_t)j, slow);
-        out_planes[plane + j] = v;
+        out[plane + j] = __float2bfloat16_rn(v);
       }
-    } else {
-      for (int j = 0; j < cc; ++j) out_planes[plane + j] = 0.f;
     }
     plane += cc;
-    out_planes[plane++] = mval;
+    out[plane++] = __float2bfloat16_rn(mval);
   }
-  out_planes[plane++] = 1.f;
+  out[plane] = __float2bfloat16_rn(1.f);
 }
 
 __global__ void __launch_bounds__(GTX * GTY) unet_gather_kernel(
@@ -1062,9 +1079,10 @@ __global__ void __launch_bounds__(GTX * GTY) unet_gather_kernel(
     int64_t cy0, int cw, int ch, int cc, int cscale, int cmask, uint64_t cprefix,
     uint64_t rprefix, float sigma, float c_in, int first_step, __nv_bfloat16* __restrict__ x_in,
     int win, int cin_pad, int P, float* __restrict__ x_noisy) {
-  __shared__ __nv_bfloat16 tile[(GTY + 2) * (GTX + 2)][GPL];
+  __shared__ __align__(16) __nv_bfloat16 tile[(GTY + 2) * (GTX + 2)][GPL];
   const int tiles_x = (win + GTX - 1) / GTX, tiles_y = (win + GTY - 1) / GTY;
   const int64_t ntiles = (int64_t)n * tiles_x * tiles_y;
+  const int64_t plane_px = (int64_t)win * win;
   int slow = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int k = (int)(t / (tiles_x * tiles_y));
@@ -1075,20 +1093,15 @@ __global__ void __launch_bounds__(GTX * GTY) unet_gather_kernel(
     for (int q = threadIdx.x; q < (GTY + 2) * (GTX + 2); q += blockDim.x) {
       const int hy = q / (GTX + 2), hx = q - hy * (GTX + 2);
       const int y = ty0 + hy - 1, x = tx0 + hx - 1;
-      float pl[GPL];
-#pragma unroll
-      for (int i = 0; i < GPL; ++i) pl[i] = 0.f;
+      *reinterpret_cast<uint4*>(tile[q]) = make_uint4(0, 0, 0, 0);
       if (y >= 0 && y < win && x >= 0 && x < win) {
         const bool interior = hy >= 1 && hy <= GTY && hx >= 1 && hx <= GTX;
-        float xn[GPL];
         gather_planes(src, src_batched, sx0, sy0, sw, sh, C, k, win, y, x, WX + x, WY + y, cpar,
                       cx0, cy0, cw, ch, cc, cscale, cmask, cprefix, rprefix, sigma, c_in,
-                      first_step, pl, interior ? xn : nullptr, &slow);
-        if (interior)
-          for (int c = 0; c < C; ++c) x_noisy[(((int64_t)k * C + c) * win + y) * win + x] = xn[c];
+                      first_step, tile[q],
+                      interior ? x_noisy + ((int64_t)k * C * win + y) * win + x : nullptr,
+                      plane_px, &slow);
       }
-#pragma unroll
-      for (int i = 0; i < GPL; ++i) tile[q][i] = __float2bfloat16_rn(pl[i]);
     }
     __syncthreads();
     // phase 2: pack the 3x3 neighbourhood of each output pixel
@@ -1112,12 +1125,15 @@ __global__ void __launch_bounds__(GTX * GTY) unet_gather_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// Fused input gather + stem: one CTA per 128-pixel tile of a window.
+// Fused input gather + stem.  One CTA owns a strip of `strip` 128-pixel tiles
+// stacked vertically (tile = trows x tw pixels, tw = min(win, 128)):
 //   1. the P input planes (c_in*x_noisy with the consistency renoise,
-//      conditioning planes + mask, constant plane) of the tile and its 1-pixel
-//      halo are evaluated into SMEM (f32);
-//   2. every thread packs its pixel's 3x3 neighbourhood (9*P <= 64 channels,
-//      zero outside the window) straight into the SWIZZLE_128B K-major layout
+//      conditioning planes + mask, constant plane) of the whole strip and its
+//      1-pixel halo are evaluated once into SMEM (bf16, GPL slots/position);
+//      the halo overhead is (rows+2)(tw+2)/(rows*tw) = 1.27x for 8x128;
+//   2. per tile, every thread packs its pixel's 3x3 neighbourhood (9*P <= 64
+//      channels, zero outside the window; P is a template parameter so the
+//      packing is register-only) straight into the SWIZZLE_128B K-major layout
 //      the tensor core reads (chunk c of row m at m*128 + ((c ^ (m&7)) * 16));
 //   3. one elected thread issues 4 x tcgen05.mma (M=128, N=64, K=16) against
 //      the SMEM-resident stem weights, commit -> mbarrier;
@@ -1125,29 +1141,33 @@ __global__ void __launch_bounds__(GTX * GTY) unet_gather_kernel(
 //      x and mp_silu(x) (bf16 NHWC).
 // The packed input never touches HBM (the unfused path wrote and re-read
 // 128 B per pixel).
-constexpr int STEM_N = 64;
+constexpr int STEM_N = 64, STEM_PLANES_MAX = 1300;   // 10 x 130 (8 rows of 128 + halo)
 
+template <int P>
 __global__ void __launch_bounds__(128) unet_stem_kernel(
     const float* __restrict__ src, int src_batched, int64_t sx0, int64_t sy0, int sw, int sh,
     int C, const int64_t* __restrict__ wxy, int n, const float* __restrict__ cpar, int64_t cx0,
     int64_t cy0, int cw, int ch, int cc, int cscale, int cmask, uint64_t cprefix,
-    uint64_t rprefix, float sigma, float c_in, int first_step, int win, int P,
+    uint64_t rprefix, float sigma, float c_in, int first_step, int win, int strip,
     const __nv_bfloat16* __restrict__ wstem, float act_gain, __nv_bfloat16* __restrict__ out_x,
     __nv_bfloat16* __restrict__ out_xa, float* __restrict__ x_noisy) {
+  static_assert(9 * P <= 64 && P <= GPL, "stem: planes do not tap-pack into 64 channels");
   __shared__ __align__(1024) uint8_t sA[128 * 128];       // packed A tile (SW128)
   __shared__ __align__(1024) uint8_t sB[STEM_N * 128];    // stem weights (SW128)
-  __shared__ float planes[390 * GPL];   // (rows+2) x (cols+2) x P; max 3 x 130 (w >= 128)
+  __shared__ __align__(16) __nv_bfloat16 planes[STEM_PLANES_MAX * GPL];
   __shared__ uint64_t mma_bar;
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int tw = win < 128 ? win : 128;           // tile width in pixels
   const int trows = 128 / tw;                     // image rows per tile
-  const int tiles_per_win = win * win / 128;
-  const int k = blockIdx.x / tiles_per_win;
-  const int tr = blockIdx.x - k * tiles_per_win;
-  const int y0 = (tr * 128) / win, x0 = (tr * 128) % win;
+  const int srows = strip * trows;                // image rows per strip
+  const int col_blocks = win / tw, row_strips = win / srows;
+  const int k = blockIdx.x / (col_blocks * row_strips);
+  const int r = blockIdx.x - k * col_blocks * row_strips;
+  const int y0 = (r / col_blocks) * srows, x0 = (r % col_blocks) * tw;
   const int hw = tw + 2;
   const int64_t WX = wxy[2 * k], WY = wxy[2 * k + 1];
+  const int64_t plane_px = (int64_t)win * win;
   int slow = 0;
 
   if (warp == 0) {
@@ -1166,90 +1186,112 @@ __global__ void __launch_bounds__(128) unet_stem_kernel(
     const uint4 v = __ldg(reinterpret_cast<const uint4*>(wstem + row * 64 + c * 8));
     *reinterpret_cast<uint4*>(sB + row * 128 + ((c ^ (row & 7)) * 16)) = v;
   }
-  // 1. planes of the tile + halo
-  const int npos = (trows + 2) * hw;
+  // 1. planes of the strip + halo
+  const int npos = (srows + 2) * hw;
   for (int q = tid; q < npos; q += 128) {
     const int hy = q / hw, hx = q - hy * hw;
     const int y = y0 + hy - 1, x = x0 + hx - 1;
-    float pl[GPL];
-#pragma unroll
-    for (int i = 0; i < GPL; ++i) pl[i] = 0.f;
+    __nv_bfloat16* pq = planes + q * GPL;
+    *reinterpret_cast<uint4*>(pq) = make_uint4(0, 0, 0, 0);
     if (y >= 0 && y < win && x >= 0 && x < win) {
-      const bool interior = hy >= 1 && hy <= trows && hx >= 1 && hx <= tw;
-      float xn[GPL];
+      const bool interior = hy >= 1 && hy <= srows && hx >= 1 && hx <= tw;
       gather_planes(src, src_batched, sx0, sy0, sw, sh, C, k, win, y, x, WX + x, WY + y, cpar,
                     cx0, cy0, cw, ch, cc, cscale, cmask, cprefix, rprefix, sigma, c_in,
-                    first_step, pl, interior ? xn : nullptr, &slow);
-      if (interior)
-        for (int c = 0; c < C; ++c) x_noisy[(((int64_t)k * C + c) * win + y) * win + x] = xn[c];
+                    first_step, pq,
+                    interior ? x_noisy + ((int64_t)k * C * win + y) * win + x : nullptr,
+                    plane_px, &slow);
     }
-    for (int i = 0; i < P; ++i) planes[q * GPL + i] = pl[i];
   }
-  __syncthreads();
-  // 2. pack pixel m's 3x3 x P neighbourhood into row m of the A tile
-  {
-    const int m = tid;
-    const int ly = m / tw, lx = m - ly * tw;
-    __align__(16) __nv_bfloat16 row[64];
-#pragma unroll
-    for (int i = 0; i < 64; ++i) row[i] = __float2bfloat16_rn(0.f);
-    for (int tap = 0; tap < 9; ++tap) {
-      const int q = (ly + tap / 3) * hw + lx + tap % 3;
-      for (int p = 0; p < P; ++p) row[tap * P + p] = __float2bfloat16_rn(planes[q * GPL + p]);
-    }
-    const uint4* rv = reinterpret_cast<const uint4*>(row);
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      *reinterpret_cast<uint4*>(sA + m * 128 + ((c ^ (m & 7)) * 16)) = rv[c];
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
-  tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
-  // 3. one GEMM: [128 x 64] x [64 x 64]^T
-  if (warp == 0) {
-    if (elect_one()) {
-      const uint64_t adesc = smem_desc_sw128(smem_u32(sA));
-      const uint64_t bdesc = smem_desc_sw128(smem_u32(sB));
-      constexpr uint32_t idesc = idesc_bf16(128, STEM_N);
+  const int m = tid;                              // A row == TMEM lane == pixel of the tile
+  const int ly = m / tw, lx = m - ly * tw;
+  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+  const float hg = 0.5f * act_gain;
+  for (int j = 0; j < strip; ++j) {
+    // 2. pack pixel m's 3x3 x P neighbourhood into row m of the A tile
+    {
+      union {
+        uint4 v[8];
+        __nv_bfloat16 e[64];
+      } row;
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        tc_mma(tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, kk ? 1u : 0u);
-      tc_commit(&mma_bar);
-    }
-    __syncwarp();
-  }
-  mbar_wait(&mma_bar, 0);
-  tc_fence_after();
-  // 4. epilogue: thread m holds pixel m's 64 accumulators
-  {
-    const int m = warp * 32 + lane;
-    const int ly = m / tw, lx = m - ly * tw;
-    const int64_t p = ((int64_t)k * win + y0 + ly) * win + x0 + lx;
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
-    const float hg = 0.5f * act_gain;
+      for (int i = 0; i < 8; ++i) row.v[i] = make_uint4(0, 0, 0, 0);
+      const int q0 = (j * trows + ly) * hw + lx;
 #pragma unroll
-    for (int c0 = 0; c0 < STEM_N; c0 += 16) {
-      float v[16];
-      tmem_ld16(taddr + c0, v);
-      uint4 o[2], oa[2];
-      __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(o);
-      __nv_bfloat162* oab = reinterpret_cast<__nv_bfloat162*>(oa);
+      for (int tap = 0; tap < 9; ++tap) {
+        union {
+          uint4 v;
+          __nv_bfloat16 e[8];
+        } pv;
+        pv.v = *reinterpret_cast<const uint4*>(planes + (q0 + (tap / 3) * hw + tap % 3) * GPL);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        ob[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-        oab[i] = __floats2bfloat162_rn(gsilu(v[2 * i], hg), gsilu(v[2 * i + 1], hg));
+        for (int p = 0; p < P; ++p) row.e[tap * P + p] = pv.e[p];
       }
-      uint4* dx = reinterpret_cast<uint4*>(out_x + p * STEM_N + c0);
-      uint4* dxa = reinterpret_cast<uint4*>(out_xa + p * STEM_N + c0);
-      dx[0] = o[0];
-      dx[1] = o[1];
-      dxa[0] = oa[0];
-      dxa[1] = oa[1];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<uint4*>(sA + m * 128 + ((c ^ (m & 7)) * 16)) = row.v[c];
     }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    // 3. one GEMM: [128 x 64] x [64 x 64]^T
+    if (warp == 0) {
+      if (elect_one()) {
+        const uint64_t adesc = smem_desc_sw128(smem_u32(sA));
+        const uint64_t bdesc = smem_desc_sw128(smem_u32(sB));
+        constexpr uint32_t idesc = idesc_bf16(128, STEM_N);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc_mma(tmem, adesc + 2 * kk, bdesc + 2 * kk, idesc, kk ? 1u : 0u);
+        tc_commit(&mma_bar);
+      }
+      __syncwarp();
+    }
+    mbar_wait(&mma_bar, (uint32_t)(j & 1));
+    tc_fence_after();
+    // 4. epilogue: thread m drains pixel m's 64 accumulators, converts to
+    //    x and mp_silu(x) (bf16) and stages them, one at a time, in the A tile
+    //    the MMA has finished with (chunk-swizzled: conflict-free); the tile's
+    //    output is one contiguous 16 KB span of NHWC, copied out coalesced
+    {
+      uint32_t r[64];
+      tmem_ld32_nw(taddr, r);
+      tmem_ld32_nw(taddr + 32, r + 32);
+      tmem_wait_ld();
+      uint4 ox[8], oa[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&ox[c]);
+        __nv_bfloat162* oab = reinterpret_cast<__nv_bfloat162*>(&oa[c]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float v0 = __uint_as_float(r[8 * c + 2 * i]);
+          const float v1 = __uint_as_float(r[8 * c + 2 * i + 1]);
+          ob[i] = __floats2bfloat162_rn(v0, v1);
+          oab[i] = __floats2bfloat162_rn(gsilu(v0, hg), gsilu(v1, hg));
+        }
+      }
+      const int64_t p0 = ((int64_t)k * win + y0 + j * trows) * win + x0;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(sA + m * 128 + ((c ^ (m & 7)) * 16)) = half ? oa[c] : ox[c];
+        __syncthreads();
+        uint4* dst = reinterpret_cast<uint4*>((half ? out_xa : out_x) + p0 * STEM_N);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int q = i * 128 + tid, row = q >> 3, c = q & 7;
+          dst[q] = *reinterpret_cast<const uint4*>(sA + row * 128 + ((c ^ (row & 7)) * 16));
+        }
+        __syncthreads();
+      }
+    }
+    tc_fence_before();
   }
-  tc_fence_before();
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
@@ -1680,15 +1722,33 @@ int ig_unet_stem(const float* src, int32_t src_batched, int64_t src_x0, int64_t 
   IG_REQUIRE(n >= 0 && window > 0 && (window * window) % 128 == 0 && window <= 4096,
              "stem: window side %d unsupported (window^2 must be a multiple of 128)", window);
   IG_REQUIRE(window >= 128 || 128 % window == 0, "stem: window %d must divide 128", window);
-  IG_REQUIRE(in_planes <= 7, "stem: %d input planes do not tap-pack into 64 channels", in_planes);
+  IG_REQUIRE(in_planes >= 1 && in_planes <= 7, "stem: %d input planes do not tap-pack into 64 channels", in_planes);
   if (n == 0) return IG_OK;
-  const int64_t tiles = (int64_t)n * window * window / 128;
-  { unet_stem_kernel<<<(unsigned)tiles, 128, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
-      src, src_batched, src_x0, src_y0, src_w, src_h, channels, wxy, n, cond_parent, cond_x0,
-      cond_y0, cond_w, cond_h, cond_c, cond_scale < 1 ? 1 : cond_scale, cond_mask_channel,
-      noise_prefix(cond_seed, 101u), noise_prefix(renoise_seed, renoise_stream), sigma, c_in,
-      first_step, window, in_planes, reinterpret_cast<const __nv_bfloat16*>(w_stem), act_gain,
-      reinterpret_cast<__nv_bfloat16*>(out_x), reinterpret_cast<__nv_bfloat16*>(out_xa), x_noisy); note_launch(); }
+  const int tw = window < 128 ? window : 128, trows = 128 / tw;
+  int strip = 8;
+  while (strip > 1 && (window % (strip * trows) != 0 || (strip * trows + 2) * (tw + 2) > STEM_PLANES_MAX))
+    strip /= 2;
+  IG_REQUIRE(window % (strip * trows) == 0, "stem: window %d has no strip tiling", window);
+  const int64_t ctas = (int64_t)n * (window / tw) * (window / (strip * trows));
+  auto launch = [&](auto kern) {
+    kern<<<(unsigned)ctas, 128, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+        src, src_batched, src_x0, src_y0, src_w, src_h, channels, wxy, n, cond_parent, cond_x0,
+        cond_y0, cond_w, cond_h, cond_c, cond_scale < 1 ? 1 : cond_scale, cond_mask_channel,
+        noise_prefix(cond_seed, 101u), noise_prefix(renoise_seed, renoise_stream), sigma, c_in,
+        first_step, window, strip, reinterpret_cast<const __nv_bfloat16*>(w_stem), act_gain,
+        reinterpret_cast<__nv_bfloat16*>(out_x), reinterpret_cast<__nv_bfloat16*>(out_xa),
+        x_noisy);
+    note_launch();
+  };
+  switch (in_planes) {
+    case 1: launch(unet_stem_kernel<1>); break;
+    case 2: launch(unet_stem_kernel<2>); break;
+    case 3: launch(unet_stem_kernel<3>); break;
+    case 4: launch(unet_stem_kernel<4>); break;
+    case 5: launch(unet_stem_kernel<5>); break;
+    case 6: launch(unet_stem_kernel<6>); break;
+    default: launch(unet_stem_kernel<7>); break;
+  }
   return cuda_check("ig_unet_stem");
 }
 
