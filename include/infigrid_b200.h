@@ -177,9 +177,15 @@ typedef struct {
   /* up2 != 0: out0/out1 are [n][2h][2w][cout] and every result is written to
    * its 2x2 block (nearest-neighbour upsample fused into the epilogue) */
   int32_t up2;
+  /* up_in bit 0: act_a is [n][h/2][w/2][ca] and is read 2x nearest-upsampled;
+   * bit 1: the same for skip_a.  The upsample happens inside the TMA load
+   * (a zero-stride replicate dimension in the tensor map), so the full-res
+   * tensor is never written.  Tensor-core path: halo kernel only (w % 128 ==
+   * 0, taps == 9), otherwise IG_ERR_UNSUPPORTED; ig_conv_simt: any shape. */
+  int32_t up_in;
 } ig_conv_params_t;
 size_t ig_conv_workspace_bytes(void);
-/* 1: force the per-tap (v1) kernel for every conv; 0: halo kernel where it applies */
+/* 0: automatic; 1: force the per-tap kernel; 2: halo kernel instead of the row ring */
 int ig_conv_set_variant(int force_per_tap);
 int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream);
 /* UNet helpers (NHWC bf16 activations):

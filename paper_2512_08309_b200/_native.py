@@ -30,7 +30,7 @@ class ConvParams(ctypes.Structure):
                 ("taps", I32), ("act_a", V), ("act_b", V), ("wgt", V), ("scale", V),
                 ("bias", V), ("res", V), ("res_a", F32), ("res_b", F32), ("act_gain", F32),
                 ("out0", V), ("out1", V), ("csa", I32), ("csb", I32), ("skip_a", V),
-                ("skip_b", V), ("wskip", V), ("up2", I32)]
+                ("skip_b", V), ("wskip", V), ("up2", I32), ("up_in", I32)]
 
 
 # name -> argtypes (every function returns int32 status unless listed in _RESTYPES)

@@ -61,6 +61,15 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1) {
   asm volatile(
@@ -173,6 +182,7 @@ struct ConvArgs {
   int bw, bh, tiles_per_img, num_tiles, kchunks_a, kchunks_b;
   int kskip_a, kskip_b;   // 64-channel chunks of the fused 1x1 skip GEMM
   int up2;                // outputs replicated onto a 2x finer grid
+  int up_a, up_sa;        // act_a / skip_a read 2x nearest-upsampled from (h/2, w/2)
   const __nv_bfloat16* skip_a;
   const __nv_bfloat16* skip_b;
   const __nv_bfloat16* wskip;
@@ -534,6 +544,11 @@ struct HaloCfg {
   static constexpr int HALO_ROWS = (ROWS + 2) * 130;
   static constexpr int HALO_TX = HALO_ROWS * 128;
   static constexpr int HALO_BYTES = (HALO_TX + 1023) / 1024 * 1024;
+  // 2x-upsampled source: ROWS/2+2 low-res rows x 132 px (66 low-res px, each
+  // replicated by the tensor map's zero-stride dimension)
+  static constexpr int UP_ROWS = ROWS / 2 + 2;
+  static constexpr int UP_TX = UP_ROWS * 132 * 128;
+  static_assert(UP_TX <= HALO_BYTES, "upsampled halo box must fit the halo buffer");
   static constexpr int B_BYTES = N * 128;
   static constexpr int TMEM_COLS = (2 * ROWS * N <= 128) ? 128 : (2 * ROWS * N <= 256) ? 256 : 512;
   static constexpr int BUDGET = 220 * 1024;
@@ -637,19 +652,31 @@ __global__ void __launch_bounds__(320, 1)
           mbar_wait(&hempty[hs], hph ^ 1);
           uint8_t* dst = sH + hs * Cfg::HALO_BYTES;
           if (kc < kchunks) {
-            mbar_expect_tx(&hfull[hs], Cfg::HALO_TX);
-            if (kc < args.kchunks_a)
-              tma_load_4d(dst, &map_a, &hfull[hs], kc * 64, x0 - 1, y0 - 1, img);
-            else
-              tma_load_4d(dst, &map_b, &hfull[hs], (kc - args.kchunks_a) * 64, x0 - 1, y0 - 1,
-                          img);
+            if (kc < args.kchunks_a && args.up_a) {
+              // upsampled rows y0-1 .. y0+ROWS live in low-res rows (y0-1)>>1 ..
+              mbar_expect_tx(&hfull[hs], Cfg::UP_TX);
+              tma_load_5d(dst, &map_a, &hfull[hs], kc * 64, 0, x0 / 2 - 1, (y0 - 1) >> 1, img);
+            } else {
+              mbar_expect_tx(&hfull[hs], Cfg::HALO_TX);
+              if (kc < args.kchunks_a)
+                tma_load_4d(dst, &map_a, &hfull[hs], kc * 64, x0 - 1, y0 - 1, img);
+              else
+                tma_load_4d(dst, &map_b, &hfull[hs], (kc - args.kchunks_a) * 64, x0 - 1, y0 - 1,
+                            img);
+            }
           } else {
             const int ks = kc - kchunks;
-            mbar_expect_tx(&hfull[hs], SKIP_TX);
-            if (ks < args.kskip_a)
-              tma_load_4d(dst, &map_sa, &hfull[hs], ks * 64, x0, y0, img);
-            else
-              tma_load_4d(dst, &map_sb, &hfull[hs], (ks - args.kskip_a) * 64, x0, y0, img);
+            if (ks < args.kskip_a && args.up_sa) {
+              // the tile's ROWS (<= 2, y0 even when 2) upsampled rows are one low-res row
+              mbar_expect_tx(&hfull[hs], 128 * 128);
+              tma_load_5d(dst, &map_sa, &hfull[hs], ks * 64, 0, x0 / 2, y0 >> 1, img);
+            } else {
+              mbar_expect_tx(&hfull[hs], SKIP_TX);
+              if (ks < args.kskip_a)
+                tma_load_4d(dst, &map_sa, &hfull[hs], ks * 64, x0, y0, img);
+              else
+                tma_load_4d(dst, &map_sb, &hfull[hs], (ks - args.kskip_a) * 64, x0, y0, img);
+            }
           }
           if (++hs == 2) { hs = 0; hph ^= 1; }
           if (!ha.resident) {
@@ -681,11 +708,15 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d0 = tmem_base + acc * ROWS * N;
+        const int y0 = ((tile % tiles_per_img) / ha.tiles_x) * ROWS;
+        const int ylo0 = (y0 - 1) >> 1;
         for (int kc = 0; kc < nchunks; ++kc) {
           mbar_wait(&hfull[hs], hph);
           tc_fence_after();
           const uint32_t hbase = smem_u32(sH + hs * Cfg::HALO_BYTES);
           const bool skipc = kc >= kchunks;
+          const bool upc = skipc ? (kc - kchunks < args.kskip_a && args.up_sa)
+                                 : (kc < args.kchunks_a && args.up_a);
           const int ntaps = skipc ? 1 : 9;
           for (int tap = 0; tap < ntaps; ++tap) {
             const int dy = tap / 3, dx = tap % 3;
@@ -704,8 +735,13 @@ __global__ void __launch_bounds__(320, 1)
               for (int rr = 0; rr < ROWS; ++rr) {
                 // halo chunk: (ROWS+2) x 130 box, tap view shifted by (dy, dx);
                 // skip chunk: ROWS x 128 box, row rr
-                const uint64_t adesc = smem_desc_sw128(
-                    hbase + (skipc ? rr * 128 : (rr + dy) * 130 + dx) * 128);
+                // upsampled halo chunk: low-res row ((y0+rr+dy-1)>>1) - ylo0, pixel dx+1
+                // of the 132-px replicated row; upsampled skip chunk: one row for all rr
+                const int prow =
+                    skipc ? (upc ? 0 : rr * 128)
+                          : (upc ? (((y0 + rr + dy - 1) >> 1) - ylo0) * 132 + dx + 1
+                                 : (rr + dy) * 130 + dx);
+                const uint64_t adesc = smem_desc_sw128(hbase + prow * 128);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                   tc_mma(d0 + rr * N, adesc + 2 * k, bdesc + 2 * k, idesc,
@@ -998,8 +1034,9 @@ __global__ void conv_simt_kernel(ConvArgs a, const __nv_bfloat16* __restrict__ a
       const int yy = y + dy, xx = x + dx;
       if (yy < 0 || yy >= a.h || xx < 0 || xx >= a.w) continue;
       const int64_t q = ((int64_t)img * a.h + yy) * a.w + xx;
+      const int64_t qa = a.up_a ? ((int64_t)img * (a.h / 2) + yy / 2) * (a.w / 2) + xx / 2 : q;
       for (int ci = 0; ci < cin; ++ci) {
-        const float xv = ci < a.ca ? __bfloat162float(act_a[q * a.ca + ci])
+        const float xv = ci < a.ca ? __bfloat162float(act_a[qa * a.ca + ci])
                                    : __bfloat162float(act_b[q * a.cb + (ci - a.ca)]);
         for (int i = 0; i < 16; ++i) {
           const int co = chunk * 16 + i;
@@ -1008,8 +1045,9 @@ __global__ void conv_simt_kernel(ConvArgs a, const __nv_bfloat16* __restrict__ a
       }
     }
     const int csa = a.kskip_a * 64, csb = a.kskip_b * 64;
+    const int64_t ps = a.up_sa ? ((int64_t)img * (a.h / 2) + y / 2) * (a.w / 2) + x / 2 : p;
     for (int ci = 0; ci < csa + csb; ++ci) {     // fused 1x1 skip GEMM
-      const float xv = ci < csa ? __bfloat162float(a.skip_a[p * csa + ci])
+      const float xv = ci < csa ? __bfloat162float(a.skip_a[ps * csa + ci])
                                 : __bfloat162float(a.skip_b[p * csb + (ci - csa)]);
       for (int i = 0; i < 16; ++i)
         acc[i] += xv * __bfloat162float(a.wskip[(int64_t)(chunk * 16 + i) * (csa + csb) + ci]);
@@ -1413,6 +1451,23 @@ static int make_act_map_box(CUtensorMap* m, const void* base, int n, int h, int 
   return r == CUDA_SUCCESS ? IG_OK : IG_ERR_CUDA;
 }
 
+// low-res [n][hl][wl][c] read as its 2x nearest upsample along x: dims (c,
+// rep, x, y, n) with a zero-byte stride on `rep`, so a box of bxl low-res
+// pixels lands as 2*bxl replicated pixel rows of 128 B
+static int make_up_map(CUtensorMap* m, const void* base, int n, int hl, int wl, int c, int bxl,
+                       int brows) {
+  cuuint64_t dims[5] = {(cuuint64_t)c, 2, (cuuint64_t)wl, (cuuint64_t)hl, (cuuint64_t)n};
+  cuuint64_t strides[4] = {0, (cuuint64_t)c * 2, (cuuint64_t)wl * c * 2,
+                           (cuuint64_t)hl * wl * c * 2};
+  cuuint32_t box[5] = {64, 2, (cuuint32_t)bxl, (cuuint32_t)brows, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? IG_OK : IG_ERR_CUDA;
+}
+
 static int make_act_map(CUtensorMap* m, const void* base, int n, int h, int w, int c, int bw,
                         int bh) {
   return make_act_map_box(m, base, n, h, w, c, bw, bh);
@@ -1516,7 +1571,10 @@ template <int N, int ROWS>
 static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaStream_t st) {
   using Cfg = HaloCfg<N, ROWS>;
   CUtensorMap ma, mb, mw;
-  if (make_act_map_box(&ma, p->act_a, p->n, p->h, p->w, p->ca, 130, ROWS + 2) != IG_OK ||
+  const int hl = p->h / 2, wl = p->w / 2;
+  const int rc_a = a.up_a ? make_up_map(&ma, p->act_a, p->n, hl, wl, p->ca, 66, Cfg::UP_ROWS)
+                          : make_act_map_box(&ma, p->act_a, p->n, p->h, p->w, p->ca, 130, ROWS + 2);
+  if (rc_a != IG_OK ||
       (p->cb > 0 && make_act_map_box(&mb, p->act_b, p->n, p->h, p->w, p->cb, 130, ROWS + 2) != IG_OK) ||
       make_w_map(&mw, p->wgt, p->taps * (p->ca + p->cb), p->cout) != IG_OK) {
     set_error("ig_conv_tc(halo): cuTensorMapEncodeTiled failed");
@@ -1525,7 +1583,9 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
   if (p->cb == 0) mb = ma;
   CUtensorMap msa = ma, msb = ma, mws = mw;
   if (p->csa > 0) {
-    if (make_act_map_box(&msa, p->skip_a, p->n, p->h, p->w, p->csa, 128, ROWS) != IG_OK ||
+    const int rc_s = a.up_sa ? make_up_map(&msa, p->skip_a, p->n, hl, wl, p->csa, 64, 1)
+                             : make_act_map_box(&msa, p->skip_a, p->n, p->h, p->w, p->csa, 128, ROWS);
+    if (rc_s != IG_OK ||
         (p->csb > 0 && make_act_map_box(&msb, p->skip_b, p->n, p->h, p->w, p->csb, 128, ROWS) != IG_OK) ||
         make_w_map(&mws, p->wskip, p->csa + p->csb, p->cout) != IG_OK) {
       set_error("ig_conv_tc(halo): cuTensorMapEncodeTiled(skip) failed");
@@ -1601,6 +1661,12 @@ static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   a->skip_b = reinterpret_cast<const __nv_bfloat16*>(p->skip_b);
   a->wskip = reinterpret_cast<const __nv_bfloat16*>(p->wskip);
   a->up2 = p->up2 != 0;
+  IG_REQUIRE((p->up_in & ~3) == 0, "conv: unknown up_in bits 0x%x", p->up_in);
+  IG_REQUIRE(p->up_in == 0 || (p->h % 2 == 0 && p->w % 2 == 0 && !p->up2),
+             "conv: up_in needs even h, w (and no up2)");
+  IG_REQUIRE(!(p->up_in & 2) || p->csa > 0, "conv: up_in bit 1 without skip_a");
+  a->up_a = p->up_in & 1;
+  a->up_sa = (p->up_in >> 1) & 1;
   (void)tc;
   return IG_OK;
 }
@@ -1631,7 +1697,11 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
   const bool halo = p->taps == 9 && p->w % 128 == 0 && g_variant != 1;
-  if (halo && p->cb == 0 && p->ca == 64 && p->csa == 0 && g_variant != 2) {
+  if (p->up_in && !halo) {
+    set_error("ig_conv_tc: upsampled inputs (up_in) need the halo kernel (3x3, w %% 128 == 0)");
+    return IG_ERR_UNSUPPORTED;
+  }
+  if (halo && p->cb == 0 && p->ca == 64 && p->csa == 0 && p->up_in == 0 && g_variant != 2) {
     if (p->cout <= 128 && p->h % 2 == 0) {
       switch (p->cout) {
         case 16: return launch_conv_rows<16, 2>(p, a, st);

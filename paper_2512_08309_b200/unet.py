@@ -39,6 +39,7 @@ RES_RA = (1 - RES_T) / math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
 RES_RB = RES_T / math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
 RES_Q = 2.0                  # ra / rb
 FUSED_STEM = True            # input gather fused into the stem GEMM (ig_unet_stem)
+FUSED_UP = True              # 2x upsample folded into the consumer convs' TMA loads
 
 
 @dataclass(frozen=True)
@@ -277,9 +278,11 @@ class UNetDevice:
 
     # -- primitive launches -------------------------------------------------
     def conv(self, name, a, b, sigma, out0=True, out1=True, skip=None, wskip=None,
-             scale=None, up2=False):
+             scale=None, up2=False, up_in=0):
         cs = self.prog.convs[name]
         n, h, w, ca = a.shape
+        if up_in & 1:                 # a is the low-res tensor, read 2x upsampled
+            h, w = 2 * h, 2 * w
         cb = 0 if b is None else b.shape[3]
         assert ca + cb == cs.cin, (name, ca, cb, cs.cin)
         if scale is None and cs.modulated:
@@ -295,7 +298,7 @@ class UNetDevice:
                        self.w[name].data_ptr(), dev.ptr(scale), None, None, 0.0, 1.0,
                        MP_SILU_GAIN, dev.ptr(o0), dev.ptr(o1),
                        0 if sa is None else sa.shape[3], 0 if sb is None else sb.shape[3],
-                       dev.ptr(sa), dev.ptr(sb), dev.ptr(wskip), int(up2))
+                       dev.ptr(sa), dev.ptr(sb), dev.ptr(wskip), int(up2), int(up_in))
         conv_launch(p)
         return o0, o1
 
@@ -313,6 +316,7 @@ class UNetDevice:
         """The network after the stem: (x, mp_silu(x)) -> F."""
         skips = [(x, xa)]
         ops = self.prog.ops
+        up = 0          # (x, xa) are low-res and the next block reads them upsampled
         for k in range(1, len(ops)):
             op = ops[k]
             if op[0] == "enc":
@@ -329,16 +333,20 @@ class UNetDevice:
             elif op[0] == "dec":
                 nm = op[1]
                 s, sa = skips.pop()
-                _, h1 = self.conv(nm + ".c1", xa, sa, sigma, out0=False)
+                _, h1 = self.conv(nm + ".c1", xa, sa, sigma, out0=False, up_in=up)
                 c2 = self.prog.convs[nm + ".c2"]
                 wsk = self._skip_weights(nm, x.shape[3] + s.shape[3], c2.cout)
                 # (ConvParams.up2 can write the 2x-upsampled outputs from the
                 # epilogue directly, but its 4x scattered stores measured slower
                 # (r01: 132 vs 121 ms/step) than the separate coalesced kernel)
                 x, xa = self.conv(nm + ".c2", h1, None, sigma, skip=(x, s), wskip=wsk,
-                                  scale=self._rb(c2.cout_pad))
+                                  scale=self._rb(c2.cout_pad), up_in=2 if up else 0)
+                up = 0
             elif op[0] == "up":
-                x, xa = upsample_launch(x), upsample_launch(xa)
+                if FUSED_UP and (2 * x.shape[2]) % 128 == 0:
+                    up = 1      # upsample inside the next convs' TMA loads
+                else:
+                    x, xa = upsample_launch(x), upsample_launch(xa)
             elif op[0] == "out":
                 f, _ = self.conv("out", xa, None, sigma, out1=False)
                 return f

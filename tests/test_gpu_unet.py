@@ -258,3 +258,83 @@ def test_fused_stem_matches_unfused(win, outer_step):
             unet.FUSED_STEM = True
     d = (outs[True] - outs[False]).abs().max().item()
     assert d <= 0.02 * outs[False].abs().max().item() + 1e-3, d
+
+
+@pytest.mark.parametrize("n,h,w,ca,cb,cout,csa,csb,up_in", [
+    (2, 64, 256, 128, 64, 64, 0, 0, 1),       # dec c1 at L0: concat(up(xa), skip)
+    (2, 32, 128, 64, 0, 128, 128, 64, 2),     # dec c2: fused skip GEMM over up(x), skip
+    (1, 32, 128, 128, 64, 128, 128, 64, 3),   # both
+    (1, 16, 128, 128, 64, 256, 128, 64, 3),   # one-row tiles (cout 256)
+    (1, 8, 256, 64, 0, 16, 0, 0, 1),
+])
+def test_conv_upsampled_inputs(n, h, w, ca, cb, cout, csa, csb, up_in):
+    """up_in: act_a / skip_a are low-res and read 2x nearest-upsampled through a
+    zero-stride TMA dimension.  Must equal (bit for bit) the same conv over the
+    materialised upsample, and the CUDA-core reference under the tolerance."""
+    g = torch.Generator(device=DEV).manual_seed(h * w + ca + cout + up_in)
+
+    def rnd(*s):
+        return torch.randn(*s, device=DEV, generator=g).bfloat16()
+
+    up = lambda t: t.repeat_interleave(2, 1).repeat_interleave(2, 2).contiguous()  # noqa: E731
+    a_lo = rnd(n, h // 2, w // 2, ca) if up_in & 1 else rnd(n, h, w, ca)
+    b = rnd(n, h, w, cb) if cb else None
+    sa_lo = None
+    if csa:
+        sa_lo = rnd(n, h // 2, w // 2, csa) if up_in & 2 else rnd(n, h, w, csa)
+    sb = rnd(n, h, w, csb) if csb else None
+    wgt = (torch.randn(cout, 9 * (ca + cb), device=DEV, generator=g) /
+           math.sqrt(9 * (ca + cb))).bfloat16()
+    wsk = (torch.randn(cout, csa + csb, device=DEV, generator=g) /
+           math.sqrt(max(csa + csb, 1))).bfloat16() if csa else None
+    scale = torch.full((cout,), 0.7, device=DEV)
+
+    def run(kind, a, sa, flags):
+        o0 = torch.empty(n, h, w, cout, device=DEV, dtype=torch.bfloat16)
+        o1 = torch.empty_like(o0)
+        p = ConvParams(n, h, w, ca, cb, cout, 9, a.data_ptr(), 0 if b is None else b.data_ptr(),
+                       wgt.data_ptr(), scale.data_ptr(), 0, 0, 0.0, 1.0, 1.5, o0.data_ptr(),
+                       o1.data_ptr(), csa, csb, 0 if sa is None else sa.data_ptr(),
+                       0 if sb is None else sb.data_ptr(), 0 if wsk is None else wsk.data_ptr(),
+                       0, flags)
+        st = torch.cuda.current_stream().cuda_stream
+        check(lib().ig_conv_tc(p, None, st) if kind == "tc" else lib().ig_conv_simt(p, st))
+        torch.cuda.synchronize()
+        return o0.float(), o1.float()
+
+    a_full = up(a_lo) if up_in & 1 else a_lo
+    sa_full = (up(sa_lo) if up_in & 2 else sa_lo) if csa else None
+    fused = run("tc", a_lo, sa_lo, up_in)
+    plain = run("tc", a_full, sa_full, 0)
+    assert torch.equal(fused[0], plain[0]) and torch.equal(fused[1], plain[1])
+    ref = run("simt", a_lo, sa_lo, up_in)
+    ref_plain = run("simt", a_full, sa_full, 0)
+    assert torch.equal(ref[0], ref_plain[0])
+    tol = 0.02 * ref[0].abs().max().item() + 0.02
+    assert (fused[0] - ref[0]).abs().max().item() < tol
+
+
+def test_conv_upsampled_inputs_need_halo_kernel():
+    a = torch.zeros(1, 16, 16, 64, device=DEV, dtype=torch.bfloat16)
+    wgt = torch.zeros(64, 9 * 64, device=DEV, dtype=torch.bfloat16)
+    o = torch.empty(1, 32, 32, 64, device=DEV, dtype=torch.bfloat16)
+    p = ConvParams(1, 32, 32, 64, 0, 64, 9, a.data_ptr(), 0, wgt.data_ptr(), 0, 0, 0, 0.0, 1.0,
+                   1.0, o.data_ptr(), o.data_ptr(), 0, 0, 0, 0, 0, 0, 1)
+    with pytest.raises(ig.ConfigError):
+        check(lib().ig_conv_tc(p, None, torch.cuda.current_stream().cuda_stream))
+
+
+def test_unet_fused_upsample_is_exact():
+    """FUSED_UP (upsample inside the TMA loads) gives the same F, bit for bit."""
+    cfg = SMALL
+    wins, xs = _phi_inputs(cfg, 2, 256, seed=5)
+    wxy = torch.tensor([[b.x0, b.y0] for b in wins], dtype=torch.int64, device=DEV)
+    src = torch.from_numpy(xs).to(DEV)
+    outs = {}
+    for fused in (False, True):
+        unet.FUSED_UP = fused
+        try:
+            outs[fused] = unet.unet_phi_batch(cfg, src, None, wxy, 256, 1, None, seed=5, steps=2)
+        finally:
+            unet.FUSED_UP = True
+    assert torch.equal(outs[True], outs[False])

@@ -14,6 +14,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+from paper_2512_08309_b200 import unet  # noqa: E402
 from paper_2512_08309_b200.unet import UNetConfig, build_program  # noqa: E402
 
 
@@ -38,11 +39,13 @@ def layer_ops(cfg, win):
     """Expected launch sequence of one forward: (kind, name, h, cin, cout, taps, outs, res)."""
     prog = build_program(cfg)
     ch = cfg.channels()
-    seq = [("gather", "gather", win, 0, cfg.cin_pad, 0, 1, 0)]
-    lv = 0
+    fused = unet.FUSED_STEM
+    seq = [] if fused else [("gather", "gather", win, 0, cfg.cin_pad, 0, 1, 0)]
     h = win
+    c = ch[0]
     for op in prog.ops:
         if op[0] == "stem":
+            # fused: reads the f32 source plane(s), writes x_noisy (f32) + x/xa
             seq.append(("conv", "stem", h, cfg.cin_pad, ch[0], 1, 2, 0))
         elif op[0] == "enc":
             nm, has_skip = op[1], op[2]
@@ -51,6 +54,7 @@ def layer_ops(cfg, win):
             c2 = prog.convs[nm + ".c2"]
             # c2 with the fused skip GEMM: reads the block input (c1.cin) once more
             seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, 2, c1.cin / c2.cout))
+            c = c2.cout
         elif op[0] == "down":
             seq.append(("pool", "down", h, 0, 0, 0, 0, 0))
             h //= 2
@@ -60,9 +64,10 @@ def layer_ops(cfg, win):
             seq.append(("conv", nm + ".c1", h, c1.cin, c1.cout, 9, 1, 0))
             c2 = prog.convs[nm + ".c2"]
             seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, 2, c1.cin / c2.cout))
+            c = c2.cout
         elif op[0] == "up":
-            seq.append(("up", "up.x", h, 0, 0, 0, 0, 0))
-            seq.append(("up", "up.xa", h, 0, 0, 0, 0, 0))
+            seq.append(("up", "up.x", h, c, 0, 0, 0, 0))
+            seq.append(("up", "up.xa", h, c, 0, 0, 0, 0))
             h *= 2
         elif op[0] == "out":
             seq.append(("conv", "out", h, ch[0], 16, 9, 1, 0))
@@ -87,7 +92,7 @@ def main():
         if kind == "conv":
             by = px * 2 * (cin + cout * (outs + res))
         elif kind == "up":
-            by = px * 2 * 64 * 1.25
+            by = px * 2 * cin * 5            # read h^2 c, write (2h)^2 c
         else:
             by = 0.0
         bound = max(fl / tf, by / bw) * 1e6
