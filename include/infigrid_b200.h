@@ -192,6 +192,9 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream);
  * ig_unet_gather_input: tap-packed stem input [n][w][w][cin_pad] from window
  *   crops (+ renoise, conditioning planes, mask, constant plane) and x_noisy;
  * ig_unet_output: Phi[n][C][h][w] = c_skip * x_noisy + c_out * F[..., c];
+ * ig_unet_out_head: the output conv fused with it: F = conv3x3(xa, w_out)
+ *   ([cout_pad][9][64] bf16, rows >= C zero) in f32, never stored (cin 64,
+ *   C <= 8, w % 128 == 0, h % 4 == 0);
  * ig_avgpool2_bf16: 2x2 mean -> out and mp_silu(out);
  * ig_upsample2_bf16: nearest 2x. */
 int ig_unet_gather_input(const float* src, int32_t src_batched, int64_t src_x0, int64_t src_y0,
@@ -205,6 +208,9 @@ int ig_unet_gather_input(const float* src, int32_t src_batched, int64_t src_x0, 
 int ig_unet_output(const void* f, int32_t n, int32_t h, int32_t w, int32_t fc,
                    const float* x_noisy, int32_t channels, float c_skip, float c_out,
                    int32_t flags, float* out, void* cuda_stream);
+int ig_unet_out_head(const void* xa, int32_t n, int32_t h, int32_t w, int32_t cin,
+                     const void* w_out, int32_t cout_pad, int32_t channels, const float* x_noisy,
+                     float c_skip, float c_out, float* out, void* cuda_stream);
 int ig_avgpool2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,
                      void* out_act, void* cuda_stream);
 int ig_upsample2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,

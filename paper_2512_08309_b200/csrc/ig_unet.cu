@@ -1338,6 +1338,148 @@ __global__ void __launch_bounds__(128) unet_stem_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused output head: Phi = c_skip * x_noisy + c_out * conv3x3(xa, w_out)[:C].
+// cout is tiny (C <= 8 data channels), where a 128-row tcgen05 MMA would be
+// bound by re-reading the 16 KB A tile from SMEM for every 16-wide N.  Here
+// one TMA box of (OUT_S+2) x 130 pixels x 64 channels (SWIZZLE_128B) feeds
+// warp-level mma.sync m16n8k16 (bf16 -> f32): A fragments via ldmatrix
+// (conflict-free on the swizzled rows), all 9 taps x 4 K-steps of B held in
+// registers, and the preconditioning applied to the f32 accumulators, so F
+// is never rounded to bf16 nor written to HBM.
+constexpr int OUT_S = 4;                                   // output rows per CTA
+constexpr int OUT_BYTES = (OUT_S + 2) * 130 * 128;               // TMA box bytes
+constexpr int OUT_STRIDE = (OUT_BYTES + 1023) / 1024 * 1024;      // SW128: 1 KB aligned buffers
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16_16816(float* d, const uint32_t* a, uint32_t b0,
+                                               uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(256) unet_out_head_kernel(
+    const __grid_constant__ CUtensorMap map_xa, const __nv_bfloat16* __restrict__ wout,
+    int n, int h, int w, int C, const float* __restrict__ x_noisy, float c_skip, float c_out,
+    float* __restrict__ out) {
+  // persistent, one CTA per SM, two TMA buffers: tile k+2 loads while k+1 computes
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* buf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                            ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(buf + 2 * OUT_STRIDE);   // [2]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tiles_x = w / 128, tiles_y = h / OUT_S;
+  const int ntiles = n * tiles_x * tiles_y;
+  auto tile_xy = [&](int t, int& img, int& y0, int& x0) {
+    img = t / (tiles_x * tiles_y);
+    const int r = t - img * tiles_x * tiles_y;
+    y0 = (r / tiles_x) * OUT_S;
+    x0 = (r % tiles_x) * 128;
+  };
+  if (threadIdx.x == 0) {
+    prefetch_map(&map_xa);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < 2; ++s) {
+      const int t0 = blockIdx.x + s * gridDim.x;
+      if (t0 < ntiles) {
+        int img, y0, x0;
+        tile_xy(t0, img, y0, x0);
+        mbar_expect_tx(&bar[s], OUT_BYTES);
+        tma_load_4d(buf + s * OUT_STRIDE, &map_xa, &bar[s], 0, x0 - 1, y0 - 1, img);
+      }
+    }
+  }
+  // B fragments (k16 x n8, "col"): lane holds W[n = lane/4][tap][16 kc + 2(lane%4) + {0,1}]
+  // and the same at +8; rows n >= C are zero in the padded weights
+  uint32_t bf[9][4][2];
+  {
+    const int nn = lane / 4, kq = 2 * (lane % 4);
+    const uint32_t* wr = reinterpret_cast<const uint32_t*>(wout + (int64_t)nn * 9 * 64);
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap)
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) {
+        bf[tap][kc][0] = __ldg(wr + (tap * 64 + kc * 16 + kq) / 2);
+        bf[tap][kc][1] = __ldg(wr + (tap * 64 + kc * 16 + kq + 8) / 2);
+      }
+  }
+  __syncthreads();
+  // ldmatrix: lanes 0-7 rows 0-7 / k 0-7, 8-15 rows 8-15 / k 0-7,
+  //           16-23 rows 0-7 / k 8-15, 24-31 rows 8-15 / k 8-15
+  const int lr = (lane & 7) + ((lane >> 3) & 1) * 8, lk = lane >> 4;
+  const int g = lane / 4, t = lane % 4;
+  // warp w: OUT_S (=4) rows x 8 m-tiles of 16 px; m-tile (row = i, px0 = 16 w)
+  const int px0 = warp * 16;
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int sb = it & 1;
+    const uint32_t sbase = smem_u32(buf + sb * OUT_STRIDE);
+    int img, y0, x0;
+    tile_xy(tile, img, y0, x0);
+    // x_noisy of this lane's outputs (issued before the MMAs)
+    float xn[OUT_S][4];
+#pragma unroll
+    for (int i = 0; i < OUT_S; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = 2 * t + (j & 1);
+        const int64_t idx =
+            (((int64_t)img * C + c) * h + y0 + i) * w + x0 + px0 + g + (j >> 1) * 8;
+        xn[i][j] = c < C ? __ldg(x_noisy + idx) : 0.f;
+      }
+    mbar_wait(&bar[sb], (uint32_t)((it >> 1) & 1));
+    float acc[OUT_S][4];
+#pragma unroll
+    for (int i = 0; i < OUT_S; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap) {
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) {
+        const int chunk = kc * 2 + lk;
+        uint32_t a[OUT_S][4];
+#pragma unroll
+        for (int i = 0; i < OUT_S; ++i) {
+          const int srow = (i + tap / 3) * 130 + px0 + tap % 3 + lr;   // SMEM pixel row
+          ldsm_x4(sbase + srow * 128 + ((chunk ^ (srow & 7)) * 16), a[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < OUT_S; ++i) mma_bf16_16816(acc[i], a[i], bf[tap][kc][0], bf[tap][kc][1]);
+      }
+    }
+    // buffer consumed: refill with the next tile while the epilogue runs
+    __syncthreads();
+    if (threadIdx.x == 0 && tile + 2 * (int)gridDim.x < ntiles) {
+      int ni, ny, nx;
+      tile_xy(tile + 2 * gridDim.x, ni, ny, nx);
+      mbar_expect_tx(&bar[sb], OUT_BYTES);
+      tma_load_4d(buf + sb * OUT_STRIDE, &map_xa, &bar[sb], 0, nx - 1, ny - 1, ni);
+    }
+    // D fragment: lane holds (pixel g, ch 2t), (g, 2t+1), (g+8, 2t), (g+8, 2t+1)
+#pragma unroll
+    for (int i = 0; i < OUT_S; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = 2 * t + (j & 1);
+        if (c < C) {
+          const int64_t idx =
+              (((int64_t)img * C + c) * h + y0 + i) * w + x0 + px0 + g + (j >> 1) * 8;
+          out[idx] = __fadd_rn(__fmul_rn(c_skip, xn[i][j]), __fmul_rn(c_out, acc[i][j]));
+        }
+      }
+  }
+}
+
 __global__ void unet_output_kernel(const __nv_bfloat16* __restrict__ f, int n, int h, int w,
                                    int fc, const float* __restrict__ x_noisy, int C,
                                    float c_skip, float c_out, float* __restrict__ out) {
@@ -1820,6 +1962,36 @@ int ig_unet_stem(const float* src, int32_t src_batched, int64_t src_x0, int64_t 
     default: launch(unet_stem_kernel<7>); break;
   }
   return cuda_check("ig_unet_stem");
+}
+
+int ig_unet_out_head(const void* xa, int32_t n, int32_t h, int32_t w, int32_t cin,
+                     const void* w_out, int32_t cout_pad, int32_t channels, const float* x_noisy,
+                     float c_skip, float c_out, float* out, void* cuda_stream) {
+  IG_REQUIRE(n >= 0 && cin == 64 && cout_pad >= 8 && channels >= 1 && channels <= 8,
+             "out_head: needs 64 input channels and 1..8 output channels");
+  IG_REQUIRE(w % 128 == 0 && h % OUT_S == 0, "out_head: %dx%d not tiled by %dx128", h, w, OUT_S);
+  if (n == 0) return IG_OK;
+  if (!encode_fn()) {
+    set_error("ig_unet_out_head: cuTensorMapEncodeTiled unavailable");
+    return IG_ERR_CUDA;
+  }
+  CUtensorMap m;
+  if (make_act_map_box(&m, xa, n, h, w, cin, 130, OUT_S + 2) != IG_OK) {
+    set_error("ig_unet_out_head: cuTensorMapEncodeTiled failed");
+    return IG_ERR_CUDA;
+  }
+  const int smem = 2 * OUT_STRIDE + 1024 + 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(unet_out_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const int64_t tiles = (int64_t)n * (w / 128) * (h / OUT_S);
+  const int ctas = (int)(tiles < kNumSMs ? tiles : kNumSMs);
+  { unet_out_head_kernel<<<ctas, 256, smem, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+      m, reinterpret_cast<const __nv_bfloat16*>(w_out), n, h, w, channels, x_noisy, c_skip, c_out,
+      out); note_launch(); }
+  return cuda_check("ig_unet_out_head");
 }
 
 int ig_unet_output(const void* f, int32_t n, int32_t h, int32_t w, int32_t fc,

@@ -40,6 +40,7 @@ RES_RB = RES_T / math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
 RES_Q = 2.0                  # ra / rb
 FUSED_STEM = True            # input gather fused into the stem GEMM (ig_unet_stem)
 FUSED_UP = True              # 2x upsample folded into the consumer convs' TMA loads
+FUSED_OUT = True             # output conv + preconditioning in one kernel (ig_unet_out_head)
 
 
 @dataclass(frozen=True)
@@ -312,8 +313,12 @@ class UNetDevice:
         x, xa = self.conv("stem", x_in, None, sigma)
         return self.forward_after_stem(x, xa, sigma)
 
-    def forward_after_stem(self, x: torch.Tensor, xa: torch.Tensor, sigma: float):
-        """The network after the stem: (x, mp_silu(x)) -> F."""
+    def forward_after_stem(self, x: torch.Tensor, xa: torch.Tensor, sigma: float, head=None):
+        """The network after the stem: (x, mp_silu(x)) -> F.
+
+        head = (x_noisy, c_skip, c_out, phi): when the fused output head
+        applies, Phi = c_skip * x_noisy + c_out * F is written into phi and
+        None is returned (F is never materialised)."""
         skips = [(x, xa)]
         ops = self.prog.ops
         up = 0          # (x, xa) are low-res and the next block reads them upsampled
@@ -348,6 +353,16 @@ class UNetDevice:
                 else:
                     x, xa = upsample_launch(x), upsample_launch(xa)
             elif op[0] == "out":
+                n, h, w, c = xa.shape
+                C = self.cfg.data_channels
+                if head is not None and FUSED_OUT and c == 64 and C <= 8 and w % 128 == 0 \
+                        and h % 4 == 0:
+                    x_noisy, c_skip, c_out, phi = head
+                    call("ig_unet_out_head", xa.data_ptr(), n, h, w, c,
+                         self.w["out"].data_ptr(), self.prog.convs["out"].cout_pad, C,
+                         x_noisy.data_ptr(), float(c_skip), float(c_out), phi.data_ptr(),
+                         dev.stream_ptr())
+                    return None
                 f, _ = self.conv("out", xa, None, sigma, out1=False)
                 return f
         raise AssertionError("program without output layer")
@@ -460,15 +475,17 @@ def unet_phi_batch(cfg: UNetConfig, src: torch.Tensor, src_region: Region | None
             call("ig_unet_stem", *common, win, cfg.in_planes(), model.w["stem"].data_ptr(),
                  MP_SILU_GAIN, x.data_ptr(), xa.data_ptr(), x_noisy.data_ptr(),
                  dev.stream_ptr())
-            f = model.forward_after_stem(x, xa, sigma)
+            f = model.forward_after_stem(x, xa, sigma,
+                                         head=(x_noisy, c_skip, c_out, phi[k0:k0 + m]))
         else:
             x_in = torch.empty((m, win, win, cfg.cin_pad), dtype=torch.bfloat16,
                                device=src.device)
             call("ig_unet_gather_input", *common, x_in.data_ptr(), win, cfg.cin_pad,
                  cfg.in_planes(), x_noisy.data_ptr(), dev.stream_ptr())
             f = model.forward(x_in, sigma)
-        call("ig_unet_output", f.data_ptr(), m, win, win, 16, x_noisy.data_ptr(), C,
-             float(c_skip), float(c_out), 0, phi[k0:k0 + m].data_ptr(), dev.stream_ptr())
+        if f is not None:
+            call("ig_unet_output", f.data_ptr(), m, win, win, 16, x_noisy.data_ptr(), C,
+                 float(c_skip), float(c_out), 0, phi[k0:k0 + m].data_ptr(), dev.stream_ptr())
     return phi
 
 

@@ -338,3 +338,37 @@ def test_unet_fused_upsample_is_exact():
         finally:
             unet.FUSED_UP = True
     assert torch.equal(outs[True], outs[False])
+
+
+@pytest.mark.parametrize("outer_step", [2, 1])
+def test_unet_fused_out_head(outer_step):
+    """ig_unet_out_head (mma.sync output conv + preconditioning, F kept in f32)
+    vs the tcgen05 out conv (F rounded to bf16) + ig_unet_output: equal up to
+    the bf16 rounding of F (|c_out| * 2^-8 |F|)."""
+    cfg = SMALL
+    wins, xs = _phi_inputs(cfg, 3, 256, seed=9)
+    wxy = torch.tensor([[b.x0, b.y0] for b in wins], dtype=torch.int64, device=DEV)
+    src = torch.from_numpy(xs).to(DEV)
+    outs = {}
+    for fused in (False, True):
+        unet.FUSED_OUT = fused
+        try:
+            outs[fused] = unet.unet_phi_batch(cfg, src, None, wxy, 256, outer_step, None,
+                                              seed=9, steps=2)
+        finally:
+            unet.FUSED_OUT = True
+    sigma = cfg.sigma_for(outer_step, 2)
+    _, c_out, _, _ = unet.precond(cfg, sigma)
+    d = (outs[True] - outs[False]).abs().max().item()
+    fmax = ((outs[False].abs().max().item()) + 1.0)
+    assert d <= abs(c_out) * fmax * 2 ** -7 + 1e-4, (d, c_out)
+    assert not torch.equal(outs[True], outs[False]) or c_out == 0
+
+
+def test_out_head_rejects_unsupported_shapes():
+    z = torch.zeros(1, 64, 64, 64, device=DEV, dtype=torch.bfloat16)
+    wo = torch.zeros(16, 9 * 64, device=DEV, dtype=torch.bfloat16)
+    xn = torch.zeros(1, 1, 64, 64, device=DEV)
+    with pytest.raises(ig.ShapeError):
+        call("ig_unet_out_head", z.data_ptr(), 1, 64, 64, 64, wo.data_ptr(), 16, 1,
+             xn.data_ptr(), 1.0, 1.0, xn.data_ptr(), torch.cuda.current_stream().cuda_stream)
