@@ -66,12 +66,17 @@ def layer_ops(cfg, win):
             seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, 2, c1.cin / c2.cout))
             c = c2.cout
         elif op[0] == "up":
-            seq.append(("up", "up.x", h, c, 0, 0, 0, 0))
-            seq.append(("up", "up.xa", h, c, 0, 0, 0, 0))
+            if not (unet.FUSED_UP and (2 * h) % 128 == 0):   # else folded into the TMA loads
+                seq.append(("up", "up.x", h, c, 0, 0, 0, 0))
+                seq.append(("up", "up.xa", h, c, 0, 0, 0, 0))
             h *= 2
         elif op[0] == "out":
-            seq.append(("conv", "out", h, ch[0], 16, 9, 1, 0))
-            seq.append(("output", "output", h, 0, 0, 0, 0, 0))
+            if unet.FUSED_OUT and h % 4 == 0 and h % 128 == 0:
+                # mma.sync head: real cout = data_channels; writes Phi (f32)
+                seq.append(("conv", "out_head", h, ch[0], cfg.data_channels, 9, 0, 0))
+            else:
+                seq.append(("conv", "out", h, ch[0], 16, 9, 1, 0))
+                seq.append(("output", "output", h, 0, 0, 0, 0, 0))
     return seq
 
 
