@@ -796,6 +796,322 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ---------------------------------------------------------------------------
+// ig_conv_tc, CTA-pair variant of the halo kernel (cta_group::2): a cluster of
+// two CTAs on two SMs computes M = 256 pixels (each CTA its own 2 x 128-pixel
+// tile) x N = cout per tcgen05.mma.cta_group::2 issued by the even (leader)
+// CTA.  Each CTA stages its OWN halo box (A, 128 rows per MMA) and HALF of the
+// weight tile (N/2 rows): per SM the tensor core reads 4 KB (A) + N/2 x 32 B (B)
+// of SMEM per K=16 step instead of 4 KB + N x 32 B, which is what limits the
+// N = 64 layers (SMEM bandwidth, not the tensor core) in the one-CTA kernel.
+//   * every TMA of both CTAs completes on the LEADER's full barriers
+//     (.cta_group::2 form); the leader arms them with both CTAs' bytes;
+//   * MMA completion is committed with .multicast::cluster to the "empty" /
+//     "tmem full" barriers of both CTAs (mask 0b11);
+//   * both CTAs' epilogue warps release an accumulator on the leader's
+//     "tmem empty" barrier (one remote arrive per warp).
+// Same tile order and epilogue as conv_halo_kernel<N, 2>; tile 2p + rank.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// shared::cluster address of `p` in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void tma2_load_4d(void* dst, const CUtensorMap* map, uint32_t bar,
+                                             int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_load_5d(void* dst, const CUtensorMap* map, uint32_t bar,
+                                             int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_load_2d(void* dst, const CUtensorMap* map, uint32_t bar,
+                                             int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit2_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int N>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
+    conv_halo2_kernel(const __grid_constant__ CUtensorMap map_a,
+                      const __grid_constant__ CUtensorMap map_b,
+                      const __grid_constant__ CUtensorMap map_w,
+                      const __grid_constant__ CUtensorMap map_sa,
+                      const __grid_constant__ CUtensorMap map_sb,
+                      const __grid_constant__ CUtensorMap map_ws, const HaloArgs ha) {
+  constexpr int ROWS = 2;
+  using Cfg = HaloCfg<N, ROWS>;
+  constexpr int BH = N / 2;                    // weight rows staged by this CTA
+  constexpr int BH_BYTES = BH * 128;
+  const ConvArgs args = ha.c;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int kchunks = args.kchunks_a + args.kchunks_b;
+  const int kskip = args.kskip_a + args.kskip_b;
+  const int nchunks = kchunks + kskip;
+  constexpr uint32_t SKIP_TX = ROWS * 128 * 128;
+  const int nb = ha.resident ? 9 * kchunks + kskip : ha.b_stages;
+  uint8_t* sH = smem;
+  uint8_t* sB = smem + 2 * Cfg::HALO_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + nb * BH_BYTES);
+  uint64_t* hfull = bars;          // [2]  (leader's used)
+  uint64_t* hempty = bars + 2;     // [2]  (each CTA's own)
+  uint64_t* tfull = bars + 4;      // [2]  (each CTA's own)
+  uint64_t* tempty = bars + 6;     // [2]  (leader's used)
+  uint64_t* wfull = bars + 8;      // [1]  (leader's used)
+  uint64_t* bfull = bars + 9;      // [b_stages] (leader's used)
+  uint64_t* bempty = bfull + ha.b_stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + ha.b_stages);
+  float* s_scale = reinterpret_cast<float*>(tmem_slot + 4);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tiles_per_img = ha.tiles_x * ha.tiles_y;
+  const int npairs = args.num_tiles / 2;
+  const int pair0 = blockIdx.x / 2, pstride = gridDim.x / 2;
+  if (args.scale && threadIdx.x >= 64)
+    for (int c = threadIdx.x - 64; c < N; c += 256) s_scale[c] = args.scale[c];
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_a);
+    if (args.kchunks_b) prefetch_map(&map_b);
+    prefetch_map(&map_w);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&hfull[s], 1);
+      mbar_init(&hempty[s], 1);
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 16);            // 8 epilogue warps x 2 CTAs
+    }
+    mbar_init(wfull, 1);
+    for (int s = 0; s < ha.b_stages; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();                          // peer barriers initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs) ----------------
+      const uint32_t l_hfull0 = mapa_u32(&hfull[0], 0), l_hfull1 = mapa_u32(&hfull[1], 0);
+      const uint32_t l_wfull = mapa_u32(wfull, 0);
+      const int brow = (int)rank * BH;
+      if (ha.resident) {
+        if (leader) mbar_expect_tx(wfull, (uint32_t)(2 * (9 * kchunks + kskip) * BH_BYTES));
+        for (int t = 0; t < 9 * kchunks; ++t) {
+          const int tap = t / kchunks, kc = t - tap * kchunks;
+          tma2_load_2d(sB + t * BH_BYTES, &map_w, l_wfull, tap * (args.ca + args.cb) + kc * 64,
+                       brow);
+        }
+        for (int ks = 0; ks < kskip; ++ks)
+          tma2_load_2d(sB + (9 * kchunks + ks) * BH_BYTES, &map_ws, l_wfull, ks * 64, brow);
+      }
+      int hs = 0, bs = 0;
+      uint32_t hph = 0, bph = 0;
+      for (int pr = pair0; pr < npairs; pr += pstride) {
+        const int tile = 2 * pr + (int)rank;
+        const int img = tile / tiles_per_img;
+        const int r = tile - img * tiles_per_img;
+        const int ty = r / ha.tiles_x;
+        const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
+        for (int kc = 0; kc < nchunks; ++kc) {
+          mbar_wait(&hempty[hs], hph ^ 1);
+          uint8_t* dst = sH + hs * Cfg::HALO_BYTES;
+          const uint32_t hb = hs ? l_hfull1 : l_hfull0;
+          if (kc < kchunks) {
+            if (kc < args.kchunks_a && args.up_a) {
+              if (leader) mbar_expect_tx(&hfull[hs], 2 * Cfg::UP_TX);
+              tma2_load_5d(dst, &map_a, hb, kc * 64, 0, x0 / 2 - 1, (y0 - 1) >> 1, img);
+            } else {
+              if (leader) mbar_expect_tx(&hfull[hs], 2 * Cfg::HALO_TX);
+              if (kc < args.kchunks_a)
+                tma2_load_4d(dst, &map_a, hb, kc * 64, x0 - 1, y0 - 1, img);
+              else
+                tma2_load_4d(dst, &map_b, hb, (kc - args.kchunks_a) * 64, x0 - 1, y0 - 1, img);
+            }
+          } else {
+            const int ks = kc - kchunks;
+            if (ks < args.kskip_a && args.up_sa) {
+              if (leader) mbar_expect_tx(&hfull[hs], 2 * 128 * 128);
+              tma2_load_5d(dst, &map_sa, hb, ks * 64, 0, x0 / 2, y0 >> 1, img);
+            } else {
+              if (leader) mbar_expect_tx(&hfull[hs], 2 * SKIP_TX);
+              if (ks < args.kskip_a)
+                tma2_load_4d(dst, &map_sa, hb, ks * 64, x0, y0, img);
+              else
+                tma2_load_4d(dst, &map_sb, hb, (ks - args.kskip_a) * 64, x0, y0, img);
+            }
+          }
+          if (++hs == 2) { hs = 0; hph ^= 1; }
+          if (!ha.resident) {
+            const int ntaps = kc < kchunks ? 9 : 1;
+            for (int tap = 0; tap < ntaps; ++tap) {
+              mbar_wait(&bempty[bs], bph ^ 1);
+              if (leader) mbar_expect_tx(&bfull[bs], 2 * BH_BYTES);
+              const uint32_t bb = mapa_u32(&bfull[bs], 0);
+              if (kc < kchunks)
+                tma2_load_2d(sB + bs * BH_BYTES, &map_w, bb, tap * (args.ca + args.cb) + kc * 64,
+                             brow);
+              else
+                tma2_load_2d(sB + bs * BH_BYTES, &map_ws, bb, (kc - kchunks) * 64, brow);
+              if (++bs == ha.b_stages) { bs = 0; bph ^= 1; }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // ---------------- MMA issuer (leader CTA only) ----------------
+      constexpr uint32_t idesc = idesc_bf16(256, N);
+      if (ha.resident) mbar_wait(wfull, 0);
+      int hs = 0, bs = 0;
+      uint32_t hph = 0, bph = 0;
+      int it = 0;
+      for (int pr = pair0; pr < npairs; pr += pstride, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + acc * ROWS * N;
+        const int tile = 2 * pr;               // both tiles of the pair share y0 parity
+        const int y0 = ((tile % tiles_per_img) / ha.tiles_x) * ROWS;
+        const int ylo0 = (y0 - 1) >> 1;
+        for (int kc = 0; kc < nchunks; ++kc) {
+          mbar_wait(&hfull[hs], hph);
+          tc_fence_after();
+          const uint32_t hbase = smem_u32(sH + hs * Cfg::HALO_BYTES);
+          const bool skipc = kc >= kchunks;
+          const bool upc = skipc ? (kc - kchunks < args.kskip_a && args.up_sa)
+                                 : (kc < args.kchunks_a && args.up_a);
+          const int ntaps = skipc ? 1 : 9;
+          for (int tap = 0; tap < ntaps; ++tap) {
+            const int dy = tap / 3, dx = tap % 3;
+            uint32_t baddr;
+            if (ha.resident) {
+              baddr = smem_u32(sB + (skipc ? 9 * kchunks + (kc - kchunks) : tap * kchunks + kc) *
+                                        BH_BYTES);
+            } else {
+              mbar_wait(&bfull[bs], bph);
+              tc_fence_after();
+              baddr = smem_u32(sB + bs * BH_BYTES);
+            }
+            const uint64_t bdesc = smem_desc_sw128(baddr);
+            if (elect_one()) {
+#pragma unroll
+              for (int rr = 0; rr < ROWS; ++rr) {
+                const int prow =
+                    skipc ? (upc ? 0 : rr * 128)
+                          : (upc ? (((y0 + rr + dy - 1) >> 1) - ylo0) * 132 + dx + 1
+                                 : (rr + dy) * 130 + dx);
+                const uint64_t adesc = smem_desc_sw128(hbase + prow * 128);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  tc_mma2(d0 + rr * N, adesc + 2 * k, bdesc + 2 * k, idesc,
+                          (kc | tap | k) ? 1u : 0u);
+              }
+              if (!ha.resident) tc_commit2_mc(&bempty[bs]);
+            }
+            __syncwarp();
+            if (!ha.resident) {
+              if (++bs == ha.b_stages) { bs = 0; bph ^= 1; }
+            }
+          }
+          if (elect_one()) tc_commit2_mc(&hempty[hs]);
+          __syncwarp();
+          if (++hs == 2) { hs = 0; hph ^= 1; }
+        }
+        if (elect_one()) tc_commit2_mc(&tfull[acc]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..9, both CTAs) ----------------
+    const int quarter = warp & 3;
+    const int grp = (warp - 2) >> 2;  // accumulator row 0 or 1
+    const int m = quarter * 32 + lane;
+    const uint32_t l_tempty0 = mapa_u32(&tempty[0], 0), l_tempty1 = mapa_u32(&tempty[1], 0);
+    int it = 0;
+    for (int pr = pair0; pr < npairs; pr += pstride, ++it) {
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int tile = 2 * pr + (int)rank;
+      const int img = tile / tiles_per_img;
+      const int r = tile - img * tiles_per_img;
+      const int ty = r / ha.tiles_x;
+      const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
+      const int64_t p = ((int64_t)img * args.h + y0 + grp) * args.w + x0 + m;
+      const uint32_t taddr =
+          tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N + grp * N;
+      epi_span<N>(args, args.scale ? s_scale : nullptr, p, 0, taddr);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc ? l_tempty1 : l_tempty0);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();                          // no CTA leaves while its peer may signal it
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(Cfg::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // ig_conv_tc, row-ring variant (3x3, one 64-channel input chunk, width a
 // multiple of 128).  Each CTA walks a contiguous strip of tiles ordered
 // (image, column, row-pair), so consecutive tiles are vertically adjacent and
@@ -1769,7 +2085,82 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
   return cuda_check("ig_conv_tc(halo)");
 }
 
-static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring
+static int make_w_map_rows(CUtensorMap* m, const void* base, int ktot, int cout, int brows) {
+  cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)cout};
+  cuuint64_t strides[1] = {(cuuint64_t)ktot * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)brows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? IG_OK : IG_ERR_CUDA;
+}
+
+template <int N>
+static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaStream_t st) {
+  constexpr int ROWS = 2;
+  using Cfg = HaloCfg<N, ROWS>;
+  constexpr int BH_BYTES = N / 2 * 128;
+  CUtensorMap ma, mb, mw;
+  const int hl = p->h / 2, wl = p->w / 2;
+  const int rc_a = a.up_a ? make_up_map(&ma, p->act_a, p->n, hl, wl, p->ca, 66, Cfg::UP_ROWS)
+                          : make_act_map_box(&ma, p->act_a, p->n, p->h, p->w, p->ca, 130, ROWS + 2);
+  if (rc_a != IG_OK ||
+      (p->cb > 0 && make_act_map_box(&mb, p->act_b, p->n, p->h, p->w, p->cb, 130, ROWS + 2) != IG_OK) ||
+      make_w_map_rows(&mw, p->wgt, p->taps * (p->ca + p->cb), p->cout, N / 2) != IG_OK) {
+    set_error("ig_conv_tc(halo2): cuTensorMapEncodeTiled failed");
+    return IG_ERR_CUDA;
+  }
+  if (p->cb == 0) mb = ma;
+  CUtensorMap msa = ma, msb = ma, mws = mw;
+  if (p->csa > 0) {
+    const int rc_s = a.up_sa ? make_up_map(&msa, p->skip_a, p->n, hl, wl, p->csa, 64, 1)
+                             : make_act_map_box(&msa, p->skip_a, p->n, p->h, p->w, p->csa, 128, ROWS);
+    if (rc_s != IG_OK ||
+        (p->csb > 0 && make_act_map_box(&msb, p->skip_b, p->n, p->h, p->w, p->csb, 128, ROWS) != IG_OK) ||
+        make_w_map_rows(&mws, p->wskip, p->csa + p->csb, p->cout, N / 2) != IG_OK) {
+      set_error("ig_conv_tc(halo2): cuTensorMapEncodeTiled(skip) failed");
+      return IG_ERR_CUDA;
+    }
+  }
+  HaloArgs ha;
+  ha.c = a;
+  ha.tiles_x = p->w / 128;
+  ha.tiles_y = p->h / ROWS;
+  ha.c.num_tiles = p->n * ha.tiles_x * ha.tiles_y;
+  const int kchunks = a.kchunks_a + a.kchunks_b;
+  const int wbytes = (9 * kchunks + a.kskip_a + a.kskip_b) * BH_BYTES;
+  const int fixed = 1024 + 2 * Cfg::HALO_BYTES + 512 + 1024;
+  int smem;
+  if (fixed + wbytes <= Cfg::BUDGET) {
+    ha.resident = 1;
+    ha.b_stages = 1;
+    smem = fixed + wbytes;
+  } else {
+    ha.resident = 0;
+    int stages = (Cfg::BUDGET - fixed) / BH_BYTES;
+    if (stages > 16) stages = 16;
+    if (stages < 2) {
+      set_error("ig_conv_tc(halo2): no room for the weight ring");
+      return IG_ERR_UNSUPPORTED;
+    }
+    ha.b_stages = stages;
+    smem = fixed + stages * BH_BYTES;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(conv_halo2_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    attr = true;
+  }
+  int grid = ha.c.num_tiles < kNumSMs ? ha.c.num_tiles : kNumSMs;
+  grid &= ~1;
+  { conv_halo2_kernel<N><<<grid, Cfg::THREADS, smem, st>>>(ma, mb, mw, msa, msb, mws, ha); note_launch(); }
+  return cuda_check("ig_conv_tc(halo2)");
+}
+
+static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs
 
 static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   IG_REQUIRE(p && p->n > 0 && p->h > 0 && p->w > 0, "conv: empty problem");
@@ -1822,7 +2213,7 @@ extern "C" {
 size_t ig_conv_workspace_bytes(void) { return 0; }
 
 // 0: automatic; 1: per-tap kernel only; 2: halo kernel instead of the row
-// ring (tests / A-B timing)
+// ring; 3: one-CTA halo kernel instead of CTA pairs (tests / A-B timing)
 int ig_conv_set_variant(int variant) {
   g_variant = variant;
   return IG_OK;
@@ -1860,6 +2251,9 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
       }
     }
   }
+  if (halo && p->cout == 64 && p->h % 2 == 0 && g_variant != 3 &&
+      ((int64_t)p->n * (p->w / 128) * (p->h / 2)) % 2 == 0)
+    return launch_conv_halo2<64>(p, a, st);
   if (halo && p->cout <= 128 && p->h % 2 == 0) {
     switch (p->cout) {
       case 16: return launch_conv_halo<16, 2>(p, a, st);

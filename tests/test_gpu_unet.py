@@ -372,3 +372,48 @@ def test_out_head_rejects_unsupported_shapes():
     with pytest.raises(ig.ShapeError):
         call("ig_unet_out_head", z.data_ptr(), 1, 64, 64, 64, wo.data_ptr(), 16, 1,
              xn.data_ptr(), 1.0, 1.0, xn.data_ptr(), torch.cuda.current_stream().cuda_stream)
+
+
+@pytest.mark.parametrize("n,h,w,ca,cb,csa,csb,up_in", [
+    (2, 64, 256, 64, 0, 0, 0, 0),
+    (1, 32, 256, 128, 64, 0, 0, 0),        # streamed weight ring (3 chunks)
+    (2, 16, 128, 64, 0, 64, 0, 0),         # fused identity skip
+    (1, 32, 256, 128, 64, 128, 64, 3),     # upsampled act_a + skip_a
+    (3, 8, 128, 64, 64, 128, 64, 0),
+])
+def test_conv_cta_pair_matches_single_cta(n, h, w, ca, cb, csa, csb, up_in):
+    """cout = 64 halo convs run as CTA pairs (tcgen05.mma.cta_group::2, M=256):
+    bit-identical to the one-CTA halo kernel (same K order per output)."""
+    g = torch.Generator(device=DEV).manual_seed(n * h + w + ca + csa + up_in)
+
+    def rnd(*s):
+        return torch.randn(*s, device=DEV, generator=g).bfloat16()
+
+    cout = 64
+    a = rnd(n, h // 2, w // 2, ca) if up_in & 1 else rnd(n, h, w, ca)
+    b = rnd(n, h, w, cb) if cb else None
+    sa = (rnd(n, h // 2, w // 2, csa) if up_in & 2 else rnd(n, h, w, csa)) if csa else None
+    sb = rnd(n, h, w, csb) if csb else None
+    wgt = (torch.randn(cout, 9 * (ca + cb), device=DEV, generator=g) /
+           math.sqrt(9 * (ca + cb))).bfloat16()
+    wsk = (torch.randn(cout, csa + csb, device=DEV, generator=g) /
+           math.sqrt(max(csa + csb, 1))).bfloat16() if csa else None
+    scale = torch.rand(cout, device=DEV, generator=g) + 0.5
+    res = {}
+    for variant in (3, 0):
+        o0 = torch.empty(n, h, w, cout, device=DEV, dtype=torch.bfloat16)
+        o1 = torch.empty_like(o0)
+        p = ConvParams(n, h, w, ca, cb, cout, 9, a.data_ptr(), 0 if b is None else b.data_ptr(),
+                       wgt.data_ptr(), scale.data_ptr(), 0, 0, 0.0, 1.0, 1.5, o0.data_ptr(),
+                       o1.data_ptr(), csa, csb, 0 if sa is None else sa.data_ptr(),
+                       0 if sb is None else sb.data_ptr(), 0 if wsk is None else wsk.data_ptr(),
+                       0, up_in)
+        check(lib().ig_conv_set_variant(variant))
+        try:
+            check(lib().ig_conv_tc(p, None, torch.cuda.current_stream().cuda_stream))
+            torch.cuda.synchronize()
+        finally:
+            check(lib().ig_conv_set_variant(0))
+        res[variant] = (o0, o1)
+    assert torch.equal(res[0][0], res[3][0]) and torch.equal(res[0][1], res[3][1])
+    assert res[0][0].abs().sum().item() > 0
