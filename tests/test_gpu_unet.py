@@ -381,15 +381,15 @@ def test_out_head_rejects_unsupported_shapes():
     (1, 32, 256, 128, 64, 128, 64, 3),     # upsampled act_a + skip_a
     (3, 8, 128, 64, 64, 128, 64, 0),
 ])
-def test_conv_cta_pair_matches_single_cta(n, h, w, ca, cb, csa, csb, up_in):
-    """cout = 64 halo convs run as CTA pairs (tcgen05.mma.cta_group::2, M=256):
-    bit-identical to the one-CTA halo kernel (same K order per output)."""
+@pytest.mark.parametrize("cout", [64, 128])
+def test_conv_cta_pair_matches_single_cta(n, h, w, ca, cb, csa, csb, up_in, cout):
+    """cout = 64 / 128 halo convs run as CTA pairs (tcgen05.mma.cta_group::2,
+    M=256): bit-identical to the one-CTA halo kernel (same K order per output)."""
     g = torch.Generator(device=DEV).manual_seed(n * h + w + ca + csa + up_in)
 
     def rnd(*s):
         return torch.randn(*s, device=DEV, generator=g).bfloat16()
 
-    cout = 64
     a = rnd(n, h // 2, w // 2, ca) if up_in & 1 else rnd(n, h, w, ca)
     b = rnd(n, h, w, cb) if cb else None
     sa = (rnd(n, h // 2, w // 2, csa) if up_in & 2 else rnd(n, h, w, csa)) if csa else None
