@@ -560,6 +560,7 @@ struct HaloArgs {
   int resident;      // weights resident in SMEM
   int b_stages;      // streamed weight ring depth (when !resident)
   int tiles_x, tiles_y;
+  int hbufs;         // halo buffers in the ring (CTA-pair kernel: 2 or 3)
 };
 
 template <int N, int ROWS>
@@ -825,9 +826,11 @@ __device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// (default .release.cta semantics: a .cluster release would fence every
+// outstanding global store of the epilogue -- MEMBAR.ALL.GPU -- before the
+// accumulator could be handed back; the MMA warp reads none of them)
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void tma2_load_4d(void* dst, const CUtensorMap* map, uint32_t bar,
                                              int c0, int c1, int c2, int c3) {
@@ -896,14 +899,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   constexpr uint32_t SKIP_TX = ROWS * 128 * 128;
   const int nb = ha.resident ? 9 * kchunks + kskip : ha.b_stages;
   uint8_t* sH = smem;
-  uint8_t* sB = smem + 2 * Cfg::HALO_BYTES;
+  uint8_t* sB = smem + ha.hbufs * Cfg::HALO_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + nb * BH_BYTES);
-  uint64_t* hfull = bars;          // [2]  (leader's used)
-  uint64_t* hempty = bars + 2;     // [2]  (each CTA's own)
-  uint64_t* tfull = bars + 4;      // [2]  (each CTA's own)
-  uint64_t* tempty = bars + 6;     // [2]  (leader's used)
-  uint64_t* wfull = bars + 8;      // [1]  (leader's used)
-  uint64_t* bfull = bars + 9;      // [b_stages] (leader's used)
+  const int HB = ha.hbufs;
+  uint64_t* hfull = bars;          // [HB] (leader's used)
+  uint64_t* hempty = bars + 4;     // [HB] (each CTA's own)
+  uint64_t* tfull = bars + 8;      // [2]  (each CTA's own)
+  uint64_t* tempty = bars + 10;    // [2]  (leader's used)
+  uint64_t* wfull = bars + 12;     // [1]  (leader's used)
+  uint64_t* bfull = bars + 13;     // [b_stages] (leader's used)
   uint64_t* bempty = bfull + ha.b_stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + ha.b_stages);
   float* s_scale = reinterpret_cast<float*>(tmem_slot + 4);
@@ -919,9 +923,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     prefetch_map(&map_a);
     if (args.kchunks_b) prefetch_map(&map_b);
     prefetch_map(&map_w);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < HB; ++s) {
       mbar_init(&hfull[s], 1);
       mbar_init(&hempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 16);            // 8 epilogue warps x 2 CTAs
     }
@@ -946,7 +952,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs) ----------------
-      const uint32_t l_hfull0 = mapa_u32(&hfull[0], 0), l_hfull1 = mapa_u32(&hfull[1], 0);
       const uint32_t l_wfull = mapa_u32(wfull, 0);
       const int brow = (int)rank * BH;
       if (ha.resident) {
@@ -970,7 +975,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         for (int kc = 0; kc < nchunks; ++kc) {
           mbar_wait(&hempty[hs], hph ^ 1);
           uint8_t* dst = sH + hs * Cfg::HALO_BYTES;
-          const uint32_t hb = hs ? l_hfull1 : l_hfull0;
+          const uint32_t hb = mapa_u32(&hfull[hs], 0);
           if (kc < kchunks) {
             if (kc < args.kchunks_a && args.up_a) {
               if (leader) mbar_expect_tx(&hfull[hs], 2 * Cfg::UP_TX);
@@ -995,7 +1000,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                 tma2_load_4d(dst, &map_sb, hb, (ks - args.kskip_a) * 64, x0, y0, img);
             }
           }
-          if (++hs == 2) { hs = 0; hph ^= 1; }
+          if (++hs == HB) { hs = 0; hph ^= 1; }
           if (!ha.resident) {
             const int ntaps = kc < kchunks ? 9 : 1;
             for (int tap = 0; tap < ntaps; ++tap) {
@@ -1071,7 +1076,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           }
           if (elect_one()) tc_commit2_mc(&hempty[hs]);
           __syncwarp();
-          if (++hs == 2) { hs = 0; hph ^= 1; }
+          if (++hs == HB) { hs = 0; hph ^= 1; }
         }
         if (elect_one()) tc_commit2_mc(&tfull[acc]);
         __syncwarp();
@@ -2085,6 +2090,8 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
   return cuda_check("ig_conv_tc(halo)");
 }
 
+static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
+                            // 4 CTA pairs with three halo buffers
 static int make_w_map_rows(CUtensorMap* m, const void* base, int ktot, int cout, int brows) {
   cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)cout};
   cuuint64_t strides[1] = {(cuuint64_t)ktot * 2};
@@ -2131,22 +2138,33 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   ha.c.num_tiles = p->n * ha.tiles_x * ha.tiles_y;
   const int kchunks = a.kchunks_a + a.kchunks_b;
   const int wbytes = (9 * kchunks + a.kskip_a + a.kskip_b) * BH_BYTES;
-  const int fixed = 1024 + 2 * Cfg::HALO_BYTES + 512 + 1024;
-  int smem;
-  if (fixed + wbytes <= Cfg::BUDGET) {
-    ha.resident = 1;
-    ha.b_stages = 1;
-    smem = fixed + wbytes;
-  } else {
-    ha.resident = 0;
-    int stages = (Cfg::BUDGET - fixed) / BH_BYTES;
-    if (stages > 16) stages = 16;
-    if (stages < 2) {
-      set_error("ig_conv_tc(halo2): no room for the weight ring");
-      return IG_ERR_UNSUPPORTED;
+  // two halo buffers with resident weights where they fit (variant 4: try
+  // three buffers, the next tile's box streaming in during the whole tile)
+  constexpr int kBudget = 226 * 1024;
+  int smem = 0;
+  ha.hbufs = 0;
+  // (r01: three buffers measured slower -- the weights then stream per tile)
+  for (int hb = (g_variant == 4 ? 3 : 2); hb >= 2 && !ha.hbufs; --hb) {
+    const int fixed = 1024 + hb * Cfg::HALO_BYTES + 512 + 1024;
+    if (fixed + wbytes <= kBudget) {
+      ha.hbufs = hb;
+      ha.resident = 1;
+      ha.b_stages = 1;
+      smem = fixed + wbytes;
+    } else {
+      int stages = (kBudget - fixed) / BH_BYTES;
+      if (stages > 16) stages = 16;
+      if (stages >= (hb == 3 ? 4 : 2)) {
+        ha.hbufs = hb;
+        ha.resident = 0;
+        ha.b_stages = stages;
+        smem = fixed + stages * BH_BYTES;
+      }
     }
-    ha.b_stages = stages;
-    smem = fixed + stages * BH_BYTES;
+  }
+  if (!ha.hbufs) {
+    set_error("ig_conv_tc(halo2): no room for the weight ring");
+    return IG_ERR_UNSUPPORTED;
   }
   static bool attr = false;
   if (!attr) {
@@ -2160,7 +2178,6 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   return cuda_check("ig_conv_tc(halo2)");
 }
 
-static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs
 
 static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   IG_REQUIRE(p && p->n > 0 && p->h > 0 && p->w > 0, "conv: empty problem");
@@ -2213,7 +2230,8 @@ extern "C" {
 size_t ig_conv_workspace_bytes(void) { return 0; }
 
 // 0: automatic; 1: per-tap kernel only; 2: halo kernel instead of the row
-// ring; 3: one-CTA halo kernel instead of CTA pairs (tests / A-B timing)
+// ring; 3: one-CTA halo kernel instead of CTA pairs; 4: CTA pairs with three
+// halo buffers (tests / A-B timing)
 int ig_conv_set_variant(int variant) {
   g_variant = variant;
   return IG_OK;
