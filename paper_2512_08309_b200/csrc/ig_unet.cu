@@ -37,8 +37,13 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// Relaxed arrive: used only to hand a drained TMEM accumulator back to the MMA
+// warp (the tcgen05.ld's have completed and tcgen05.fence::before_thread_sync
+// precedes it).  A release arrive would add a MEMBAR that waits for the
+// epilogue's outstanding global stores, which nobody on the other side reads.
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
@@ -826,11 +831,12 @@ __device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
-// (default .release.cta semantics: a .cluster release would fence every
-// outstanding global store of the epilogue -- MEMBAR.ALL.GPU -- before the
-// accumulator could be handed back; the MMA warp reads none of them)
+// (relaxed, as mbar_arrive: a .release.cluster arrive fenced every outstanding
+// global store of the epilogue -- MEMBAR.ALL.GPU -- before the accumulator
+// could be handed back; the MMA warp reads none of them)
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
 }
 __device__ __forceinline__ void tma2_load_4d(void* dst, const CUtensorMap* map, uint32_t bar,
                                              int c0, int c1, int c2, int c3) {
