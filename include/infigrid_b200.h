@@ -183,6 +183,13 @@ typedef struct {
    * tensor is never written.  Tensor-core path: halo kernel only (w % 128 ==
    * 0, taps == 9), otherwise IG_ERR_UNSUPPORTED; ig_conv_simt: any shape. */
   int32_t up_in;
+  /* gutter bit 0: act_a, act_b, skip_a, skip_b, res, out0 and out1 use the
+   * gutter layout [n][h][w+2][c] (zero columns at x = -1 and x = w; widths
+   * <= 64): every 3x3 tap is then a 1-D shift over the h*(w+2) positions of
+   * an image, so narrow levels run the CTA-pair halo kernel with one 1-D
+   * halo box per chunk; the outputs' gutter columns are written as zeros.
+   * bit 1: the up_in (low-res) sources are in the gutter layout. */
+  int32_t gutter;
 } ig_conv_params_t;
 size_t ig_conv_workspace_bytes(void);
 /* 0: automatic; 1: force the per-tap kernel; 2: halo kernel instead of the row ring */
@@ -196,7 +203,9 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream);
  *   ([cout_pad][9][64] bf16, rows >= C zero) in f32, never stored (cin 64,
  *   C <= 8, w % 128 == 0, h % 4 == 0);
  * ig_avgpool2_bf16: 2x2 mean -> out and mp_silu(out);
- * ig_upsample2_bf16: nearest 2x. */
+ * ig_upsample2_bf16: nearest 2x.
+ * layout (pool / upsample): bit 0 input, bit 1 output in the gutter layout
+ * [n][h][w+2][c] of ig_conv_params_t.gutter (zero columns written). */
 int ig_unet_gather_input(const float* src, int32_t src_batched, int64_t src_x0, int64_t src_y0,
                          int32_t src_w, int32_t src_h, int32_t channels, const int64_t* wxy,
                          int32_t n, const float* cond_parent, int64_t cond_x0, int64_t cond_y0,
@@ -212,9 +221,9 @@ int ig_unet_out_head(const void* xa, int32_t n, int32_t h, int32_t w, int32_t ci
                      const void* w_out, int32_t cout_pad, int32_t channels, const float* x_noisy,
                      float c_skip, float c_out, float* out, void* cuda_stream);
 int ig_avgpool2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,
-                     void* out_act, void* cuda_stream);
+                     void* out_act, int32_t layout, void* cuda_stream);
 int ig_upsample2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,
-                      void* cuda_stream);
+                      int32_t layout, void* cuda_stream);
 /* Fused UNet input gather + stem convolution (64 output channels): builds the
  * tap-packed input planes of each 128-pixel tile in SMEM (window crops of the
  * source canvas/batch, consistency renoise, conditioning + mask, constant

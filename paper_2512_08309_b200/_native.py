@@ -30,7 +30,8 @@ class ConvParams(ctypes.Structure):
                 ("taps", I32), ("act_a", V), ("act_b", V), ("wgt", V), ("scale", V),
                 ("bias", V), ("res", V), ("res_a", F32), ("res_b", F32), ("act_gain", F32),
                 ("out0", V), ("out1", V), ("csa", I32), ("csb", I32), ("skip_a", V),
-                ("skip_b", V), ("wskip", V), ("up2", I32), ("up_in", I32)]
+                ("skip_b", V), ("wskip", V), ("up2", I32), ("up_in", I32),
+                ("gutter", I32)]
 
 
 # name -> argtypes (every function returns int32 status unless listed in _RESTYPES)
@@ -65,8 +66,8 @@ SIGNATURES = {
     "ig_unet_stem": [V, I32, I64, I64, I32, I32, I32, V, I32, V, I64, I64, I32, I32, I32, I32,
                      I32, U64, U64, U32, F32, F32, I32, I32, I32, V, F32, V, V, V, V],
     "ig_unet_out_head": [V, I32, I32, I32, I32, V, I32, I32, V, F32, F32, V, V],
-    "ig_avgpool2_bf16": [V, I32, I32, I32, I32, V, V, V],
-    "ig_upsample2_bf16": [V, I32, I32, I32, I32, V, V],
+    "ig_avgpool2_bf16": [V, I32, I32, I32, I32, V, V, I32, V],
+    "ig_upsample2_bf16": [V, I32, I32, I32, I32, V, I32, V],
 }
 _RESTYPES = {"ig_last_error": c_char_p, "ig_abi_version": c_int32,
              "ig_launch_count": ctypes.c_longlong,

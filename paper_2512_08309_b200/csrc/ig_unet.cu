@@ -188,6 +188,9 @@ struct ConvArgs {
   int kskip_a, kskip_b;   // 64-channel chunks of the fused 1x1 skip GEMM
   int up2;                // outputs replicated onto a 2x finer grid
   int up_a, up_sa;        // act_a / skip_a read 2x nearest-upsampled from (h/2, w/2)
+  int gut;                // activations in the gutter layout [n][h][w+2][c] (see ig_conv_tc)
+  int gut_up;             // the upsampled (up_in) sources are in the gutter layout
+  int gP;                 // gutter layout: positions per image, h * (w + 2)
   const __nv_bfloat16* skip_a;
   const __nv_bfloat16* skip_b;
   const __nv_bfloat16* wskip;
@@ -234,7 +237,8 @@ __device__ __forceinline__ void store_out(const ConvArgs& a, __nv_bfloat16* base
 }
 
 // epilogue of one 16-channel chunk for pixel p
-__device__ __forceinline__ void epi_chunk(const ConvArgs& a, int64_t p, int c0, const float* acc) {
+__device__ __forceinline__ void epi_chunk(const ConvArgs& a, int64_t p, int c0, const float* acc,
+                                          bool zero = false) {
   float y[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i)
@@ -250,6 +254,10 @@ __device__ __forceinline__ void epi_chunk(const ConvArgs& a, int64_t p, int c0, 
       y[i] = a.res_a * __bfloat162float(rb0[i]) + a.res_b * y[i];
       y[i + 8] = a.res_a * __bfloat162float(rb1[i]) + a.res_b * y[i + 8];
     }
+  }
+  if (zero) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) y[i] = 0.f;
   }
   if (a.out0) {
     uint4 o[2];
@@ -287,7 +295,7 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
 // identity), fused mp_sum / mp_silu, 16-byte stores.
 template <int NC>
 __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale, int64_t p,
-                                         int c0, uint32_t taddr) {
+                                         int c0, uint32_t taddr, bool zero = false) {
   constexpr int BC = NC < 32 ? NC : 32;
   const int64_t off = p * a.cout + c0;
   const int64_t ob0 = out_base(a, p) + c0;
@@ -342,6 +350,10 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
           y[8 * i + 2 * j + 1] = fmaf(a.res_a, f.y, a.res_b * y[8 * i + 2 * j + 1]);
         }
       }
+    }
+    if (zero) {   // gutter column of the gutter layout: keep it zero (= conv padding)
+#pragma unroll
+      for (int i = 0; i < BC; ++i) y[i] = 0.f;
     }
     if (a.out0) {
 #pragma unroll
@@ -854,6 +866,14 @@ __device__ __forceinline__ void tma2_load_5d(void* dst, const CUtensorMap* map, 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void tma2_load_3d(void* dst, const CUtensorMap* map, uint32_t bar,
+                                             int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void tma2_load_2d(void* dst, const CUtensorMap* map, uint32_t bar,
                                              int c0, int c1) {
   asm volatile(
@@ -881,7 +901,20 @@ __device__ __forceinline__ void tc_commit2_mc(uint64_t* bar) {
       : "memory");
 }
 
-template <int N>
+// Gutter layout (GUT, narrow images w <= 64): activations are [n][h][w+2][c]
+// with zero columns at x = -1 and x = w, so over the per-image sequence of
+// h*(w+2) positions every 3x3 tap is a pure 1-D shift (dy-1)*(w+2) + (dx-1)
+// and the image's top/bottom padding is the TMA's out-of-range zero fill.  A
+// tile is ROWS x 128 consecutive positions (accumulator row rr = positions
+// rr*128 ..); its halo is ONE 1-D range of gboxes(ROWS) x 136 positions from
+// which all 9 taps of both rows are descriptor views, so narrow levels get the
+// same A reuse as the 2-D halo kernel.  The epilogue keeps gutter positions
+// at zero and drops positions past the image.
+constexpr int GBOX = 136;                    // positions per gutter TMA box (8-row aligned)
+// boxes per gutter halo: ROWS*128 + 2(w+3) positions, w <= 64
+__host__ __device__ constexpr int gboxes(int rows) { return rows == 1 ? 2 : 3; }
+
+template <int N, int ROWS, bool GUT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     conv_halo2_kernel(const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b,
@@ -889,8 +922,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                       const __grid_constant__ CUtensorMap map_sa,
                       const __grid_constant__ CUtensorMap map_sb,
                       const __grid_constant__ CUtensorMap map_ws, const HaloArgs ha) {
-  constexpr int ROWS = 2;
   using Cfg = HaloCfg<N, ROWS>;
+  constexpr int HBYTES = GUT ? gboxes(ROWS) * GBOX * 128 : Cfg::HALO_BYTES;
   constexpr int BH = N / 2;                    // weight rows staged by this CTA
   constexpr int BH_BYTES = BH * 128;
   const ConvArgs args = ha.c;
@@ -905,7 +938,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   constexpr uint32_t SKIP_TX = ROWS * 128 * 128;
   const int nb = ha.resident ? 9 * kchunks + kskip : ha.b_stages;
   uint8_t* sH = smem;
-  uint8_t* sB = smem + ha.hbufs * Cfg::HALO_BYTES;
+  uint8_t* sB = smem + ha.hbufs * HBYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + nb * BH_BYTES);
   const int HB = ha.hbufs;
   uint64_t* hfull = bars;          // [HB] (leader's used)
@@ -920,7 +953,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles_per_img = ha.tiles_x * ha.tiles_y;
-  const int npairs = args.num_tiles / 2;
+  const int npairs = (args.num_tiles + 1) / 2;   // odd count (GUT): the last tile is a dummy
   const int pair0 = blockIdx.x / 2, pstride = gridDim.x / 2;
   if (args.scale && threadIdx.x >= 64)
     for (int c = threadIdx.x - 64; c < N; c += 256) s_scale[c] = args.scale[c];
@@ -980,9 +1013,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
         for (int kc = 0; kc < nchunks; ++kc) {
           mbar_wait(&hempty[hs], hph ^ 1);
-          uint8_t* dst = sH + hs * Cfg::HALO_BYTES;
+          uint8_t* dst = sH + hs * HBYTES;
           const uint32_t hb = mapa_u32(&hfull[hs], 0);
-          if (kc < kchunks) {
+          if constexpr (GUT) {
+            // (a dummy tile has img == n: out of range, zero filled, bytes still counted)
+            const int q0 = r * ROWS * 128;
+            if (kc < kchunks) {
+              if (leader) mbar_expect_tx(&hfull[hs], 2 * HBYTES);
+              const CUtensorMap* m = kc < args.kchunks_a ? &map_a : &map_b;
+              const int c = (kc < args.kchunks_a ? kc : kc - args.kchunks_a) * 64;
+              const int start = q0 - (args.w + 3);
+#pragma unroll
+              for (int bx = 0; bx < gboxes(ROWS); ++bx)
+                tma2_load_3d(dst + bx * GBOX * 128, m, hb, c, start + bx * GBOX, img);
+            } else {
+              const int ks = kc - kchunks;
+              if (leader) mbar_expect_tx(&hfull[hs], 2 * ROWS * 128 * 128);
+              if (ks < args.kskip_a)
+                tma2_load_3d(dst, &map_sa, hb, ks * 64, q0, img);
+              else
+                tma2_load_3d(dst, &map_sb, hb, (ks - args.kskip_a) * 64, q0, img);
+            }
+          } else if (kc < kchunks) {
             if (kc < args.kchunks_a && args.up_a) {
               if (leader) mbar_expect_tx(&hfull[hs], 2 * Cfg::UP_TX);
               tma2_load_5d(dst, &map_a, hb, kc * 64, 0, x0 / 2 - 1, (y0 - 1) >> 1, img);
@@ -1043,7 +1095,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         for (int kc = 0; kc < nchunks; ++kc) {
           mbar_wait(&hfull[hs], hph);
           tc_fence_after();
-          const uint32_t hbase = smem_u32(sH + hs * Cfg::HALO_BYTES);
+          const uint32_t hbase = smem_u32(sH + hs * HBYTES);
           const bool skipc = kc >= kchunks;
           const bool upc = skipc ? (kc - kchunks < args.kskip_a && args.up_sa)
                                  : (kc < args.kchunks_a && args.up_a);
@@ -1064,9 +1116,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
 #pragma unroll
               for (int rr = 0; rr < ROWS; ++rr) {
                 const int prow =
-                    skipc ? (upc ? 0 : rr * 128)
-                          : (upc ? (((y0 + rr + dy - 1) >> 1) - ylo0) * 132 + dx + 1
-                                 : (rr + dy) * 130 + dx);
+                    GUT ? rr * 128 + (skipc ? 0 : dy * (args.w + 2) + dx)
+                    : skipc ? (upc ? 0 : rr * 128)
+                            : (upc ? (((y0 + rr + dy - 1) >> 1) - ylo0) * 132 + dx + 1
+                                   : (rr + dy) * 130 + dx);
                 const uint64_t adesc = smem_desc_sw128(hbase + prow * 128);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
@@ -1102,12 +1155,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       const int tile = 2 * pr + (int)rank;
       const int img = tile / tiles_per_img;
       const int r = tile - img * tiles_per_img;
-      const int ty = r / ha.tiles_x;
-      const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
-      const int64_t p = ((int64_t)img * args.h + y0 + grp) * args.w + x0 + m;
-      const uint32_t taddr =
-          tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N + grp * N;
-      epi_span<N>(args, args.scale ? s_scale : nullptr, p, 0, taddr);
+      if constexpr (GUT) {
+        // ROWS = 2: warp group g drains accumulator row g; ROWS = 1: the two
+        // warp groups split the columns of the one row
+        constexpr int NC = ROWS == 2 ? N : N / 2;
+        const int row = ROWS == 2 ? grp : 0;
+        const int q = (r * ROWS + row) * 128 + m;
+        if (img < args.n && q < args.gP) {
+          const int col = q % (args.w + 2);
+          const uint32_t taddr =
+              tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N + row * N;
+          epi_span<NC>(args, args.scale ? s_scale : nullptr, (int64_t)img * args.gP + q,
+                       ROWS == 2 ? 0 : grp * NC, taddr, col == 0 || col == args.w + 1);
+        }
+      } else {
+        const int ty = r / ha.tiles_x;
+        const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
+        const int64_t p = ((int64_t)img * args.h + y0 + grp) * args.w + x0 + m;
+        const uint32_t taddr =
+            tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N + grp * N;
+        epi_span<N>(args, args.scale ? s_scale : nullptr, p, 0, taddr);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc ? l_tempty1 : l_tempty0);
@@ -1345,23 +1413,42 @@ __global__ void __launch_bounds__(320, 1)
 __global__ void conv_simt_kernel(ConvArgs a, const __nv_bfloat16* __restrict__ act_a,
                                  const __nv_bfloat16* __restrict__ act_b,
                                  const __nv_bfloat16* __restrict__ wgt) {
-  const int64_t total = (int64_t)a.n * a.h * a.w * (a.cout / 16);
+  // one thread per (output position, 16-channel chunk); positions are pixels,
+  // or in the gutter layout the h x (w+2) grid including the zero columns
+  const int64_t per_img = a.gut ? (int64_t)a.gP : (int64_t)a.h * a.w;
+  const int64_t total = (int64_t)a.n * per_img * (a.cout / 16);
   const int cin = a.ca + a.cb;
+  const int wl = a.w / 2, hl = a.h / 2;
+  const int lpitch = a.gut_up ? wl + 2 : wl;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int chunk = (int)(idx % (a.cout / 16));
     const int64_t p = idx / (a.cout / 16);
-    const int img = (int)(p / ((int64_t)a.h * a.w));
-    const int rem = (int)(p - (int64_t)img * a.h * a.w);
-    const int y = rem / a.w, x = rem - (rem / a.w) * a.w;
+    const int img = (int)(p / per_img);
+    const int rem = (int)(p - img * per_img);
+    const int pitch = a.gut ? a.w + 2 : a.w;
+    const int y = rem / pitch, xg = rem - (rem / pitch) * pitch;
+    const int x = a.gut ? xg - 1 : xg;
     float acc[16];
     for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+    const bool gutter_col = a.gut && (x < 0 || x >= a.w);
+    if (gutter_col) {
+      epi_chunk(a, p, chunk * 16, acc, true);
+      continue;
+    }
+    auto full_at = [&](int yy, int xx) -> int64_t {
+      return a.gut ? (int64_t)img * a.gP + (int64_t)yy * (a.w + 2) + xx + 1
+                   : ((int64_t)img * a.h + yy) * a.w + xx;
+    };
+    auto low_at = [&](int yy, int xx) -> int64_t {
+      return ((int64_t)img * hl + yy / 2) * lpitch + xx / 2 + (a.gut_up ? 1 : 0);
+    };
     for (int tap = 0; tap < a.taps; ++tap) {
       const int dy = a.taps == 9 ? tap / 3 - 1 : 0, dx = a.taps == 9 ? tap % 3 - 1 : 0;
       const int yy = y + dy, xx = x + dx;
       if (yy < 0 || yy >= a.h || xx < 0 || xx >= a.w) continue;
-      const int64_t q = ((int64_t)img * a.h + yy) * a.w + xx;
-      const int64_t qa = a.up_a ? ((int64_t)img * (a.h / 2) + yy / 2) * (a.w / 2) + xx / 2 : q;
+      const int64_t q = full_at(yy, xx);
+      const int64_t qa = a.up_a ? low_at(yy, xx) : q;
       for (int ci = 0; ci < cin; ++ci) {
         const float xv = ci < a.ca ? __bfloat162float(act_a[qa * a.ca + ci])
                                    : __bfloat162float(act_b[q * a.cb + (ci - a.ca)]);
@@ -1372,7 +1459,7 @@ __global__ void conv_simt_kernel(ConvArgs a, const __nv_bfloat16* __restrict__ a
       }
     }
     const int csa = a.kskip_a * 64, csb = a.kskip_b * 64;
-    const int64_t ps = a.up_sa ? ((int64_t)img * (a.h / 2) + y / 2) * (a.w / 2) + x / 2 : p;
+    const int64_t ps = a.up_sa ? low_at(y, x) : p;
     for (int ci = 0; ci < csa + csb; ++ci) {     // fused 1x1 skip GEMM
       const float xv = ci < csa ? __bfloat162float(a.skip_a[ps * csa + ci])
                                 : __bfloat162float(a.skip_b[p * csb + (ci - csa)]);
@@ -1823,71 +1910,87 @@ __global__ void unet_output_kernel(const __nv_bfloat16* __restrict__ f, int n, i
   }
 }
 
+// layout bit 0: input in the gutter layout [n][h][w+2][c]; bit 1: output in
+// the gutter layout (its zero columns are written too)
 __global__ void avgpool2_kernel(const __nv_bfloat16* __restrict__ in, int n, int h, int w, int c,
                                 float gain, __nv_bfloat16* __restrict__ out,
-                                __nv_bfloat16* __restrict__ out_act) {
+                                __nv_bfloat16* __restrict__ out_act, int layout) {
   // one output row per CTA iteration: no 64-bit divisions in the inner loop
+  const int ig = layout & 1, og = (layout >> 1) & 1;
   const int oh = h / 2, ow = w / 2;
+  const int ip = w + 2 * ig, op = ow + 2 * og;
   const int c8 = c / 8;
-  const int row_items = ow * c8;
+  const int row_items = op * c8;
   const int rows = n * oh;
+  const float hg = 0.5f * gain;
   for (int row = blockIdx.x; row < rows; row += gridDim.x) {
     const int img = row / oh, oy = row - (row / oh) * oh;
-    const __nv_bfloat16* r0 = in + ((int64_t)img * h + 2 * oy) * w * c;
-    const __nv_bfloat16* r1 = r0 + (int64_t)w * c;
-    __nv_bfloat16* o0 = out + (int64_t)row * ow * c;
-    __nv_bfloat16* o1 = out_act + (int64_t)row * ow * c;
+    const __nv_bfloat16* r0 = in + (((int64_t)img * h + 2 * oy) * ip + ig) * c;
+    const __nv_bfloat16* r1 = r0 + (int64_t)ip * c;
+    __nv_bfloat16* o0 = out + (int64_t)row * op * c;
+    __nv_bfloat16* o1 = out_act + (int64_t)row * op * c;
     for (int q = threadIdx.x; q < row_items; q += blockDim.x) {
-      const int ox = q / c8, cv = q - ox * c8;
-      const int64_t off = (int64_t)(2 * ox) * c + cv * 8;
-      const uint4 va = __ldg(reinterpret_cast<const uint4*>(r0 + off));
-      const uint4 vb = __ldg(reinterpret_cast<const uint4*>(r0 + off + c));
-      const uint4 vc = __ldg(reinterpret_cast<const uint4*>(r1 + off));
-      const uint4 vd = __ldg(reinterpret_cast<const uint4*>(r1 + off + c));
-      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&va);
-      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&vb);
-      const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&vc);
-      const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&vd);
-      uint4 o, oa;
-      __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
-      __nv_bfloat162* oab = reinterpret_cast<__nv_bfloat162*>(&oa);
-      const float hg = 0.5f * gain;
+      const int oxg = q / c8, cv = q - oxg * c8;
+      const int ox = oxg - og;
+      uint4 o = make_uint4(0, 0, 0, 0), oa = make_uint4(0, 0, 0, 0);
+      if (ox >= 0 && ox < ow) {
+        const int64_t off = (int64_t)(2 * ox) * c + cv * 8;
+        const uint4 va = __ldg(reinterpret_cast<const uint4*>(r0 + off));
+        const uint4 vb = __ldg(reinterpret_cast<const uint4*>(r0 + off + c));
+        const uint4 vc = __ldg(reinterpret_cast<const uint4*>(r1 + off));
+        const uint4 vd = __ldg(reinterpret_cast<const uint4*>(r1 + off + c));
+        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&va);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&vb);
+        const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&vc);
+        const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&vd);
+        __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+        __nv_bfloat162* oab = reinterpret_cast<__nv_bfloat162*>(&oa);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 fa = __bfloat1622float2(a2[i]), fb = __bfloat1622float2(b2[i]);
-        const float2 fc = __bfloat1622float2(c2[i]), fd = __bfloat1622float2(d2[i]);
-        const float mx = ((fa.x + fb.x) + (fc.x + fd.x)) * 0.25f;
-        const float my = ((fa.y + fb.y) + (fc.y + fd.y)) * 0.25f;
-        ob[i] = __floats2bfloat162_rn(mx, my);
-        oab[i] = __floats2bfloat162_rn(gsilu(mx, hg), gsilu(my, hg));
+        for (int i = 0; i < 4; ++i) {
+          const float2 fa = __bfloat1622float2(a2[i]), fb = __bfloat1622float2(b2[i]);
+          const float2 fc = __bfloat1622float2(c2[i]), fd = __bfloat1622float2(d2[i]);
+          const float mx = ((fa.x + fb.x) + (fc.x + fd.x)) * 0.25f;
+          const float my = ((fa.y + fb.y) + (fc.y + fd.y)) * 0.25f;
+          ob[i] = __floats2bfloat162_rn(mx, my);
+          oab[i] = __floats2bfloat162_rn(gsilu(mx, hg), gsilu(my, hg));
+        }
       }
-      *reinterpret_cast<uint4*>(o0 + (int64_t)ox * c + cv * 8) = o;
-      *reinterpret_cast<uint4*>(o1 + (int64_t)ox * c + cv * 8) = oa;
+      *reinterpret_cast<uint4*>(o0 + (int64_t)oxg * c + cv * 8) = o;
+      *reinterpret_cast<uint4*>(o1 + (int64_t)oxg * c + cv * 8) = oa;
     }
   }
 }
 
 __global__ void upsample2_kernel(const __nv_bfloat16* __restrict__ in, int n, int h, int w, int c,
-                                 __nv_bfloat16* __restrict__ out) {
+                                 __nv_bfloat16* __restrict__ out, int layout) {
   // one INPUT row per CTA iteration; each 16-byte chunk is written to the
   // 2x2 output pixels it covers (two output rows, two adjacent pixels)
+  const int ig = layout & 1, og = (layout >> 1) & 1;
   const int c8 = c / 8;
-  const int ow = 2 * w;
+  const int ip = w + 2 * ig, op = 2 * w + 2 * og;
   const int row_items = w * c8;
   const int rows = n * h;
   for (int row = blockIdx.x; row < rows; row += gridDim.x) {
     const int img = row / h, y = row - (row / h) * h;
-    const __nv_bfloat16* src = in + (int64_t)row * w * c;
-    __nv_bfloat16* d0 = out + ((int64_t)img * 2 * h + 2 * y) * ow * c;
-    __nv_bfloat16* d1 = d0 + (int64_t)ow * c;
+    const __nv_bfloat16* src = in + ((int64_t)row * ip + ig) * c;
+    __nv_bfloat16* d0 = out + ((int64_t)img * 2 * h + 2 * y) * op * c;
+    __nv_bfloat16* d1 = d0 + (int64_t)op * c;
     for (int q = threadIdx.x; q < row_items; q += blockDim.x) {
       const int x = q / c8, cv = q - x * c8;
       const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + (int64_t)x * c + cv * 8));
-      const int64_t o = (int64_t)(2 * x) * c + cv * 8;
+      const int64_t o = (int64_t)(2 * x + og) * c + cv * 8;
       *reinterpret_cast<uint4*>(d0 + o) = v;
       *reinterpret_cast<uint4*>(d0 + o + c) = v;
       *reinterpret_cast<uint4*>(d1 + o) = v;
       *reinterpret_cast<uint4*>(d1 + o + c) = v;
+    }
+    if (og) {   // the two zero columns of both output rows
+      for (int q = threadIdx.x; q < 2 * c8; q += blockDim.x) {
+        const int64_t o = (int64_t)(q < c8 ? 0 : op - 1) * c + (q % c8) * 8;
+        const uint4 z = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(d0 + o) = z;
+        *reinterpret_cast<uint4*>(d1 + o) = z;
+      }
     }
   }
 }
@@ -1924,13 +2027,29 @@ static int make_act_map_box(CUtensorMap* m, const void* base, int n, int h, int 
 // rep, x, y, n) with a zero-byte stride on `rep`, so a box of bxl low-res
 // pixels lands as 2*bxl replicated pixel rows of 128 B
 static int make_up_map(CUtensorMap* m, const void* base, int n, int hl, int wl, int c, int bxl,
-                       int brows) {
+                       int brows, bool gut = false) {
+  // gutter source [n][hl][wl+2][c]: start one pixel in, rows of wl+2 pixels
+  const int pitch = gut ? wl + 2 : wl;
+  if (gut) base = static_cast<const char*>(base) + (size_t)c * 2;
   cuuint64_t dims[5] = {(cuuint64_t)c, 2, (cuuint64_t)wl, (cuuint64_t)hl, (cuuint64_t)n};
-  cuuint64_t strides[4] = {0, (cuuint64_t)c * 2, (cuuint64_t)wl * c * 2,
-                           (cuuint64_t)hl * wl * c * 2};
+  cuuint64_t strides[4] = {0, (cuuint64_t)c * 2, (cuuint64_t)pitch * c * 2,
+                           (cuuint64_t)hl * pitch * c * 2};
   cuuint32_t box[5] = {64, 2, (cuuint32_t)bxl, (cuuint32_t)brows, 1};
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? IG_OK : IG_ERR_CUDA;
+}
+
+// gutter layout: per image a 1-D sequence of P positions, box of `len` positions
+static int make_pos_map(CUtensorMap* m, const void* base, int n, int P, int c, int len) {
+  cuuint64_t dims[3] = {(cuuint64_t)c, (cuuint64_t)P, (cuuint64_t)n};
+  cuuint64_t strides[2] = {(cuuint64_t)c * 2, (cuuint64_t)P * c * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)len, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -2041,7 +2160,8 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
   using Cfg = HaloCfg<N, ROWS>;
   CUtensorMap ma, mb, mw;
   const int hl = p->h / 2, wl = p->w / 2;
-  const int rc_a = a.up_a ? make_up_map(&ma, p->act_a, p->n, hl, wl, p->ca, 66, Cfg::UP_ROWS)
+  const int rc_a = a.up_a ? make_up_map(&ma, p->act_a, p->n, hl, wl, p->ca, 66, Cfg::UP_ROWS,
+                                        a.gut_up)
                           : make_act_map_box(&ma, p->act_a, p->n, p->h, p->w, p->ca, 130, ROWS + 2);
   if (rc_a != IG_OK ||
       (p->cb > 0 && make_act_map_box(&mb, p->act_b, p->n, p->h, p->w, p->cb, 130, ROWS + 2) != IG_OK) ||
@@ -2052,7 +2172,7 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
   if (p->cb == 0) mb = ma;
   CUtensorMap msa = ma, msb = ma, mws = mw;
   if (p->csa > 0) {
-    const int rc_s = a.up_sa ? make_up_map(&msa, p->skip_a, p->n, hl, wl, p->csa, 64, 1)
+    const int rc_s = a.up_sa ? make_up_map(&msa, p->skip_a, p->n, hl, wl, p->csa, 64, 1, a.gut_up)
                              : make_act_map_box(&msa, p->skip_a, p->n, p->h, p->w, p->csa, 128, ROWS);
     if (rc_s != IG_OK ||
         (p->csb > 0 && make_act_map_box(&msb, p->skip_b, p->n, p->h, p->w, p->csb, 128, ROWS) != IG_OK) ||
@@ -2110,17 +2230,24 @@ static int make_w_map_rows(CUtensorMap* m, const void* base, int ktot, int cout,
   return r == CUDA_SUCCESS ? IG_OK : IG_ERR_CUDA;
 }
 
-template <int N>
+template <int N, int ROWS, bool GUT>
 static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaStream_t st) {
-  constexpr int ROWS = 2;
   using Cfg = HaloCfg<N, ROWS>;
   constexpr int BH_BYTES = N / 2 * 128;
+  constexpr int HBYTES = GUT ? gboxes(ROWS) * GBOX * 128 : Cfg::HALO_BYTES;
   CUtensorMap ma, mb, mw;
   const int hl = p->h / 2, wl = p->w / 2;
-  const int rc_a = a.up_a ? make_up_map(&ma, p->act_a, p->n, hl, wl, p->ca, 66, Cfg::UP_ROWS)
-                          : make_act_map_box(&ma, p->act_a, p->n, p->h, p->w, p->ca, 130, ROWS + 2);
-  if (rc_a != IG_OK ||
-      (p->cb > 0 && make_act_map_box(&mb, p->act_b, p->n, p->h, p->w, p->cb, 130, ROWS + 2) != IG_OK) ||
+  int rc_a;
+  if (GUT)
+    rc_a = make_pos_map(&ma, p->act_a, p->n, a.gP, p->ca, GBOX);
+  else
+    rc_a = a.up_a ? make_up_map(&ma, p->act_a, p->n, hl, wl, p->ca, 66, Cfg::UP_ROWS, a.gut_up)
+                  : make_act_map_box(&ma, p->act_a, p->n, p->h, p->w, p->ca, 130, ROWS + 2);
+  int rc_b = IG_OK;
+  if (p->cb > 0)
+    rc_b = GUT ? make_pos_map(&mb, p->act_b, p->n, a.gP, p->cb, GBOX)
+               : make_act_map_box(&mb, p->act_b, p->n, p->h, p->w, p->cb, 130, ROWS + 2);
+  if (rc_a != IG_OK || rc_b != IG_OK ||
       make_w_map_rows(&mw, p->wgt, p->taps * (p->ca + p->cb), p->cout, N / 2) != IG_OK) {
     set_error("ig_conv_tc(halo2): cuTensorMapEncodeTiled failed");
     return IG_ERR_CUDA;
@@ -2128,10 +2255,17 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   if (p->cb == 0) mb = ma;
   CUtensorMap msa = ma, msb = ma, mws = mw;
   if (p->csa > 0) {
-    const int rc_s = a.up_sa ? make_up_map(&msa, p->skip_a, p->n, hl, wl, p->csa, 64, 1)
-                             : make_act_map_box(&msa, p->skip_a, p->n, p->h, p->w, p->csa, 128, ROWS);
-    if (rc_s != IG_OK ||
-        (p->csb > 0 && make_act_map_box(&msb, p->skip_b, p->n, p->h, p->w, p->csb, 128, ROWS) != IG_OK) ||
+    int rc_s, rc_sb = IG_OK;
+    if (GUT) {
+      rc_s = make_pos_map(&msa, p->skip_a, p->n, a.gP, p->csa, ROWS * 128);
+      if (p->csb > 0) rc_sb = make_pos_map(&msb, p->skip_b, p->n, a.gP, p->csb, ROWS * 128);
+    } else {
+      rc_s = a.up_sa ? make_up_map(&msa, p->skip_a, p->n, hl, wl, p->csa, 64, 1, a.gut_up)
+                     : make_act_map_box(&msa, p->skip_a, p->n, p->h, p->w, p->csa, 128, ROWS);
+      if (p->csb > 0)
+        rc_sb = make_act_map_box(&msb, p->skip_b, p->n, p->h, p->w, p->csb, 128, ROWS);
+    }
+    if (rc_s != IG_OK || rc_sb != IG_OK ||
         make_w_map_rows(&mws, p->wskip, p->csa + p->csb, p->cout, N / 2) != IG_OK) {
       set_error("ig_conv_tc(halo2): cuTensorMapEncodeTiled(skip) failed");
       return IG_ERR_CUDA;
@@ -2139,8 +2273,13 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   }
   HaloArgs ha;
   ha.c = a;
-  ha.tiles_x = p->w / 128;
-  ha.tiles_y = p->h / ROWS;
+  if (GUT) {
+    ha.tiles_x = 1;
+    ha.tiles_y = (a.gP + ROWS * 128 - 1) / (ROWS * 128);
+  } else {
+    ha.tiles_x = p->w / 128;
+    ha.tiles_y = p->h / ROWS;
+  }
   ha.c.num_tiles = p->n * ha.tiles_x * ha.tiles_y;
   const int kchunks = a.kchunks_a + a.kchunks_b;
   const int wbytes = (9 * kchunks + a.kskip_a + a.kskip_b) * BH_BYTES;
@@ -2151,7 +2290,7 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   ha.hbufs = 0;
   // (r01: three buffers measured slower -- the weights then stream per tile)
   for (int hb = (g_variant == 4 ? 3 : 2); hb >= 2 && !ha.hbufs; --hb) {
-    const int fixed = 1024 + hb * Cfg::HALO_BYTES + 512 + 1024;
+    const int fixed = 1024 + hb * HBYTES + 512 + 1024;
     if (fixed + wbytes <= kBudget) {
       ha.hbufs = hb;
       ha.resident = 1;
@@ -2174,13 +2313,13 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(conv_halo2_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024);
+    cudaFuncSetAttribute(conv_halo2_kernel<N, ROWS, GUT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  int grid = ha.c.num_tiles < kNumSMs ? ha.c.num_tiles : kNumSMs;
-  grid &= ~1;
-  { conv_halo2_kernel<N><<<grid, Cfg::THREADS, smem, st>>>(ma, mb, mw, msa, msb, mws, ha); note_launch(); }
+  const int ctas = 2 * ((ha.c.num_tiles + 1) / 2);
+  const int grid = ctas < kNumSMs ? ctas : kNumSMs;
+  { conv_halo2_kernel<N, ROWS, GUT><<<grid, Cfg::THREADS, smem, st>>>(ma, mb, mw, msa, msb, mws, ha); note_launch(); }
   return cuda_check("ig_conv_tc(halo2)");
 }
 
@@ -2190,7 +2329,8 @@ static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   IG_REQUIRE(p->taps == 9 || p->taps == 1, "conv: taps must be 9 or 1");
   IG_REQUIRE(p->ca % 64 == 0 && p->cb % 64 == 0 && p->ca > 0, "conv: channels must be multiples of 64");
   IG_REQUIRE(p->cout % 16 == 0 && p->cout >= 16 && p->cout <= 256, "conv: cout must be 16..256, /16");
-  IG_REQUIRE(((int64_t)p->h * p->w) % 128 == 0, "conv: h*w must be a multiple of 128");
+  IG_REQUIRE(((int64_t)p->h * p->w) % 128 == 0 || (p->gutter & 1),
+             "conv: h*w must be a multiple of 128");
   IG_REQUIRE((p->w & (p->w - 1)) == 0, "conv: width must be a power of two");
   IG_REQUIRE(p->cb == 0 || p->act_b != nullptr, "conv: act_b missing");
   a->n = p->n; a->h = p->h; a->w = p->w; a->ca = p->ca; a->cb = p->cb; a->cout = p->cout;
@@ -2223,6 +2363,16 @@ static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   IG_REQUIRE(!(p->up_in & 2) || p->csa > 0, "conv: up_in bit 1 without skip_a");
   a->up_a = p->up_in & 1;
   a->up_sa = (p->up_in >> 1) & 1;
+  IG_REQUIRE((p->gutter & ~3) == 0, "conv: unknown gutter bits 0x%x", p->gutter);
+  IG_REQUIRE(!(p->gutter & 2) || p->up_in, "conv: gutter bit 1 without up_in");
+  a->gut = p->gutter & 1;
+  a->gut_up = (p->gutter >> 1) & 1;
+  a->gP = p->h * (p->w + 2);
+  if (a->gut) {
+    IG_REQUIRE(p->w <= 64 && !p->up2, "conv: gutter layout is for widths <= 64 (got %d)", p->w);
+    a->tiles_per_img = (a->gP + 127) / 128;
+    a->num_tiles = a->tiles_per_img * p->n;
+  }
   (void)tc;
   return IG_OK;
 }
@@ -2260,9 +2410,23 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
   }
   const bool pair = halo && (p->cout == 64 || p->cout == 128) && p->h % 2 == 0 &&
                     g_variant != 3 && ((int64_t)p->n * (p->w / 128) * (p->h / 2)) % 2 == 0;
+  if (p->gutter & 1) {
+    if (p->taps != 9 || p->up_in || g_variant == 1 || g_variant == 3) {
+      set_error("ig_conv_tc: the gutter layout needs the 3x3 CTA-pair kernel (no up_in)");
+      return IG_ERR_UNSUPPORTED;
+    }
+    switch (p->cout) {
+      case 64: return launch_conv_halo2<64, 2, true>(p, a, st);
+      case 128: return launch_conv_halo2<128, 2, true>(p, a, st);
+      case 256: return launch_conv_halo2<256, 1, true>(p, a, st);
+      default:
+        set_error("ig_conv_tc: gutter layout supports cout 64 / 128 / 256, not %d", p->cout);
+        return IG_ERR_UNSUPPORTED;
+    }
+  }
   if (pair) {   // measured faster than the row ring too (r01: enc0.0.c1 395 vs 446 us)
-    if (p->cout == 64) return launch_conv_halo2<64>(p, a, st);
-    return launch_conv_halo2<128>(p, a, st);
+    if (p->cout == 64) return launch_conv_halo2<64, 2, false>(p, a, st);
+    return launch_conv_halo2<128, 2, false>(p, a, st);
   }
   if (halo && p->cb == 0 && p->ca == 64 && p->csa == 0 && p->up_in == 0 && g_variant != 2) {
     if (p->cout <= 128 && p->h % 2 == 0) {
@@ -2313,7 +2477,7 @@ int ig_conv_simt(const ig_conv_params_t* p, void* cuda_stream) {
   ConvArgs a;
   int rc = conv_args(p, &a, false);
   if (rc) return rc;
-  const int64_t total = (int64_t)p->n * p->h * p->w * (p->cout / 16);
+  const int64_t total = (int64_t)p->n * (a.gut ? a.gP : p->h * p->w) * (p->cout / 16);
   { conv_simt_kernel<<<grid_for(total, 128, 64), 128, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       a, reinterpret_cast<const __nv_bfloat16*>(p->act_a),
       reinterpret_cast<const __nv_bfloat16*>(p->act_b),
@@ -2428,22 +2592,22 @@ int ig_unet_output(const void* f, int32_t n, int32_t h, int32_t w, int32_t fc,
 }
 
 int ig_avgpool2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,
-                     void* out_act, void* cuda_stream) {
+                     void* out_act, int32_t layout, void* cuda_stream) {
   IG_REQUIRE(h % 2 == 0 && w % 2 == 0 && c % 8 == 0, "avgpool2: bad shape");
   const int64_t total = (int64_t)n * (h / 2);
   { avgpool2_kernel<<<grid_for(total, 1, 16), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(in), n, h, w, c, 1.0f / 0.596f,
-      reinterpret_cast<__nv_bfloat16*>(out), reinterpret_cast<__nv_bfloat16*>(out_act)); note_launch(); }
+      reinterpret_cast<__nv_bfloat16*>(out), reinterpret_cast<__nv_bfloat16*>(out_act), layout); note_launch(); }
   return cuda_check("ig_avgpool2_bf16");
 }
 
 int ig_upsample2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,
-                      void* cuda_stream) {
+                      int32_t layout, void* cuda_stream) {
   IG_REQUIRE(c % 8 == 0, "upsample2: channels must be a multiple of 8");
   const int64_t total = (int64_t)n * h;
   { upsample2_kernel<<<grid_for(total, 1, 16), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(in), n, h, w, c,
-      reinterpret_cast<__nv_bfloat16*>(out)); note_launch(); }
+      reinterpret_cast<__nv_bfloat16*>(out), layout); note_launch(); }
   return cuda_check("ig_upsample2_bf16");
 }
 

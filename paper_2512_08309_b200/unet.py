@@ -41,6 +41,7 @@ RES_Q = 2.0                  # ra / rb
 FUSED_STEM = True            # input gather fused into the stem GEMM (ig_unet_stem)
 FUSED_UP = True              # 2x upsample folded into the consumer convs' TMA loads
 FUSED_OUT = True             # output conv + preconditioning in one kernel (ig_unet_out_head)
+FUSED_GUTTER = True          # narrow levels (w <= 64) in the gutter layout (1-D tap shifts)
 
 
 @dataclass(frozen=True)
@@ -279,16 +280,20 @@ class UNetDevice:
 
     # -- primitive launches -------------------------------------------------
     def conv(self, name, a, b, sigma, out0=True, out1=True, skip=None, wskip=None,
-             scale=None, up2=False, up_in=0):
+             scale=None, up2=False, up_in=0, gutter=0):
+        """gutter bit 0: activations in the gutter layout (n, h, w+2, c); bit 1:
+        the up_in low-res sources are."""
         cs = self.prog.convs[name]
         n, h, w, ca = a.shape
         if up_in & 1:                 # a is the low-res tensor, read 2x upsampled
-            h, w = 2 * h, 2 * w
+            h, w = 2 * h, 2 * (w - 2 if gutter & 2 else w)
+        elif gutter & 1:
+            w = w - 2
         cb = 0 if b is None else b.shape[3]
         assert ca + cb == cs.cin, (name, ca, cb, cs.cin)
         if scale is None and cs.modulated:
             scale = self._scale(name, sigma)      # None: identity
-        oh, ow = (2 * h, 2 * w) if up2 else (h, w)
+        oh, ow = (2 * h, 2 * w) if up2 else (h, w + 2 if gutter & 1 else w)
         o0 = torch.empty((n, oh, ow, cs.cout_pad), dtype=torch.bfloat16, device=a.device) \
             if out0 else None
         o1 = torch.empty((n, oh, ow, cs.cout_pad), dtype=torch.bfloat16, device=a.device) \
@@ -299,7 +304,8 @@ class UNetDevice:
                        self.w[name].data_ptr(), dev.ptr(scale), None, None, 0.0, 1.0,
                        MP_SILU_GAIN, dev.ptr(o0), dev.ptr(o1),
                        0 if sa is None else sa.shape[3], 0 if sb is None else sb.shape[3],
-                       dev.ptr(sa), dev.ptr(sb), dev.ptr(wskip), int(up2), int(up_in))
+                       dev.ptr(sa), dev.ptr(sb), dev.ptr(wskip), int(up2), int(up_in),
+                       int(gutter))
         conv_launch(p)
         return o0, o1
 
@@ -313,6 +319,12 @@ class UNetDevice:
         x, xa = self.conv("stem", x_in, None, sigma)
         return self.forward_after_stem(x, xa, sigma)
 
+    def _gutter(self, lv: int, w: int) -> bool:
+        """Level lv (width w) keeps its activations in the gutter layout: narrow
+        levels below the stem whose convs the CTA-pair kernel covers."""
+        return bool(FUSED_GUTTER and lv >= 1 and w <= 64
+                    and self.cfg.channels()[lv] in (64, 128, 256))
+
     def forward_after_stem(self, x: torch.Tensor, xa: torch.Tensor, sigma: float, head=None):
         """The network after the stem: (x, mp_silu(x)) -> F.
 
@@ -322,36 +334,49 @@ class UNetDevice:
         skips = [(x, xa)]
         ops = self.prog.ops
         up = 0          # (x, xa) are low-res and the next block reads them upsampled
+        lv, w = 0, x.shape[2]       # level and logical width of (x, xa)
+        gut = self._gutter(lv, w)   # (x, xa) in the gutter layout
         for k in range(1, len(ops)):
             op = ops[k]
             if op[0] == "enc":
                 nm = op[1]
-                _, h1 = self.conv(nm + ".c1", xa, None, sigma, out0=False)
+                g = int(gut)
+                _, h1 = self.conv(nm + ".c1", xa, None, sigma, out0=False, gutter=g)
                 c2 = self.prog.convs[nm + ".c2"]
                 wsk = self._skip_weights(nm, x.shape[3], c2.cout)
                 x, xa = self.conv(nm + ".c2", h1, None, sigma, skip=(x,), wskip=wsk,
-                                  scale=self._rb(c2.cout_pad))
+                                  scale=self._rb(c2.cout_pad), gutter=g)
                 skips.append((x, xa))
             elif op[0] == "down":
-                x, xa = pool_launch(x)
+                ng = self._gutter(lv + 1, w // 2)
+                x, xa = pool_launch(x, w, int(gut) | (int(ng) << 1))
+                lv, w, gut = lv + 1, w // 2, ng
                 skips.append((x, xa))
             elif op[0] == "dec":
                 nm = op[1]
                 s, sa = skips.pop()
-                _, h1 = self.conv(nm + ".c1", xa, sa, sigma, out0=False, up_in=up)
+                if up:
+                    # low-res (x, xa) of level lv+1, possibly in the gutter layout
+                    g = 2 * int(up_gut)
+                else:
+                    g = int(gut)
+                _, h1 = self.conv(nm + ".c1", xa, sa, sigma, out0=False, up_in=up, gutter=g)
                 c2 = self.prog.convs[nm + ".c2"]
                 wsk = self._skip_weights(nm, x.shape[3] + s.shape[3], c2.cout)
                 # (ConvParams.up2 can write the 2x-upsampled outputs from the
                 # epilogue directly, but its 4x scattered stores measured slower
                 # (r01: 132 vs 121 ms/step) than the separate coalesced kernel)
                 x, xa = self.conv(nm + ".c2", h1, None, sigma, skip=(x, s), wskip=wsk,
-                                  scale=self._rb(c2.cout_pad), up_in=2 if up else 0)
+                                  scale=self._rb(c2.cout_pad), up_in=2 if up else 0, gutter=g)
                 up = 0
             elif op[0] == "up":
-                if FUSED_UP and (2 * x.shape[2]) % 128 == 0:
-                    up = 1      # upsample inside the next convs' TMA loads
+                ng = self._gutter(lv - 1, 2 * w)
+                if FUSED_UP and (2 * w) % 128 == 0 and not ng:
+                    up, up_gut = 1, gut     # upsample inside the next convs' TMA loads
                 else:
-                    x, xa = upsample_launch(x), upsample_launch(xa)
+                    lay = int(gut) | (int(ng) << 1)
+                    x, xa = upsample_launch(x, w, lay), upsample_launch(xa, w, lay)
+                lv, w, gut = lv - 1, 2 * w, ng
             elif op[0] == "out":
                 n, h, w, c = xa.shape
                 C = self.cfg.data_channels
@@ -419,19 +444,25 @@ def conv_launch(p: ConvParams):
         TIMING.events.append((a, b))
 
 
-def pool_launch(x: torch.Tensor):
-    n, h, w, c = x.shape
-    o = torch.empty((n, h // 2, w // 2, c), dtype=torch.bfloat16, device=x.device)
+def pool_launch(x: torch.Tensor, w: int | None = None, layout: int = 0):
+    """2x2 mean pool -> (out, mp_silu(out)); w = logical width, layout bit 0 /
+    bit 1: input / output in the gutter layout."""
+    n, h, wx, c = x.shape
+    w = wx if w is None else w
+    ow = w // 2 + (2 if layout & 2 else 0)
+    o = torch.empty((n, h // 2, ow, c), dtype=torch.bfloat16, device=x.device)
     oa = torch.empty_like(o)
-    call("ig_avgpool2_bf16", x.data_ptr(), n, h, w, c, o.data_ptr(), oa.data_ptr(),
+    call("ig_avgpool2_bf16", x.data_ptr(), n, h, w, c, o.data_ptr(), oa.data_ptr(), layout,
          dev.stream_ptr())
     return o, oa
 
 
-def upsample_launch(x: torch.Tensor):
-    n, h, w, c = x.shape
-    o = torch.empty((n, 2 * h, 2 * w, c), dtype=torch.bfloat16, device=x.device)
-    call("ig_upsample2_bf16", x.data_ptr(), n, h, w, c, o.data_ptr(), dev.stream_ptr())
+def upsample_launch(x: torch.Tensor, w: int | None = None, layout: int = 0):
+    n, h, wx, c = x.shape
+    w = wx if w is None else w
+    ow = 2 * w + (2 if layout & 2 else 0)
+    o = torch.empty((n, 2 * h, ow, c), dtype=torch.bfloat16, device=x.device)
+    call("ig_upsample2_bf16", x.data_ptr(), n, h, w, c, o.data_ptr(), layout, dev.stream_ptr())
     return o
 
 

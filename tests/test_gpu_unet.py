@@ -418,3 +418,125 @@ def test_conv_cta_pair_matches_single_cta(n, h, w, ca, cb, csa, csb, up_in, cout
     for v in (0, 4):
         assert torch.equal(res[v][0], res[3][0]) and torch.equal(res[v][1], res[3][1]), v
     assert res[0][0].abs().sum().item() > 0
+
+
+def _to_gutter(t):
+    """(n, h, w, c) -> gutter layout (n, h, w+2, c) with zero columns."""
+    return F.pad(t, (0, 0, 1, 1)).contiguous()
+
+
+@pytest.mark.parametrize("n,h,w,ca,cb,cout,csa,csb", [
+    (3, 64, 64, 128, 0, 128, 0, 0),        # odd tile count: dummy tile of the last pair
+    (2, 64, 64, 128, 128, 128, 128, 128),  # concat input + fused skip GEMM
+    (1, 32, 32, 256, 0, 256, 256, 0),      # 1088 positions: partial last tile
+    (2, 32, 32, 256, 256, 256, 0, 0),
+    (2, 16, 16, 64, 0, 64, 64, 0),
+])
+def test_conv_gutter_layout(n, h, w, ca, cb, cout, csa, csb):
+    """Narrow levels in the gutter layout (1-D tap shifts, CTA-pair kernel):
+    interior = the standard-layout conv, gutter columns = 0; the CUDA-core
+    reference in the gutter layout is bit-identical to its standard layout."""
+    g = torch.Generator(device=DEV).manual_seed(n + h + ca + cb + cout + csa)
+
+    def rnd(*s):
+        return torch.randn(*s, device=DEV, generator=g).bfloat16()
+
+    a, b = rnd(n, h, w, ca), (rnd(n, h, w, cb) if cb else None)
+    sa, sb = (rnd(n, h, w, csa) if csa else None), (rnd(n, h, w, csb) if csb else None)
+    wgt = (torch.randn(cout, 9 * (ca + cb), device=DEV, generator=g) /
+           math.sqrt(9 * (ca + cb))).bfloat16()
+    wsk = (torch.randn(cout, csa + csb, device=DEV, generator=g) /
+           math.sqrt(max(csa + csb, 1))).bfloat16() if csa else None
+    scale = torch.rand(cout, device=DEV, generator=g) + 0.5
+
+    def run(kind, gut):
+        cv = _to_gutter if gut else (lambda t: t)
+        ins = [None if t is None else cv(t) for t in (a, b, sa, sb)]
+        o0 = torch.full((n, h, w + 2 * gut, cout), 7.0, device=DEV, dtype=torch.bfloat16)
+        o1 = torch.full_like(o0, 7.0)
+        ptr = [0 if t is None else t.data_ptr() for t in ins]
+        p = ConvParams(n, h, w, ca, cb, cout, 9, ptr[0], ptr[1], wgt.data_ptr(),
+                       scale.data_ptr(), 0, 0, 0.0, 1.0, 1.5, o0.data_ptr(), o1.data_ptr(),
+                       csa, csb, ptr[2], ptr[3], 0 if wsk is None else wsk.data_ptr(), 0, 0,
+                       int(gut))
+        st = torch.cuda.current_stream().cuda_stream
+        check(lib().ig_conv_tc(p, None, st) if kind == "tc" else lib().ig_conv_simt(p, st))
+        torch.cuda.synchronize()
+        return o0.float(), o1.float()
+
+    ref0, ref1 = run("simt", False)
+    s0, s1 = run("simt", True)
+    assert torch.equal(s0[:, :, 1:-1], ref0) and torch.equal(s1[:, :, 1:-1], ref1)
+    t0, t1 = run("tc", True)
+    for t in (t0, t1):
+        assert torch.all(t[:, :, 0] == 0) and torch.all(t[:, :, -1] == 0)
+    tol = 0.02 * ref0.abs().max().item() + 0.02
+    assert (t0[:, :, 1:-1] - ref0).abs().max().item() < tol
+    assert (t1[:, :, 1:-1] - ref1).abs().max().item() < 0.02 * ref1.abs().max().item() + 0.02
+
+
+@pytest.mark.parametrize("layout", [0, 1, 2, 3])
+def test_pool_upsample_gutter_layouts(layout):
+    from paper_2512_08309_b200.unet import pool_launch, upsample_launch
+    g = torch.Generator(device=DEV).manual_seed(layout)
+    x = torch.randn(2, 32, 64, 128, device=DEV, generator=g).bfloat16()
+    xin = _to_gutter(x) if layout & 1 else x
+    o, oa = pool_launch(xin, 64, layout)
+    ref = F.avg_pool2d(x.float().permute(0, 3, 1, 2), 2).permute(0, 2, 3, 1)
+    got = o.float()[:, :, 1:-1] if layout & 2 else o.float()
+    assert (got - ref).abs().max().item() < 2e-2
+    if layout & 2:
+        assert torch.all(o[:, :, 0] == 0) and torch.all(oa[:, :, -1] == 0)
+    u = upsample_launch(xin, 64, layout)
+    uref = x.repeat_interleave(2, 1).repeat_interleave(2, 2)
+    ug = u[:, :, 1:-1] if layout & 2 else u
+    assert torch.equal(ug, uref)
+    if layout & 2:
+        assert torch.all(u[:, :, 0] == 0) and torch.all(u[:, :, -1] == 0)
+
+
+def test_conv_upsampled_gutter_source():
+    """up_in from low-res tensors in the gutter layout (gutter bit 1)."""
+    n, h, w, ca, cb, cout, csa, csb = 2, 128, 128, 128, 64, 128, 128, 64
+    g = torch.Generator(device=DEV).manual_seed(11)
+
+    def rnd(*s):
+        return torch.randn(*s, device=DEV, generator=g).bfloat16()
+
+    a_lo, b, sa_lo, sb = rnd(n, h // 2, w // 2, ca), rnd(n, h, w, cb), \
+        rnd(n, h // 2, w // 2, csa), rnd(n, h, w, csb)
+    wgt = (torch.randn(cout, 9 * (ca + cb), device=DEV, generator=g) / 40).bfloat16()
+    wsk = (torch.randn(cout, csa + csb, device=DEV, generator=g) / 14).bfloat16()
+    res = []
+    for gut in (0, 1):
+        cv = _to_gutter if gut else (lambda t: t)
+        A, SA = cv(a_lo), cv(sa_lo)
+        o0 = torch.empty(n, h, w, cout, device=DEV, dtype=torch.bfloat16)
+        o1 = torch.empty_like(o0)
+        p = ConvParams(n, h, w, ca, cb, cout, 9, A.data_ptr(), b.data_ptr(), wgt.data_ptr(),
+                       0, 0, 0, 0.0, 1.0, 1.5, o0.data_ptr(), o1.data_ptr(), csa, csb,
+                       SA.data_ptr(), sb.data_ptr(), wsk.data_ptr(), 0, 3, 2 * gut)
+        check(lib().ig_conv_tc(p, None, torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        res.append((o0, o1))
+    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
+
+
+def test_unet_gutter_levels_match_standard_layout():
+    """Default 4-level UNet at 256^2: levels 2/3 (64 / 32 px) in the gutter layout
+    vs the standard per-tap path: same Phi to bf16-accumulation tolerance."""
+    cfg = unet.UNetConfig()
+    wins, xs = _phi_inputs(cfg, 3, 256, seed=4)
+    wxy = torch.tensor([[b.x0, b.y0] for b in wins], dtype=torch.int64, device=DEV)
+    src = torch.from_numpy(xs).to(DEV)
+    outs = {}
+    for gut in (False, True):
+        unet.FUSED_GUTTER = gut
+        try:
+            outs[gut] = unet.unet_phi_batch(cfg, src, None, wxy, 256, 1, None, seed=4, steps=2)
+        finally:
+            unet.FUSED_GUTTER = True
+    d = (outs[True] - outs[False])
+    scale = outs[False].std().item()
+    assert d.pow(2).mean().sqrt().item() < 0.01 * scale, (d.abs().max().item(), scale)
+    assert d.abs().max().item() < 0.1 * scale
