@@ -1048,7 +1048,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           } else {
             const int ks = kc - kchunks;
             if (ks < args.kskip_a && args.up_sa) {
-              if (leader) mbar_expect_tx(&hfull[hs], 2 * 128 * 128);
+              // the tile's ROWS upsampled rows (y0 even when ROWS >= 2) are
+              // max(1, ROWS/2) low-res rows
+              if (leader) mbar_expect_tx(&hfull[hs], 2 * (ROWS >= 2 ? ROWS / 2 : 1) * 128 * 128);
               tma2_load_5d(dst, &map_sa, hb, ks * 64, 0, x0 / 2, y0 >> 1, img);
             } else {
               if (leader) mbar_expect_tx(&hfull[hs], 2 * SKIP_TX);
@@ -1117,7 +1119,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
               for (int rr = 0; rr < ROWS; ++rr) {
                 const int prow =
                     GUT ? rr * 128 + (skipc ? 0 : dy * (args.w + 2) + dx)
-                    : skipc ? (upc ? 0 : rr * 128)
+                    : skipc ? (upc ? (rr >> 1) * 128 : rr * 128)
                             : (upc ? (((y0 + rr + dy - 1) >> 1) - ylo0) * 132 + dx + 1
                                    : (rr + dy) * 130 + dx);
                 const uint64_t adesc = smem_desc_sw128(hbase + prow * 128);
@@ -1169,12 +1171,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                        ROWS == 2 ? 0 : grp * NC, taddr, col == 0 || col == args.w + 1);
         }
       } else {
+        // warp group g drains accumulator rows g, g+2, ..
         const int ty = r / ha.tiles_x;
         const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
-        const int64_t p = ((int64_t)img * args.h + y0 + grp) * args.w + x0 + m;
-        const uint32_t taddr =
-            tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N + grp * N;
-        epi_span<N>(args, args.scale ? s_scale : nullptr, p, 0, taddr);
+#pragma unroll
+        for (int row = grp; row < ROWS; row += 2) {
+          const int64_t p = ((int64_t)img * args.h + y0 + row) * args.w + x0 + m;
+          const uint32_t taddr =
+              tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N + row * N;
+          epi_span<N>(args, args.scale ? s_scale : nullptr, p, 0, taddr);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -2217,7 +2223,7 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
 }
 
 static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
-                            // 4 CTA pairs with three halo buffers
+                            // 4 CTA pairs with three halo buffers, 5 no 4-row tiles
 static int make_w_map_rows(CUtensorMap* m, const void* base, int ktot, int cout, int brows) {
   cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)cout};
   cuuint64_t strides[1] = {(cuuint64_t)ktot * 2};
@@ -2260,7 +2266,8 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
       rc_s = make_pos_map(&msa, p->skip_a, p->n, a.gP, p->csa, ROWS * 128);
       if (p->csb > 0) rc_sb = make_pos_map(&msb, p->skip_b, p->n, a.gP, p->csb, ROWS * 128);
     } else {
-      rc_s = a.up_sa ? make_up_map(&msa, p->skip_a, p->n, hl, wl, p->csa, 64, 1, a.gut_up)
+      rc_s = a.up_sa ? make_up_map(&msa, p->skip_a, p->n, hl, wl, p->csa, 64,
+                                   ROWS >= 2 ? ROWS / 2 : 1, a.gut_up)
                      : make_act_map_box(&msa, p->skip_a, p->n, p->h, p->w, p->csa, 128, ROWS);
       if (p->csb > 0)
         rc_sb = make_act_map_box(&msb, p->skip_b, p->n, p->h, p->w, p->csb, 128, ROWS);
@@ -2387,7 +2394,8 @@ size_t ig_conv_workspace_bytes(void) { return 0; }
 
 // 0: automatic; 1: per-tap kernel only; 2: halo kernel instead of the row
 // ring; 3: one-CTA halo kernel instead of CTA pairs; 4: CTA pairs with three
-// halo buffers (tests / A-B timing)
+// halo buffers; 5: two-row instead of four-row CTA-pair tiles for cout 64
+// (tests / A-B timing)
 int ig_conv_set_variant(int variant) {
   g_variant = variant;
   return IG_OK;
@@ -2425,6 +2433,13 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
     }
   }
   if (pair) {   // measured faster than the row ring too (r01: enc0.0.c1 395 vs 446 us)
+    // cout 64: 4-row tiles (a 6 x 130 halo box feeds 144 MMAs) for the
+    // multi-chunk layers (r01: dec0.0.c1 976 -> 707 us); single-chunk layers
+    // measured marginally faster with 2-row tiles
+    const bool deep = a.kchunks_a + a.kchunks_b >= 2 || a.kskip_a + a.kskip_b >= 3;
+    if (p->cout == 64 && deep && p->h % 4 == 0 && g_variant != 5 &&
+        ((int64_t)p->n * (p->w / 128) * (p->h / 4)) % 2 == 0)
+      return launch_conv_halo2<64, 4, false>(p, a, st);
     if (p->cout == 64) return launch_conv_halo2<64, 2, false>(p, a, st);
     return launch_conv_halo2<128, 2, false>(p, a, st);
   }
