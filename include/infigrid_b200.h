@@ -188,8 +188,15 @@ typedef struct {
    * <= 64): every 3x3 tap is then a 1-D shift over the h*(w+2) positions of
    * an image, so narrow levels run the CTA-pair halo kernel with one 1-D
    * halo box per chunk; the outputs' gutter columns are written as zeros.
-   * bit 1: the up_in (low-res) sources are in the gutter layout. */
+   * bit 1: the up_in (low-res) sources are in the gutter layout;
+   * bit 2: the fused-pool outputs (pool0/pool1) are in the gutter layout. */
   int32_t gutter;
+  /* pool0 / pool1 (or NULL): the 2x2 mean pool of out0 and its mp_silu,
+   * [n][h/2][w/2][cout], written by the same epilogue (bit-identical to
+   * ig_avgpool2_bf16 on out0); CTA-pair kernel only (3x3, w % 128 == 0,
+   * cout 64 / 128, 2-D layout). */
+  void* pool0;
+  void* pool1;
 } ig_conv_params_t;
 size_t ig_conv_workspace_bytes(void);
 /* 0: automatic; 1: force the per-tap kernel; 2: halo kernel instead of the row ring */

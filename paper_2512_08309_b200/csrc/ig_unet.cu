@@ -191,6 +191,9 @@ struct ConvArgs {
   int gut;                // activations in the gutter layout [n][h][w+2][c] (see ig_conv_tc)
   int gut_up;             // the upsampled (up_in) sources are in the gutter layout
   int gP;                 // gutter layout: positions per image, h * (w + 2)
+  __nv_bfloat16* pool0;   // fused 2x2 mean pool of out0 -> [n][h/2][w/2][cout] (or null)
+  __nv_bfloat16* pool1;   // and its mp_silu
+  int pool_gut;           // pooled tensors in the gutter layout
   const __nv_bfloat16* skip_a;
   const __nv_bfloat16* skip_b;
   const __nv_bfloat16* wskip;
@@ -296,15 +299,33 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
 template <int NC>
 __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale, int64_t p,
                                          int c0, uint32_t taddr, bool zero = false) {
+  // every ConvArgs field this epilogue needs is read ONCE, before any store:
+  // the output pointers are generic, so the compiler must otherwise assume a
+  // store may alias `a` and reload its fields (generic loads, long scoreboard)
+  const int cout = a.cout, up2 = a.up2, aw = a.w;
+  const __nv_bfloat16* __restrict__ resp = a.res;
+  const float* __restrict__ bias = a.bias;
+  const float res_a = a.res_a, res_b = a.res_b;
+  __nv_bfloat16* __restrict__ out0 = a.out0;
+  __nv_bfloat16* __restrict__ out1 = a.out1;
+  const float hg = 0.5f * a.act_gain;
+  auto st = [&](__nv_bfloat16* __restrict__ base, int64_t o, uint4 v) {
+    *reinterpret_cast<uint4*>(base + o) = v;
+    if (up2) {
+      const int64_t rs = (int64_t)2 * aw * cout;
+      *reinterpret_cast<uint4*>(base + o + cout) = v;
+      *reinterpret_cast<uint4*>(base + o + rs) = v;
+      *reinterpret_cast<uint4*>(base + o + rs + cout) = v;
+    }
+  };
   constexpr int BC = NC < 32 ? NC : 32;
-  const int64_t off = p * a.cout + c0;
+  const int64_t off = p * cout + c0;
   const int64_t ob0 = out_base(a, p) + c0;
   uint4 res[NC / 8];
-  if (a.res) {
+  if (resp) {
 #pragma unroll
-    for (int i = 0; i < NC / 8; ++i) res[i] = ldg_nc_v4(a.res + off + 8 * i);
+    for (int i = 0; i < NC / 8; ++i) res[i] = ldg_nc_v4(resp + off + 8 * i);
   }
-  const float hg = 0.5f * a.act_gain;
 #pragma unroll
   for (int b = 0; b < NC; b += BC) {
     uint32_t r[BC];
@@ -335,19 +356,19 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
       y[i] = __uint_as_float(r[i]);
       if (s_scale) y[i] *= s_scale[c0 + b + i];
     }
-    if (a.bias) {
+    if (bias) {
 #pragma unroll
-      for (int i = 0; i < BC; ++i) y[i] += __ldg(a.bias + c0 + b + i);
+      for (int i = 0; i < BC; ++i) y[i] += __ldg(bias + c0 + b + i);
     }
-    if (a.res) {
+    if (resp) {
 #pragma unroll
       for (int i = 0; i < BC / 8; ++i) {
         const __nv_bfloat162* rb = reinterpret_cast<const __nv_bfloat162*>(&res[b / 8 + i]);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float2 f = __bfloat1622float2(rb[j]);
-          y[8 * i + 2 * j] = fmaf(a.res_a, f.x, a.res_b * y[8 * i + 2 * j]);
-          y[8 * i + 2 * j + 1] = fmaf(a.res_a, f.y, a.res_b * y[8 * i + 2 * j + 1]);
+          y[8 * i + 2 * j] = fmaf(res_a, f.x, res_b * y[8 * i + 2 * j]);
+          y[8 * i + 2 * j + 1] = fmaf(res_a, f.y, res_b * y[8 * i + 2 * j + 1]);
         }
       }
     }
@@ -355,17 +376,18 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
 #pragma unroll
       for (int i = 0; i < BC; ++i) y[i] = 0.f;
     }
-    if (a.out0) {
+
+    if (out0) {
 #pragma unroll
       for (int i = 0; i < BC / 8; ++i) {
         uint4 o;
         __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
         for (int j = 0; j < 4; ++j) ob[j] = __floats2bfloat162_rn(y[8 * i + 2 * j], y[8 * i + 2 * j + 1]);
-        store_out(a, a.out0, ob0 + b + 8 * i, o);
+        st(out0, ob0 + b + 8 * i, o);
       }
     }
-    if (a.out1) {
+    if (out1) {
 #pragma unroll
       for (int i = 0; i < BC / 8; ++i) {
         uint4 o;
@@ -373,7 +395,7 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           ob[j] = __floats2bfloat162_rn(gsilu(y[8 * i + 2 * j], hg), gsilu(y[8 * i + 2 * j + 1], hg));
-        store_out(a, a.out1, ob0 + b + 8 * i, o);
+        st(out1, ob0 + b + 8 * i, o);
       }
     }
   }
@@ -389,8 +411,7 @@ __global__ void __launch_bounds__(320, 1)
                    const __grid_constant__ CUtensorMap map_ws, const ConvArgs args) {
   using Cfg = ConvCfg<N>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + Cfg::STAGES * Cfg::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE);
@@ -556,6 +577,114 @@ __global__ void __launch_bounds__(320, 1)
 // layer fit next to the halo ring they are loaded once per CTA and stay
 // resident.  8 epilogue warps: warp group g drains accumulator row g (or half
 // of the columns when ROWS == 1).
+// Epilogue of an image-row PAIR (rows 2j, 2j+1 of a tile: the same TMEM lane,
+// accumulator columns taddr0 / taddr1) for NC columns from c0, with the 2x2
+// mean pool fused: the vertical pair is in this thread's registers, the
+// horizontal pair one lane shuffle away; the even lane writes the pooled
+// pixel.  Sum order ((a+b)+(c+d))*0.25 on the bf16-rounded outputs, exactly as
+// avgpool2_kernel, so pool0/pool1 are bit-identical to pooling out0.
+template <int NC>
+__device__ __forceinline__ void epi_pool_pair(const ConvArgs& a, const float* s_scale,
+                                              int64_t p0, int64_t p1, int64_t pp, int64_t pz,
+                                              int c0, uint32_t taddr0, uint32_t taddr1) {
+  constexpr int BC = NC < 32 ? NC : 32;
+  const float hg = 0.5f * a.act_gain;
+  const bool even = !(threadIdx.x & 1);
+  // fields read once before any store (see epi_span)
+  const int64_t cout = a.cout;
+  const float* __restrict__ bias = a.bias;
+  __nv_bfloat16* __restrict__ out0 = a.out0;
+  __nv_bfloat16* __restrict__ out1 = a.out1;
+  __nv_bfloat16* __restrict__ pool0 = a.pool0;
+  __nv_bfloat16* __restrict__ pool1 = a.pool1;
+#pragma unroll 1
+  for (int b = 0; b < NC; b += BC) {
+    uint32_t r0[BC], r1[BC];
+    if constexpr (BC == 32) {
+      tmem_ld32_nw(taddr0 + c0 + b, r0);
+      tmem_ld32_nw(taddr1 + c0 + b, r1);
+    } else {
+      static_assert(BC == 32 || BC == 16, "epi_pool_pair: 16 or 32-column blocks");
+      uint32_t t0[16], t1[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+          "%13,%14,%15}, [%16];"
+          : "=r"(t0[0]), "=r"(t0[1]), "=r"(t0[2]), "=r"(t0[3]), "=r"(t0[4]), "=r"(t0[5]),
+            "=r"(t0[6]), "=r"(t0[7]), "=r"(t0[8]), "=r"(t0[9]), "=r"(t0[10]), "=r"(t0[11]),
+            "=r"(t0[12]), "=r"(t0[13]), "=r"(t0[14]), "=r"(t0[15])
+          : "r"(taddr0 + c0 + b));
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+          "%13,%14,%15}, [%16];"
+          : "=r"(t1[0]), "=r"(t1[1]), "=r"(t1[2]), "=r"(t1[3]), "=r"(t1[4]), "=r"(t1[5]),
+            "=r"(t1[6]), "=r"(t1[7]), "=r"(t1[8]), "=r"(t1[9]), "=r"(t1[10]), "=r"(t1[11]),
+            "=r"(t1[12]), "=r"(t1[13]), "=r"(t1[14]), "=r"(t1[15])
+          : "r"(taddr1 + c0 + b));
+#pragma unroll
+      for (int i = 0; i < 16; ++i) { r0[i] = t0[i]; r1[i] = t1[i]; }
+    }
+    tmem_wait_ld();
+    float y0[BC], y1[BC];
+#pragma unroll
+    for (int i = 0; i < BC; ++i) {
+      const float sc = s_scale ? s_scale[c0 + b + i] : 1.f;
+      y0[i] = __uint_as_float(r0[i]) * sc;
+      y1[i] = __uint_as_float(r1[i]) * sc;
+    }
+    if (bias) {
+#pragma unroll
+      for (int i = 0; i < BC; ++i) {
+        const float bb = __ldg(bias + c0 + b + i);
+        y0[i] += bb;
+        y1[i] += bb;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < BC / 8; ++i) {
+      uint4 o0, o1, q0, q1, po, pa;
+      __nv_bfloat162* ob0 = reinterpret_cast<__nv_bfloat162*>(&o0);
+      __nv_bfloat162* ob1 = reinterpret_cast<__nv_bfloat162*>(&o1);
+      __nv_bfloat162* qb0 = reinterpret_cast<__nv_bfloat162*>(&q0);
+      __nv_bfloat162* qb1 = reinterpret_cast<__nv_bfloat162*>(&q1);
+      __nv_bfloat162* pob = reinterpret_cast<__nv_bfloat162*>(&po);
+      __nv_bfloat162* pab = reinterpret_cast<__nv_bfloat162*>(&pa);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = 8 * i + 2 * j;
+        ob0[j] = __floats2bfloat162_rn(y0[k], y0[k + 1]);
+        ob1[j] = __floats2bfloat162_rn(y1[k], y1[k + 1]);
+        qb0[j] = __floats2bfloat162_rn(gsilu(y0[k], hg), gsilu(y0[k + 1], hg));
+        qb1[j] = __floats2bfloat162_rn(gsilu(y1[k], hg), gsilu(y1[k + 1], hg));
+        const float2 f0 = __bfloat1622float2(ob0[j]), f1 = __bfloat1622float2(ob1[j]);
+        const float h0x = f0.x + __shfl_xor_sync(0xffffffffu, f0.x, 1);
+        const float h0y = f0.y + __shfl_xor_sync(0xffffffffu, f0.y, 1);
+        const float h1x = f1.x + __shfl_xor_sync(0xffffffffu, f1.x, 1);
+        const float h1y = f1.y + __shfl_xor_sync(0xffffffffu, f1.y, 1);
+        const float mx = (h0x + h1x) * 0.25f, my = (h0y + h1y) * 0.25f;
+        pob[j] = __floats2bfloat162_rn(mx, my);
+        pab[j] = __floats2bfloat162_rn(gsilu(mx, hg), gsilu(my, hg));
+      }
+      const int64_t co = c0 + b + 8 * i;
+      if (out0) {
+        *reinterpret_cast<uint4*>(out0 + p0 * cout + co) = o0;
+        *reinterpret_cast<uint4*>(out0 + p1 * cout + co) = o1;
+      }
+      if (out1) {
+        *reinterpret_cast<uint4*>(out1 + p0 * cout + co) = q0;
+        *reinterpret_cast<uint4*>(out1 + p1 * cout + co) = q1;
+      }
+      if (even) {
+        *reinterpret_cast<uint4*>(pool0 + pp * cout + co) = po;
+        *reinterpret_cast<uint4*>(pool1 + pp * cout + co) = pa;
+        if (pz >= 0) {
+          *reinterpret_cast<uint4*>(pool0 + pz * cout + co) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(pool1 + pz * cout + co) = make_uint4(0, 0, 0, 0);
+        }
+      }
+    }
+  }
+}
+
 template <int N, int ROWS>
 struct HaloCfg {
   static constexpr int HALO_ROWS = (ROWS + 2) * 130;
@@ -591,8 +720,7 @@ __global__ void __launch_bounds__(320, 1)
   using Cfg = HaloCfg<N, ROWS>;
   const ConvArgs args = ha.c;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int kchunks = args.kchunks_a + args.kchunks_b;
   // skip chunks ride through the halo ring as ROWS x 128-pixel boxes (no halo)
   // and use one weight tile each (fused 1x1 skip GEMM)
@@ -928,8 +1056,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   constexpr int BH_BYTES = BH * 128;
   const ConvArgs args = ha.c;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int kchunks = args.kchunks_a + args.kchunks_b;
@@ -1171,15 +1298,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                        ROWS == 2 ? 0 : grp * NC, taddr, col == 0 || col == args.w + 1);
         }
       } else {
-        // warp group g drains accumulator rows g, g+2, ..
         const int ty = r / ha.tiles_x;
         const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
+        if (args.pool0) {
+          // row pairs (2j, 2j+1); warp group g takes half of the columns of both
 #pragma unroll
-        for (int row = grp; row < ROWS; row += 2) {
-          const int64_t p = ((int64_t)img * args.h + y0 + row) * args.w + x0 + m;
-          const uint32_t taddr =
-              tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N + row * N;
-          epi_span<N>(args, args.scale ? s_scale : nullptr, p, 0, taddr);
+          for (int j = 0; j < ROWS / 2; ++j) {
+            const int64_t p0 = ((int64_t)img * args.h + y0 + 2 * j) * args.w + x0 + m;
+            const int wo = args.w / 2, py = (y0 >> 1) + j, px = (x0 + m) >> 1;
+            int64_t pp, pz = -1;
+            if (args.pool_gut) {   // pooled tensor in the gutter layout [n][h/2][w/2+2][c]
+              pp = ((int64_t)img * (args.h / 2) + py) * (wo + 2) + px + 1;
+              pz = px == 0 ? pp - 1 : (px == wo - 1 ? pp + 1 : -1);
+            } else {
+              pp = ((int64_t)img * (args.h / 2) + py) * wo + px;
+            }
+            const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N;
+            epi_pool_pair<N / 2>(args, args.scale ? s_scale : nullptr, p0, p0 + args.w, pp, pz,
+                                 grp * (N / 2), tl + (2 * j) * N, tl + (2 * j + 1) * N);
+          }
+        } else {
+          // warp group g drains accumulator rows g, g+2, ..
+#pragma unroll
+          for (int row = grp; row < ROWS; row += 2) {
+            const int64_t p = ((int64_t)img * args.h + y0 + row) * args.w + x0 + m;
+            const uint32_t taddr =
+                tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N + row * N;
+            epi_span<N>(args, args.scale ? s_scale : nullptr, p, 0, taddr);
+          }
         }
       }
       tc_fence_before();
@@ -1241,8 +1387,7 @@ __global__ void __launch_bounds__(320, 1)
   using Cfg = RowCfg<N, ROWS>;
   const ConvArgs args = ra.c;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int nb = ra.resident ? 9 : ra.b_stages;
   uint8_t* sR = smem;
   uint8_t* sB = smem + Cfg::RING * Cfg::ROW_BYTES;
@@ -1791,8 +1936,7 @@ __global__ void __launch_bounds__(256) unet_out_head_kernel(
     float* __restrict__ out) {
   // persistent, one CTA per SM, two TMA buffers: tile k+2 loads while k+1 computes
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* buf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                            ~uintptr_t(1023));
+  uint8_t* buf = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(buf + 2 * OUT_STRIDE);   // [2]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles_x = w / 128, tiles_y = h / OUT_S;
@@ -2370,7 +2514,13 @@ static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   IG_REQUIRE(!(p->up_in & 2) || p->csa > 0, "conv: up_in bit 1 without skip_a");
   a->up_a = p->up_in & 1;
   a->up_sa = (p->up_in >> 1) & 1;
-  IG_REQUIRE((p->gutter & ~3) == 0, "conv: unknown gutter bits 0x%x", p->gutter);
+  a->pool0 = reinterpret_cast<__nv_bfloat16*>(p->pool0);
+  a->pool1 = reinterpret_cast<__nv_bfloat16*>(p->pool1);
+  IG_REQUIRE(!p->pool0 || (p->pool1 && p->h % 2 == 0 && p->w % 2 == 0 && !p->up2 && !p->res),
+             "conv: fused pool needs pool0 and pool1, an even image and no residual input");
+  IG_REQUIRE((p->gutter & ~7) == 0, "conv: unknown gutter bits 0x%x", p->gutter);
+  IG_REQUIRE(!(p->gutter & 4) || p->pool0, "conv: gutter bit 2 without a fused pool");
+  a->pool_gut = (p->gutter >> 2) & 1;
   IG_REQUIRE(!(p->gutter & 2) || p->up_in, "conv: gutter bit 1 without up_in");
   a->gut = p->gutter & 1;
   a->gut_up = (p->gutter >> 1) & 1;
@@ -2418,6 +2568,11 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
   }
   const bool pair = halo && (p->cout == 64 || p->cout == 128) && p->h % 2 == 0 &&
                     g_variant != 3 && ((int64_t)p->n * (p->w / 128) * (p->h / 2)) % 2 == 0;
+  if (p->pool0 && (!pair || (p->gutter & 1))) {
+    set_error("ig_conv_tc: the fused pool needs the 2-D CTA-pair kernel (3x3, w %% 128 == 0, "
+              "cout 64/128)");
+    return IG_ERR_UNSUPPORTED;
+  }
   if (p->gutter & 1) {
     if (p->taps != 9 || p->up_in || g_variant == 1 || g_variant == 3) {
       set_error("ig_conv_tc: the gutter layout needs the 3x3 CTA-pair kernel (no up_in)");
@@ -2492,6 +2647,7 @@ int ig_conv_simt(const ig_conv_params_t* p, void* cuda_stream) {
   ConvArgs a;
   int rc = conv_args(p, &a, false);
   if (rc) return rc;
+  IG_REQUIRE(!p->pool0, "ig_conv_simt: no fused pool (pool out0 with ig_avgpool2_bf16)");
   const int64_t total = (int64_t)p->n * (a.gut ? a.gP : p->h * p->w) * (p->cout / 16);
   { conv_simt_kernel<<<grid_for(total, 128, 64), 128, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       a, reinterpret_cast<const __nv_bfloat16*>(p->act_a),
@@ -2611,7 +2767,7 @@ int ig_avgpool2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c,
   IG_REQUIRE(h % 2 == 0 && w % 2 == 0 && c % 8 == 0, "avgpool2: bad shape");
   const int64_t total = (int64_t)n * (h / 2);
   { avgpool2_kernel<<<grid_for(total, 1, 16), 256, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
-      reinterpret_cast<const __nv_bfloat16*>(in), n, h, w, c, 1.0f / 0.596f,
+      reinterpret_cast<const __nv_bfloat16*>(in), n, h, w, c, (float)(1.0 / 0.596),
       reinterpret_cast<__nv_bfloat16*>(out), reinterpret_cast<__nv_bfloat16*>(out_act), layout); note_launch(); }
   return cuda_check("ig_avgpool2_bf16");
 }

@@ -42,6 +42,11 @@ FUSED_STEM = True            # input gather fused into the stem GEMM (ig_unet_st
 FUSED_UP = True              # 2x upsample folded into the consumer convs' TMA loads
 FUSED_OUT = True             # output conv + preconditioning in one kernel (ig_unet_out_head)
 FUSED_GUTTER = True          # narrow levels (w <= 64) in the gutter layout (1-D tap shifts)
+# encoder 2x2 pool written by the producing conv's epilogue (bit-exact, tested).
+# Off: measured slower (r01: enc0.0.c2 479 -> 847 us) -- the c2 epilogue, not
+# the MMAs, is then the per-tile critical path (a second round of tanh /
+# shuffles / stores per column pair), which costs more than the pool kernel.
+FUSED_POOL = False
 
 
 @dataclass(frozen=True)
@@ -280,7 +285,7 @@ class UNetDevice:
 
     # -- primitive launches -------------------------------------------------
     def conv(self, name, a, b, sigma, out0=True, out1=True, skip=None, wskip=None,
-             scale=None, up2=False, up_in=0, gutter=0):
+             scale=None, up2=False, up_in=0, gutter=0, pool=None):
         """gutter bit 0: activations in the gutter layout (n, h, w+2, c); bit 1:
         the up_in low-res sources are."""
         cs = self.prog.convs[name]
@@ -305,7 +310,8 @@ class UNetDevice:
                        MP_SILU_GAIN, dev.ptr(o0), dev.ptr(o1),
                        0 if sa is None else sa.shape[3], 0 if sb is None else sb.shape[3],
                        dev.ptr(sa), dev.ptr(sb), dev.ptr(wskip), int(up2), int(up_in),
-                       int(gutter))
+                       int(gutter), dev.ptr(pool[0] if pool else None),
+                       dev.ptr(pool[1] if pool else None))
         conv_launch(p)
         return o0, o1
 
@@ -318,6 +324,14 @@ class UNetDevice:
         residual read), and the epilogue scales by rb."""
         x, xa = self.conv("stem", x_in, None, sigma)
         return self.forward_after_stem(x, xa, sigma)
+
+    @staticmethod
+    def _fusable_pool(h1: torch.Tensor, gut: bool, cout: int) -> bool:
+        """The c2 conv producing (x, xa) can also write their 2x2 pool: the
+        2-D CTA-pair kernel runs it (mirror of ig_conv_tc's dispatch)."""
+        n, h, w, _ = h1.shape
+        return bool(FUSED_POOL and not gut and w % 128 == 0 and h % 2 == 0
+                    and cout in (64, 128) and (n * (w // 128) * (h // 2)) % 2 == 0)
 
     def _gutter(self, lv: int, w: int) -> bool:
         """Level lv (width w) keeps its activations in the gutter layout: narrow
@@ -333,6 +347,7 @@ class UNetDevice:
         None is returned (F is never materialised)."""
         skips = [(x, xa)]
         ops = self.prog.ops
+        pool = None     # fused-pool outputs of the last encoder block
         up = 0          # (x, xa) are low-res and the next block reads them upsampled
         lv, w = 0, x.shape[2]       # level and logical width of (x, xa)
         gut = self._gutter(lv, w)   # (x, xa) in the gutter layout
@@ -344,12 +359,26 @@ class UNetDevice:
                 _, h1 = self.conv(nm + ".c1", xa, None, sigma, out0=False, gutter=g)
                 c2 = self.prog.convs[nm + ".c2"]
                 wsk = self._skip_weights(nm, x.shape[3], c2.cout)
+                pool = None
+                if k + 1 < len(ops) and ops[k + 1][0] == "down" and \
+                        self._fusable_pool(h1, gut, c2.cout_pad):
+                    # the 2x2 pool of this block's output, written by its epilogue
+                    ng = self._gutter(lv + 1, w // 2)
+                    n_, h_ = h1.shape[0], h1.shape[1]
+                    shp = (n_, h_ // 2, w // 2 + (2 if ng else 0), c2.cout_pad)
+                    pool = (torch.empty(shp, dtype=torch.bfloat16, device=h1.device),
+                            torch.empty(shp, dtype=torch.bfloat16, device=h1.device))
+                    g |= 4 * int(ng)
                 x, xa = self.conv(nm + ".c2", h1, None, sigma, skip=(x,), wskip=wsk,
-                                  scale=self._rb(c2.cout_pad), gutter=g)
+                                  scale=self._rb(c2.cout_pad), gutter=g, pool=pool)
                 skips.append((x, xa))
             elif op[0] == "down":
                 ng = self._gutter(lv + 1, w // 2)
-                x, xa = pool_launch(x, w, int(gut) | (int(ng) << 1))
+                if pool is not None:
+                    x, xa = pool
+                    pool = None
+                else:
+                    x, xa = pool_launch(x, w, int(gut) | (int(ng) << 1))
                 lv, w, gut = lv + 1, w // 2, ng
                 skips.append((x, xa))
             elif op[0] == "dec":

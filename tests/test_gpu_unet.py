@@ -540,3 +540,50 @@ def test_unet_gutter_levels_match_standard_layout():
     scale = outs[False].std().item()
     assert d.pow(2).mean().sqrt().item() < 0.01 * scale, (d.abs().max().item(), scale)
     assert d.abs().max().item() < 0.1 * scale
+
+
+@pytest.mark.parametrize("n,h,w,ca,cout,gut_out", [
+    (2, 64, 256, 64, 64, False),      # 2-row tiles
+    (1, 64, 256, 128, 64, False),     # (multi-chunk: 4-row tiles)
+    (2, 32, 128, 128, 128, True),     # pooled output in the gutter layout (next level w=64)
+])
+def test_conv_fused_pool_bit_exact(n, h, w, ca, cout, gut_out):
+    """pool0/pool1 from the conv epilogue == ig_avgpool2_bf16 on its out0 (bit for bit)."""
+    from paper_2512_08309_b200.unet import pool_launch
+    g = torch.Generator(device=DEV).manual_seed(h + w + ca + cout)
+    a = torch.randn(n, h, w, ca, device=DEV, generator=g).bfloat16()
+    sk = torch.randn(n, h, w, 64, device=DEV, generator=g).bfloat16()
+    wgt = (torch.randn(cout, 9 * ca, device=DEV, generator=g) / math.sqrt(9 * ca)).bfloat16()
+    wsk = (torch.randn(cout, 64, device=DEV, generator=g) / 8).bfloat16()
+    scale = torch.rand(cout, device=DEV, generator=g) + 0.5
+    o0 = torch.empty(n, h, w, cout, device=DEV, dtype=torch.bfloat16)
+    o1 = torch.empty_like(o0)
+    pw = w // 2 + (2 if gut_out else 0)
+    p0 = torch.full((n, h // 2, pw, cout), 3.0, device=DEV, dtype=torch.bfloat16)
+    p1 = torch.full_like(p0, 3.0)
+    p = ConvParams(n, h, w, ca, 0, cout, 9, a.data_ptr(), 0, wgt.data_ptr(), scale.data_ptr(),
+                   0, 0, 0.0, 1.0, unet.MP_SILU_GAIN, o0.data_ptr(), o1.data_ptr(), 64, 0,
+                   sk.data_ptr(), 0, wsk.data_ptr(), 0, 0, 4 if gut_out else 0,
+                   p0.data_ptr(), p1.data_ptr())
+    check(lib().ig_conv_tc(p, None, torch.cuda.current_stream().cuda_stream))
+    r0, r1 = pool_launch(o0, w, 2 if gut_out else 0)
+    torch.cuda.synchronize()
+    assert torch.equal(p0, r0) and torch.equal(p1, r1)
+    if gut_out:
+        assert torch.all(p0[:, :, 0] == 0) and torch.all(p1[:, :, -1] == 0)
+
+
+def test_unet_fused_pool_is_exact():
+    cfg = unet.UNetConfig()
+    wins, xs = _phi_inputs(cfg, 2, 256, seed=6)
+    wxy = torch.tensor([[b.x0, b.y0] for b in wins], dtype=torch.int64, device=DEV)
+    src = torch.from_numpy(xs).to(DEV)
+    outs = {}
+    default = unet.FUSED_POOL
+    for fused in (False, True):
+        unet.FUSED_POOL = fused
+        try:
+            outs[fused] = unet.unet_phi_batch(cfg, src, None, wxy, 256, 1, None, seed=6, steps=2)
+        finally:
+            unet.FUSED_POOL = default
+    assert torch.equal(outs[True], outs[False])
