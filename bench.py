@@ -250,19 +250,26 @@ def run_gpu(args):
         "dtype": "bf16",
         "data": "synthetic (seed-0 coordinate noise; random-init UNet weights, torch.manual_seed(0))",
         "config": {
-            "workload": ("cfg2: InfiniteDiffusion 2048x2048 region, 256-px windows stride 128, "
-                         "2-step consistency sampler, UNet Phi (EDM2-style, base %d, mults %s, "
-                         "%d block/level), 1 region per GPU per step" % (
-                             ucfg.base, list(ucfg.mults), ucfg.blocks))
+            "workload": (("cfg5: one %dx%d region per step, 256-px windows stride 128, 2-step "
+                          "sampler, UNet Phi (base %d, mults %s), owner-computes window rows "
+                          "sharded over %d GPU(s) with P2P halo exchange of boundary Phi "
+                          "(bitwise equal to 1 GPU)" % (big, big, ucfg.base, list(ucfg.mults),
+                                                        world)) if sharded else
+                         ("cfg2: InfiniteDiffusion 2048x2048 region, 256-px windows stride 128, "
+                          "2-step consistency sampler, UNet Phi (EDM2-style, base %d, mults %s, "
+                          "%d block/level), 1 region per GPU per step" % (
+                              ucfg.base, list(ucfg.mults), ucfg.blocks)))
                         if args.phi == "unet" else
                         "cfg2 geometry with the reference's analytic shrink_smooth Phi "
                         "(bit-exact leg), 1 region per GPU per step",
             "phi": args.phi,
-            "region_px": REGION, "window": WINDOW, "stride": STRIDE, "sampler_steps": T,
+            "region_px": big if sharded else REGION, "window": WINDOW, "stride": STRIDE,
+            "sampler_steps": T,
             "phi_calls_per_region": calls,
             "mpx_per_s": round(px_total / (ms_max / 1e3) / 1e6, 3),
             "e2e_mpx_per_s": round(px_total / (e2e_ms / 1e3) / 1e6, 3),
-            "parallelism": f"independent regions x{world} (no data-path collective)",
+            "parallelism": (f"row-strip shards x{world} + halo exchange" if sharded else
+                            f"independent regions x{world} (no data-path collective)"),
             "l2": "inputs larger than L2: every step streams GBs of fresh activations",
         },
         "roofline": {

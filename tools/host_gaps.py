@@ -1,6 +1,6 @@
 """Where does the GPU sit idle inside a bench step?  (torch.profiler timeline)
 
-python tools/host_gaps.py [--steps 1]
+python tools/host_gaps.py [--phi analytic]
 Runs the cfg2 UNet step (bench.py's workload) twice to warm up, profiles one
 more with CPU + CUDA activities, and prints the device span, summed kernel
 time, the largest idle gaps between consecutive kernels, and the top host
@@ -19,8 +19,11 @@ from paper_2512_08309_b200 import unet  # noqa: E402
 from paper_2512_08309_b200.grid import Region, WindowLayout  # noqa: E402
 
 cfg = unet.UNetConfig()
-scfg = ig.SamplerConfig(steps=2, layout=WindowLayout(256, 128), seed=0,
-                        denoiser=ig.DenoiserSpec(kind="unet", unet=cfg), name="bench")
+analytic = "--phi" in sys.argv and sys.argv[sys.argv.index("--phi") + 1] == "analytic"
+spec = (ig.DenoiserSpec(kind="shrink_smooth", radius=1, lambdas=(0.6, 0.4)) if analytic
+        else ig.DenoiserSpec(kind="unet", unet=cfg))
+scfg = ig.SamplerConfig(steps=2, layout=WindowLayout(256, 128), seed=0, denoiser=spec,
+                        name="bench")
 
 
 def step(k):
