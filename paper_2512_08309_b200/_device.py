@@ -56,16 +56,53 @@ def empty(shape, dtype) -> torch.Tensor:
                        else dtype, device=device())
 
 
+class _Staging:
+    """A small ring of grow-only pinned host buffers for host->device copies.
+    Pinning a fresh buffer per upload (tensor.pin_memory()) cost ~2.6 ms per
+    call on the analytic-Phi step; a slot is reused once the copy that last
+    read it has executed (its event)."""
+
+    SLOTS = 8
+
+    def __init__(self):
+        self.bufs = [None] * self.SLOTS
+        self.events = [None] * self.SLOTS
+        self.i = 0
+
+    def upload(self, a: np.ndarray) -> torch.Tensor:
+        nbytes = a.nbytes
+        k = self.i
+        self.i = (self.i + 1) % self.SLOTS
+        buf = self.bufs[k]
+        if buf is None or buf.numel() < nbytes:
+            buf = self.bufs[k] = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8,
+                                             pin_memory=True)
+            self.events[k] = None
+        if self.events[k] is not None:
+            self.events[k].synchronize()
+        host = buf[:nbytes]
+        host.numpy()[:] = a.reshape(-1).view(np.uint8)
+        out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=device())
+        out.view(-1).view(torch.uint8).copy_(host, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.events[k] = ev
+        return out
+
+
+_staging = None
+
+
 def upload(arr: np.ndarray) -> torch.Tensor:
     """Host array -> device tensor via pinned staging (async on the current stream)."""
+    global _staging
     a = np.ascontiguousarray(arr)
-    if not a.flags.writeable:
-        a = a.copy()
-    t = torch.from_numpy(a)
-    traffic["h2d"] += t.numel() * t.element_size()
-    if t.numel() * t.element_size() >= 1 << 16:
-        t = t.pin_memory()
-    return t.to(device(), non_blocking=True)
+    traffic["h2d"] += a.nbytes
+    if a.nbytes == 0:
+        return torch.from_numpy(a.copy()).to(device())
+    if _staging is None:
+        _staging = _Staging()
+    return _staging.upload(a)
 
 
 def upload_i64(values) -> torch.Tensor:

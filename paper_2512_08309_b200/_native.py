@@ -90,6 +90,10 @@ def lib():
             fn.argtypes = args
             fn.restype = _RESTYPES.get(name, c_int32)
         _lib = L
+        # A/B timing of conv kernel variants (ig_conv_set_variant), e.g. from bench.py
+        v = os.environ.get("IG_CONV_VARIANT")
+        if v:
+            L.ig_conv_set_variant(int(v))
     return _lib
 
 
