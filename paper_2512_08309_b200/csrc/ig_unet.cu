@@ -707,6 +707,8 @@ struct HaloArgs {
   int b_stages;      // streamed weight ring depth (when !resident)
   int tiles_x, tiles_y;
   int hbufs;         // halo buffers in the ring (CTA-pair kernel: 2 or 3)
+  int sbufs;         // CTA-pair kernel: separate ring for the 1x1 skip chunks (0: they
+                     // ride in the halo ring)
 };
 
 template <int N, int ROWS>
@@ -1064,16 +1066,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   const int nchunks = kchunks + kskip;
   constexpr uint32_t SKIP_TX = ROWS * 128 * 128;
   const int nb = ha.resident ? 9 * kchunks + kskip : ha.b_stages;
+  constexpr int SBYTES = ROWS * 128 * 128;   // one skip chunk: the tile's pixels, no halo
   uint8_t* sH = smem;
-  uint8_t* sB = smem + ha.hbufs * HBYTES;
+  uint8_t* sS = smem + ha.hbufs * HBYTES;      // skip ring (ha.sbufs slots)
+  uint8_t* sB = sS + ha.sbufs * SBYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + nb * BH_BYTES);
-  const int HB = ha.hbufs;
+  const int HB = ha.hbufs, SB = ha.sbufs;
   uint64_t* hfull = bars;          // [HB] (leader's used)
   uint64_t* hempty = bars + 4;     // [HB] (each CTA's own)
   uint64_t* tfull = bars + 8;      // [2]  (each CTA's own)
   uint64_t* tempty = bars + 10;    // [2]  (leader's used)
   uint64_t* wfull = bars + 12;     // [1]  (leader's used)
-  uint64_t* bfull = bars + 13;     // [b_stages] (leader's used)
+  uint64_t* sfull = bars + 13;     // [SB] (leader's used)
+  uint64_t* sempty = bars + 15;    // [SB] (each CTA's own)
+  uint64_t* bfull = bars + 17;     // [b_stages] (leader's used)
   uint64_t* bempty = bfull + ha.b_stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + ha.b_stages);
   float* s_scale = reinterpret_cast<float*>(tmem_slot + 4);
@@ -1098,6 +1104,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       mbar_init(&tempty[s], 16);            // 8 epilogue warps x 2 CTAs
     }
     mbar_init(wfull, 1);
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], 1);
+    }
     for (int s = 0; s < ha.b_stages; ++s) {
       mbar_init(&bfull[s], 1);
       mbar_init(&bempty[s], 1);
@@ -1130,8 +1140,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         for (int ks = 0; ks < kskip; ++ks)
           tma2_load_2d(sB + (9 * kchunks + ks) * BH_BYTES, &map_ws, l_wfull, ks * 64, brow);
       }
-      int hs = 0, bs = 0;
-      uint32_t hph = 0, bph = 0;
+      int hs = 0, bs = 0, ss = 0;
+      uint32_t hph = 0, bph = 0, sph = 0;
       for (int pr = pair0; pr < npairs; pr += pstride) {
         const int tile = 2 * pr + (int)rank;
         const int img = tile / tiles_per_img;
@@ -1139,14 +1149,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         const int ty = r / ha.tiles_x;
         const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
         for (int kc = 0; kc < nchunks; ++kc) {
-          mbar_wait(&hempty[hs], hph ^ 1);
-          uint8_t* dst = sH + hs * HBYTES;
-          const uint32_t hb = mapa_u32(&hfull[hs], 0);
+          const bool sring = SB && kc >= kchunks;    // skip chunk in its own ring
+          uint64_t* fb = sring ? &sfull[ss] : &hfull[hs];
+          mbar_wait(sring ? &sempty[ss] : &hempty[hs], (sring ? sph : hph) ^ 1);
+          uint8_t* dst = sring ? sS + ss * SBYTES : sH + hs * HBYTES;
+          const uint32_t hb = mapa_u32(fb, 0);
           if constexpr (GUT) {
             // (a dummy tile has img == n: out of range, zero filled, bytes still counted)
             const int q0 = r * ROWS * 128;
             if (kc < kchunks) {
-              if (leader) mbar_expect_tx(&hfull[hs], 2 * HBYTES);
+              if (leader) mbar_expect_tx(fb, 2 * HBYTES);
               const CUtensorMap* m = kc < args.kchunks_a ? &map_a : &map_b;
               const int c = (kc < args.kchunks_a ? kc : kc - args.kchunks_a) * 64;
               const int start = q0 - (args.w + 3);
@@ -1155,7 +1167,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                 tma2_load_3d(dst + bx * GBOX * 128, m, hb, c, start + bx * GBOX, img);
             } else {
               const int ks = kc - kchunks;
-              if (leader) mbar_expect_tx(&hfull[hs], 2 * ROWS * 128 * 128);
+              if (leader) mbar_expect_tx(fb, 2 * ROWS * 128 * 128);
               if (ks < args.kskip_a)
                 tma2_load_3d(dst, &map_sa, hb, ks * 64, q0, img);
               else
@@ -1163,10 +1175,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             }
           } else if (kc < kchunks) {
             if (kc < args.kchunks_a && args.up_a) {
-              if (leader) mbar_expect_tx(&hfull[hs], 2 * Cfg::UP_TX);
+              if (leader) mbar_expect_tx(fb, 2 * Cfg::UP_TX);
               tma2_load_5d(dst, &map_a, hb, kc * 64, 0, x0 / 2 - 1, (y0 - 1) >> 1, img);
             } else {
-              if (leader) mbar_expect_tx(&hfull[hs], 2 * Cfg::HALO_TX);
+              if (leader) mbar_expect_tx(fb, 2 * Cfg::HALO_TX);
               if (kc < args.kchunks_a)
                 tma2_load_4d(dst, &map_a, hb, kc * 64, x0 - 1, y0 - 1, img);
               else
@@ -1177,17 +1189,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             if (ks < args.kskip_a && args.up_sa) {
               // the tile's ROWS upsampled rows (y0 even when ROWS >= 2) are
               // max(1, ROWS/2) low-res rows
-              if (leader) mbar_expect_tx(&hfull[hs], 2 * (ROWS >= 2 ? ROWS / 2 : 1) * 128 * 128);
+              if (leader) mbar_expect_tx(fb, 2 * (ROWS >= 2 ? ROWS / 2 : 1) * 128 * 128);
               tma2_load_5d(dst, &map_sa, hb, ks * 64, 0, x0 / 2, y0 >> 1, img);
             } else {
-              if (leader) mbar_expect_tx(&hfull[hs], 2 * SKIP_TX);
+              if (leader) mbar_expect_tx(fb, 2 * SKIP_TX);
               if (ks < args.kskip_a)
                 tma2_load_4d(dst, &map_sa, hb, ks * 64, x0, y0, img);
               else
                 tma2_load_4d(dst, &map_sb, hb, (ks - args.kskip_a) * 64, x0, y0, img);
             }
           }
-          if (++hs == HB) { hs = 0; hph ^= 1; }
+          if (sring) {
+            if (++ss == SB) { ss = 0; sph ^= 1; }
+          } else if (++hs == HB) {
+            hs = 0;
+            hph ^= 1;
+          }
           if (!ha.resident) {
             const int ntaps = kc < kchunks ? 9 : 1;
             for (int tap = 0; tap < ntaps; ++tap) {
@@ -1210,8 +1227,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       // ---------------- MMA issuer (leader CTA only) ----------------
       constexpr uint32_t idesc = idesc_bf16(256, N);
       if (ha.resident) mbar_wait(wfull, 0);
-      int hs = 0, bs = 0;
-      uint32_t hph = 0, bph = 0;
+      int hs = 0, bs = 0, ss = 0;
+      uint32_t hph = 0, bph = 0, sph = 0;
       int it = 0;
       for (int pr = pair0; pr < npairs; pr += pstride, ++it) {
         const int acc = it & 1;
@@ -1222,10 +1239,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         const int y0 = ((tile % tiles_per_img) / ha.tiles_x) * ROWS;
         const int ylo0 = (y0 - 1) >> 1;
         for (int kc = 0; kc < nchunks; ++kc) {
-          mbar_wait(&hfull[hs], hph);
-          tc_fence_after();
-          const uint32_t hbase = smem_u32(sH + hs * HBYTES);
           const bool skipc = kc >= kchunks;
+          const bool sring = SB && skipc;
+          mbar_wait(sring ? &sfull[ss] : &hfull[hs], sring ? sph : hph);
+          tc_fence_after();
+          const uint32_t hbase = smem_u32(sring ? sS + ss * SBYTES : sH + hs * HBYTES);
           const bool upc = skipc ? (kc - kchunks < args.kskip_a && args.up_sa)
                                  : (kc < args.kchunks_a && args.up_a);
           const int ntaps = skipc ? 1 : 9;
@@ -1262,9 +1280,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
               if (++bs == ha.b_stages) { bs = 0; bph ^= 1; }
             }
           }
-          if (elect_one()) tc_commit2_mc(&hempty[hs]);
+          if (elect_one()) tc_commit2_mc(sring ? &sempty[ss] : &hempty[hs]);
           __syncwarp();
-          if (++hs == HB) { hs = 0; hph ^= 1; }
+          if (sring) {
+            if (++ss == SB) { ss = 0; sph ^= 1; }
+          } else if (++hs == HB) {
+            hs = 0;
+            hph ^= 1;
+          }
         }
         if (elect_one()) tc_commit2_mc(&tfull[acc]);
         __syncwarp();
@@ -2367,7 +2390,8 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
 }
 
 static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
-                            // 4 CTA pairs with three halo buffers, 5 no 4-row tiles
+                            // 4 CTA pairs with three halo buffers, 5 no 4-row tiles,
+                            // 6 separate ring for the skip chunks
 static int make_w_map_rows(CUtensorMap* m, const void* base, int ktot, int cout, int brows) {
   cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)cout};
   cuuint64_t strides[1] = {(cuuint64_t)ktot * 2};
@@ -2437,11 +2461,21 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   // two halo buffers with resident weights where they fit (variant 4: try
   // three buffers, the next tile's box streaming in during the whole tile)
   constexpr int kBudget = 226 * 1024;
+  constexpr int SBYTES = ROWS * 128 * 128;
   int smem = 0;
   ha.hbufs = 0;
+  // variant 6: skip chunks in their own ring (when it fits next to resident
+  // weights), so an 8-MMA skip chunk never holds a halo slot.  Off by default:
+  // measured neutral-to-slower (r01: enc0.0.c2 479 -> 492 us, dec0.1.c2 571 -> 606)
+  const int kskip = a.kskip_a + a.kskip_b;
+  ha.sbufs = 0;
+  if (kskip && g_variant == 6) {
+    for (int sb = (kskip >= 2 ? 2 : 1); sb >= 1 && !ha.sbufs; --sb)
+      if (1024 + 2 * HBYTES + sb * SBYTES + 512 + 1024 + wbytes <= kBudget) ha.sbufs = sb;
+  }
   // (r01: three buffers measured slower -- the weights then stream per tile)
   for (int hb = (g_variant == 4 ? 3 : 2); hb >= 2 && !ha.hbufs; --hb) {
-    const int fixed = 1024 + hb * HBYTES + 512 + 1024;
+    const int fixed = 1024 + hb * HBYTES + ha.sbufs * SBYTES + 512 + 1024;
     if (fixed + wbytes <= kBudget) {
       ha.hbufs = hb;
       ha.resident = 1;
@@ -2544,8 +2578,8 @@ size_t ig_conv_workspace_bytes(void) { return 0; }
 
 // 0: automatic; 1: per-tap kernel only; 2: halo kernel instead of the row
 // ring; 3: one-CTA halo kernel instead of CTA pairs; 4: CTA pairs with three
-// halo buffers; 5: two-row instead of four-row CTA-pair tiles for cout 64
-// (tests / A-B timing)
+// halo buffers; 5: two-row instead of four-row CTA-pair tiles for cout 64;
+// 6: separate skip-chunk ring (tests / A-B timing)
 int ig_conv_set_variant(int variant) {
   g_variant = variant;
   return IG_OK;

@@ -400,7 +400,7 @@ def test_conv_cta_pair_matches_single_cta(n, h, w, ca, cb, csa, csb, up_in, cout
            math.sqrt(max(csa + csb, 1))).bfloat16() if csa else None
     scale = torch.rand(cout, device=DEV, generator=g) + 0.5
     res = {}
-    for variant in (3, 0, 4, 5):
+    for variant in (3, 0, 4, 5, 6):
         o0 = torch.empty(n, h, w, cout, device=DEV, dtype=torch.bfloat16)
         o1 = torch.empty_like(o0)
         p = ConvParams(n, h, w, ca, cb, cout, 9, a.data_ptr(), 0 if b is None else b.data_ptr(),
@@ -415,7 +415,7 @@ def test_conv_cta_pair_matches_single_cta(n, h, w, ca, cb, csa, csb, up_in, cout
         finally:
             check(lib().ig_conv_set_variant(0))
         res[variant] = (o0, o1)
-    for v in (0, 4, 5):
+    for v in (0, 4, 5, 6):
         assert torch.equal(res[v][0], res[3][0]) and torch.equal(res[v][1], res[3][1]), v
     assert res[0][0].abs().sum().item() > 0
 
