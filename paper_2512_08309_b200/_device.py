@@ -82,7 +82,8 @@ class _Staging:
             self.events[k].synchronize()
         host = buf[:nbytes]
         host.numpy()[:] = a.reshape(-1).view(np.uint8)
-        out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=device())
+        out = torch.empty(a.shape, dtype=torch.from_numpy(np.empty(0, a.dtype)).dtype,
+                          device=device())
         out.view(-1).view(torch.uint8).copy_(host, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
