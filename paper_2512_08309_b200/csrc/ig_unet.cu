@@ -284,6 +284,13 @@ __device__ __forceinline__ void epi_chunk(const ConvArgs& a, int64_t p, int c0, 
   }
 }
 
+// 32-byte global store (sm_100: STG.E.256): a lane fills a whole sector
+__device__ __forceinline__ void stg_v8(void* p, uint4 a, uint4 b) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y),
+               "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+
 __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -309,13 +316,14 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
   __nv_bfloat16* __restrict__ out0 = a.out0;
   __nv_bfloat16* __restrict__ out1 = a.out1;
   const float hg = 0.5f * a.act_gain;
-  auto st = [&](__nv_bfloat16* __restrict__ base, int64_t o, uint4 v) {
-    *reinterpret_cast<uint4*>(base + o) = v;
+  // 16 channels (32 B, one sector) per store
+  auto st = [&](__nv_bfloat16* __restrict__ base, int64_t o, uint4 v0, uint4 v1) {
+    stg_v8(base + o, v0, v1);
     if (up2) {
       const int64_t rs = (int64_t)2 * aw * cout;
-      *reinterpret_cast<uint4*>(base + o + cout) = v;
-      *reinterpret_cast<uint4*>(base + o + rs) = v;
-      *reinterpret_cast<uint4*>(base + o + rs + cout) = v;
+      stg_v8(base + o + cout, v0, v1);
+      stg_v8(base + o + rs, v0, v1);
+      stg_v8(base + o + rs + cout, v0, v1);
     }
   };
   constexpr int BC = NC < 32 ? NC : 32;
@@ -377,25 +385,26 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
       for (int i = 0; i < BC; ++i) y[i] = 0.f;
     }
 
+    static_assert(BC % 16 == 0, "epi_span: 16-channel store groups");
     if (out0) {
 #pragma unroll
-      for (int i = 0; i < BC / 8; ++i) {
-        uint4 o;
-        __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+      for (int i = 0; i < BC / 16; ++i) {
+        uint4 o[2];
+        __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(o);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ob[j] = __floats2bfloat162_rn(y[8 * i + 2 * j], y[8 * i + 2 * j + 1]);
-        st(out0, ob0 + b + 8 * i, o);
+        for (int j = 0; j < 8; ++j) ob[j] = __floats2bfloat162_rn(y[16 * i + 2 * j], y[16 * i + 2 * j + 1]);
+        st(out0, ob0 + b + 16 * i, o[0], o[1]);
       }
     }
     if (out1) {
 #pragma unroll
-      for (int i = 0; i < BC / 8; ++i) {
-        uint4 o;
-        __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+      for (int i = 0; i < BC / 16; ++i) {
+        uint4 o[2];
+        __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(o);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          ob[j] = __floats2bfloat162_rn(gsilu(y[8 * i + 2 * j], hg), gsilu(y[8 * i + 2 * j + 1], hg));
-        st(out1, ob0 + b + 8 * i, o);
+        for (int j = 0; j < 8; ++j)
+          ob[j] = __floats2bfloat162_rn(gsilu(y[16 * i + 2 * j], hg), gsilu(y[16 * i + 2 * j + 1], hg));
+        st(out1, ob0 + b + 16 * i, o[0], o[1]);
       }
     }
   }
