@@ -1944,9 +1944,12 @@ __global__ void __launch_bounds__(128) unet_stem_kernel(
 // (conflict-free on the swizzled rows), all 9 taps x 4 K-steps of B held in
 // registers, and the preconditioning applied to the f32 accumulators, so F
 // is never rounded to bf16 nor written to HBM.
-constexpr int OUT_S = 4;                                   // output rows per CTA
-constexpr int OUT_BYTES = (OUT_S + 2) * 130 * 128;               // TMA box bytes
-constexpr int OUT_STRIDE = (OUT_BYTES + 1023) / 1024 * 1024;      // SW128: 1 KB aligned buffers
+// S output rows per tile, NB TMA buffers in flight per CTA
+template <int S>
+struct OutCfg {
+  static constexpr int BYTES = (S + 2) * 130 * 128;                 // TMA box bytes
+  static constexpr int STRIDE = (BYTES + 1023) / 1024 * 1024;       // SW128: 1 KB aligned
+};
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t* r) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -1962,14 +1965,16 @@ __device__ __forceinline__ void mma_bf16_16816(float* d, const uint32_t* a, uint
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+template <int OUT_S, int NB>
 __global__ void __launch_bounds__(256) unet_out_head_kernel(
     const __grid_constant__ CUtensorMap map_xa, const __nv_bfloat16* __restrict__ wout,
     int n, int h, int w, int C, const float* __restrict__ x_noisy, float c_skip, float c_out,
     float* __restrict__ out) {
-  // persistent, one CTA per SM, two TMA buffers: tile k+2 loads while k+1 computes
+  // persistent, one CTA per SM, NB TMA buffers: tile k+NB loads while k+1.. compute
+  constexpr int OUT_BYTES = OutCfg<OUT_S>::BYTES, OUT_STRIDE = OutCfg<OUT_S>::STRIDE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* buf = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(buf + 2 * OUT_STRIDE);   // [2]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(buf + NB * OUT_STRIDE);   // [NB]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles_x = w / 128, tiles_y = h / OUT_S;
   const int ntiles = n * tiles_x * tiles_y;
@@ -1981,10 +1986,9 @@ __global__ void __launch_bounds__(256) unet_out_head_kernel(
   };
   if (threadIdx.x == 0) {
     prefetch_map(&map_xa);
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int s = 0; s < NB; ++s) mbar_init(&bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NB; ++s) {
       const int t0 = blockIdx.x + s * gridDim.x;
       if (t0 < ntiles) {
         int img, y0, x0;
@@ -2013,11 +2017,11 @@ __global__ void __launch_bounds__(256) unet_out_head_kernel(
   //           16-23 rows 0-7 / k 8-15, 24-31 rows 8-15 / k 8-15
   const int lr = (lane & 7) + ((lane >> 3) & 1) * 8, lk = lane >> 4;
   const int g = lane / 4, t = lane % 4;
-  // warp w: OUT_S (=4) rows x 8 m-tiles of 16 px; m-tile (row = i, px0 = 16 w)
+  // warp w: OUT_S rows x 8 m-tiles of 16 px; m-tile (row = i, px0 = 16 w)
   const int px0 = warp * 16;
   int it = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int sb = it & 1;
+    const int sb = it % NB;
     const uint32_t sbase = smem_u32(buf + sb * OUT_STRIDE);
     int img, y0, x0;
     tile_xy(tile, img, y0, x0);
@@ -2032,7 +2036,7 @@ __global__ void __launch_bounds__(256) unet_out_head_kernel(
             (((int64_t)img * C + c) * h + y0 + i) * w + x0 + px0 + g + (j >> 1) * 8;
         xn[i][j] = c < C ? __ldg(x_noisy + idx) : 0.f;
       }
-    mbar_wait(&bar[sb], (uint32_t)((it >> 1) & 1));
+    mbar_wait(&bar[sb], (uint32_t)((it / NB) & 1));
     float acc[OUT_S][4];
 #pragma unroll
     for (int i = 0; i < OUT_S; ++i)
@@ -2055,9 +2059,9 @@ __global__ void __launch_bounds__(256) unet_out_head_kernel(
     }
     // buffer consumed: refill with the next tile while the epilogue runs
     __syncthreads();
-    if (threadIdx.x == 0 && tile + 2 * (int)gridDim.x < ntiles) {
+    if (threadIdx.x == 0 && tile + NB * (int)gridDim.x < ntiles) {
       int ni, ny, nx;
-      tile_xy(tile + 2 * gridDim.x, ni, ny, nx);
+      tile_xy(tile + NB * gridDim.x, ni, ny, nx);
       mbar_expect_tx(&bar[sb], OUT_BYTES);
       tma_load_4d(buf + sb * OUT_STRIDE, &map_xa, &bar[sb], 0, nx - 1, ny - 1, ni);
     }
@@ -2400,7 +2404,7 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
 
 static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
                             // 4 CTA pairs with three halo buffers, 5 no 4-row tiles,
-                            // 6 separate ring for the skip chunks
+                            // 6 separate ring for the skip chunks, 7 2-row/3-buffer out head
 static int make_w_map_rows(CUtensorMap* m, const void* base, int ktot, int cout, int brows) {
   cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)cout};
   cuuint64_t strides[1] = {(cuuint64_t)ktot * 2};
@@ -2768,29 +2772,33 @@ int ig_unet_out_head(const void* xa, int32_t n, int32_t h, int32_t w, int32_t ci
                      float c_skip, float c_out, float* out, void* cuda_stream) {
   IG_REQUIRE(n >= 0 && cin == 64 && cout_pad >= 8 && channels >= 1 && channels <= 8,
              "out_head: needs 64 input channels and 1..8 output channels");
-  IG_REQUIRE(w % 128 == 0 && h % OUT_S == 0, "out_head: %dx%d not tiled by %dx128", h, w, OUT_S);
+  IG_REQUIRE(w % 128 == 0 && h % 4 == 0, "out_head: %dx%d not tiled by 4x128", h, w);
   if (n == 0) return IG_OK;
   if (!encode_fn()) {
     set_error("ig_unet_out_head: cuTensorMapEncodeTiled unavailable");
     return IG_ERR_CUDA;
   }
-  CUtensorMap m;
-  if (make_act_map_box(&m, xa, n, h, w, cin, 130, OUT_S + 2) != IG_OK) {
-    set_error("ig_unet_out_head: cuTensorMapEncodeTiled failed");
-    return IG_ERR_CUDA;
-  }
-  const int smem = 2 * OUT_STRIDE + 1024 + 64;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(unet_out_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  const int64_t tiles = (int64_t)n * (w / 128) * (h / OUT_S);
-  const int ctas = (int)(tiles < kNumSMs ? tiles : kNumSMs);
-  { unet_out_head_kernel<<<ctas, 256, smem, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
-      m, reinterpret_cast<const __nv_bfloat16*>(w_out), n, h, w, channels, x_noisy, c_skip, c_out,
-      out); note_launch(); }
-  return cuda_check("ig_unet_out_head");
+  auto launch = [&](auto kern, int S, int NB, int stride) -> int {
+    CUtensorMap m;
+    if (make_act_map_box(&m, xa, n, h, w, cin, 130, S + 2) != IG_OK) {
+      set_error("ig_unet_out_head: cuTensorMapEncodeTiled failed");
+      return IG_ERR_CUDA;
+    }
+    const int smem = NB * stride + 1024 + 64;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int64_t tiles = (int64_t)n * (w / 128) * (h / S);
+    const int ctas = (int)(tiles < kNumSMs ? tiles : kNumSMs);
+    { kern<<<ctas, 256, smem, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+        m, reinterpret_cast<const __nv_bfloat16*>(w_out), n, h, w, channels, x_noisy, c_skip,
+        c_out, out); note_launch(); }
+    return cuda_check("ig_unet_out_head");
+  };
+  // default: 4-row tiles, two buffers.  Variant 7: 2-row tiles, three buffers in flight
+  // (measured slower, r01: 184 vs 165 us per 64 windows -- the kernel is bound by the
+  // ldmatrix re-reads of A for the 9 taps, not by its TMA loads)
+  if (g_variant == 7)
+    return launch(unet_out_head_kernel<2, 3>, 2, 3, OutCfg<2>::STRIDE);
+  return launch(unet_out_head_kernel<4, 2>, 4, 2, OutCfg<4>::STRIDE);
 }
 
 int ig_unet_output(const void* f, int32_t n, int32_t h, int32_t w, int32_t fc,
