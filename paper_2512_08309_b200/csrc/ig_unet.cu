@@ -2080,6 +2080,131 @@ __global__ void __launch_bounds__(256) unet_out_head_kernel(
   }
 }
 
+// Output head, tap-in-N form (C = 1 data channel; SMEM holds 2 boxes + the partials): the A fragment of an
+// INPUT pixel block is loaded once per 16-channel step and multiplied by all
+// 9 taps at once (N = 9*C taps padded to 16 or 24): D[px][tap] = the
+// contribution of input pixel px to the output pixel it reaches through that
+// tap.  The partials go to SMEM (f32, [input row][px][tap]) and each output
+// sums its 9 taps -- SMEM traffic per pixel ~0.3 KB instead of the 9x
+// ldmatrix re-reads (1.15 KB) of unet_out_head_kernel.
+template <int C>
+__global__ void __launch_bounds__(256) unet_out_head_tn_kernel(
+    const __grid_constant__ CUtensorMap map_xa, const __nv_bfloat16* __restrict__ wout,
+    int n, int h, int w, const float* __restrict__ x_noisy, float c_skip, float c_out,
+    float* __restrict__ out) {
+  constexpr int S = 4;                                  // output rows per tile
+  constexpr int IR = S + 2;                             // input rows per tile
+  constexpr int NT = (9 * C + 7) / 8;                   // n8 tiles of taps
+  constexpr int TP = 9 * C;                             // partials per input pixel
+  constexpr int PX = 130;                               // input pixels per row (9 blocks of 16)
+  constexpr int BYTES = OutCfg<S>::BYTES, STRIDE = OutCfg<S>::STRIDE;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* buf = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* part = reinterpret_cast<float*>(buf + 2 * STRIDE);        // [IR][PX][TP]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(part + IR * PX * TP);  // [2]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tiles_x = w / 128, tiles_y = h / S;
+  const int ntiles = n * tiles_x * tiles_y;
+  auto tile_xy = [&](int t, int& img, int& y0, int& x0) {
+    img = t / (tiles_x * tiles_y);
+    const int r = t - img * tiles_x * tiles_y;
+    y0 = (r / tiles_x) * S;
+    x0 = (r % tiles_x) * 128;
+  };
+  if (threadIdx.x == 0) {
+    prefetch_map(&map_xa);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < 2; ++s) {
+      const int t0 = blockIdx.x + s * gridDim.x;
+      if (t0 < ntiles) {
+        int img, y0, x0;
+        tile_xy(t0, img, y0, x0);
+        mbar_expect_tx(&bar[s], BYTES);
+        tma_load_4d(buf + s * STRIDE, &map_xa, &bar[s], 0, x0 - 1, y0 - 1, img);
+      }
+    }
+  }
+  // B fragments: column n = c*9 + tap (tap = dy*3+dx), k = input channel;
+  // lane holds W[c][tap][16 kc + 2(lane%4) + {0,1}] (and +8) for n = lane/4 + 8 nt
+  uint32_t bf[NT][4][2];
+  {
+    const int kq = 2 * (lane % 4);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int ncol = nt * 8 + lane / 4;
+      const bool valid = ncol < TP;
+      const int c = valid ? ncol / 9 : 0, tap = valid ? ncol % 9 : 0;
+      const uint32_t* wr = reinterpret_cast<const uint32_t*>(wout + ((int64_t)c * 9 + tap) * 64);
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) {
+        bf[nt][kc][0] = valid ? __ldg(wr + (kc * 16 + kq) / 2) : 0u;
+        bf[nt][kc][1] = valid ? __ldg(wr + (kc * 16 + kq + 8) / 2) : 0u;
+      }
+    }
+  }
+  __syncthreads();
+  const int lr = (lane & 7) + ((lane >> 3) & 1) * 8, lk = lane >> 4;
+  const int g = lane / 4, t = lane % 4;
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int sb = it & 1;
+    const uint32_t sbase = smem_u32(buf + sb * STRIDE);
+    int img, y0, x0;
+    tile_xy(tile, img, y0, x0);
+    mbar_wait(&bar[sb], (uint32_t)((it >> 1) & 1));
+    // 1. partials: IR rows x 9 blocks of 16 input pixels, spread over the 8 warps
+    for (int blk = warp; blk < IR * 9; blk += 8) {
+      const int r = blk / 9, px0 = (blk - r * 9) * 16;
+      float acc[NT][4];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[nt][j] = 0.f;
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) {
+        // rows past the 130-pixel box read the next row's pixels: their
+        // partials only reach outputs outside the tile and are never summed
+        const int srow = min(r * 130 + px0 + lr, IR * 130 - 1);
+        const int chunk = kc * 2 + lk;
+        uint32_t a[4];
+        ldsm_x4(sbase + srow * 128 + ((chunk ^ (srow & 7)) * 16), a);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[nt], a, bf[nt][kc][0], bf[nt][kc][1]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int col = nt * 8 + 2 * t + (j & 1);
+          const int px = px0 + g + (j >> 1) * 8;
+          if (col < TP && px < PX) part[(r * PX + px) * TP + col] = acc[nt][j];
+        }
+    }
+    __syncthreads();
+    // buffer consumed: refill with the next tile
+    if (threadIdx.x == 0 && tile + 2 * (int)gridDim.x < ntiles) {
+      int ni, ny, nx;
+      tile_xy(tile + 2 * gridDim.x, ni, ny, nx);
+      mbar_expect_tx(&bar[sb], BYTES);
+      tma_load_4d(buf + sb * STRIDE, &map_xa, &bar[sb], 0, nx - 1, ny - 1, ni);
+    }
+    // 2. each output sums its 9 taps: output (i, x) <- input (i+dy, x+dx) (halo coords)
+    for (int q = threadIdx.x; q < S * 128 * C; q += 256) {
+      const int c = q / (S * 128), rem = q - c * S * 128;
+      const int i = rem / 128, x = rem - i * 128;
+      float sum = 0.f;
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap)
+        sum += part[((i + tap / 3) * PX + x + tap % 3) * TP + c * 9 + tap];
+      const int64_t idx = (((int64_t)img * C + c) * h + y0 + i) * w + x0 + x;
+      out[idx] = __fadd_rn(__fmul_rn(c_skip, __ldg(x_noisy + idx)), __fmul_rn(c_out, sum));
+    }
+    __syncthreads();   // partials consumed before the next tile overwrites them
+  }
+}
+
 __global__ void unet_output_kernel(const __nv_bfloat16* __restrict__ f, int n, int h, int w,
                                    int fc, const float* __restrict__ x_noisy, int C,
                                    float c_skip, float c_out, float* __restrict__ out) {
@@ -2404,7 +2529,8 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
 
 static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
                             // 4 CTA pairs with three halo buffers, 5 no 4-row tiles,
-                            // 6 separate ring for the skip chunks, 7 2-row/3-buffer out head
+                            // 6 separate ring for the skip chunks, 7 2-row/3-buffer out head,
+                            // 8 per-tap out head for C = 1
 static int make_w_map_rows(CUtensorMap* m, const void* base, int ktot, int cout, int brows) {
   cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)cout};
   cuuint64_t strides[1] = {(cuuint64_t)ktot * 2};
@@ -2793,6 +2919,23 @@ int ig_unet_out_head(const void* xa, int32_t n, int32_t h, int32_t w, int32_t ci
         c_out, out); note_launch(); }
     return cuda_check("ig_unet_out_head");
   };
+  // tap-in-N head for C = 1 (variant 8: the per-tap ldmatrix head)
+  if (channels == 1 && g_variant != 8) {
+    CUtensorMap m;
+    if (make_act_map_box(&m, xa, n, h, w, cin, 130, 4 + 2) != IG_OK) {
+      set_error("ig_unet_out_head: cuTensorMapEncodeTiled failed");
+      return IG_ERR_CUDA;
+    }
+    const int smem = 2 * OutCfg<4>::STRIDE + 6 * 130 * 9 * 4 + 1024 + 64;
+    const int64_t tiles = (int64_t)n * (w / 128) * (h / 4);
+    const int ctas = (int)(tiles < kNumSMs ? tiles : kNumSMs);
+    auto kern = unet_out_head_tn_kernel<1>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    { kern<<<ctas, 256, smem, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+        m, reinterpret_cast<const __nv_bfloat16*>(w_out), n, h, w, x_noisy, c_skip, c_out,
+        out); note_launch(); }
+    return cuda_check("ig_unet_out_head");
+  }
   // default: 4-row tiles, two buffers.  Variant 7: 2-row tiles, three buffers in flight
   // (measured slower, r01: 184 vs 165 us per 64 windows -- the kernel is bound by the
   // ldmatrix re-reads of A for the 9 taps, not by its TMA loads)

@@ -587,3 +587,32 @@ def test_unet_fused_pool_is_exact():
         finally:
             unet.FUSED_POOL = default
     assert torch.equal(outs[True], outs[False])
+
+
+def test_out_head_tap_in_n_matches_per_tap():
+    """C = 1 output head (tap-in-N, partials summed in SMEM) vs the per-tap
+    ldmatrix head (variant 8): same Phi to f32 summation-order rounding."""
+    n, h, w = 3, 64, 256
+    g = torch.Generator(device=DEV).manual_seed(12)
+    xa = torch.randn(n, h, w, 64, device=DEV, generator=g).bfloat16()
+    wo = torch.zeros(16, 9 * 64, device=DEV)
+    wo[0] = torch.randn(9 * 64, device=DEV, generator=g) / 24
+    wo = wo.bfloat16()
+    xn = torch.randn(n, 1, h, w, device=DEV, generator=g)
+    outs = {}
+    for v in (0, 8):
+        o = torch.empty(n, 1, h, w, device=DEV)
+        check(lib().ig_conv_set_variant(v))
+        try:
+            call("ig_unet_out_head", xa.data_ptr(), n, h, w, 64, wo.data_ptr(), 16, 1,
+                 xn.data_ptr(), 0.3, 0.9, o.data_ptr(), torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+        finally:
+            check(lib().ig_conv_set_variant(0))
+        outs[v] = o
+    ref = 0.3 * xn + 0.9 * F.conv2d(xa.float().permute(0, 3, 1, 2),
+                                    wo[:1].float().reshape(1, 3, 3, 64).permute(0, 3, 1, 2),
+                                    padding=1)
+    for v, o in outs.items():
+        assert (o - ref).abs().max().item() < 1e-3 * ref.abs().max().item() + 1e-4, v
+    assert (outs[0] - outs[8]).abs().max().item() < 1e-4 * ref.abs().max().item() + 1e-5
