@@ -131,10 +131,19 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # IG_BENCH_SMOKE_1GPU=1: control-flow smoke test of the N-rank path on one GPU
+    # (independent regions, no kernel waits on another rank; gloo, shared device).
+    # Never a measurement.
+    smoke1 = os.environ.get("IG_BENCH_SMOKE_1GPU") == "1"
+    if smoke1:
+        local = 0
     torch.cuda.set_device(local)
     dev.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if smoke1:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ucfg = _workload(args)
     if args.phi == "analytic":
         # the reference's own analytic Phi: the bit-exact parity leg
@@ -193,7 +202,8 @@ def run_gpu(args):
     conv_ms, conv_n = unet.TIMING.collect()
     unet.TIMING.disable()
     ms = e0.elapsed_time(e1)
-    ms_t = torch.tensor([ms], device="cuda")
+    red_dev = "cpu" if smoke1 else "cuda"          # gloo smoke: reduce on the host
+    ms_t = torch.tensor([ms], device=red_dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
@@ -211,7 +221,7 @@ def run_gpu(args):
     barrier()
     wall_e2e = (time.perf_counter() - t0) * 1e3
     e2e_ms = max(f0.elapsed_time(f1), wall_e2e)
-    e2e_t = torch.tensor([e2e_ms], device="cuda")
+    e2e_t = torch.tensor([e2e_ms], device=red_dev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_t.item())

@@ -164,21 +164,25 @@ def p2p_exchange(dist, device, window_shape, dtype):
     tensor per (src, dst) pair, all sends/recvs of a step in one batch."""
     import torch
 
+    # gloo moves host memory only: stage device windows through the host there
+    # (NCCL sends the device buffers directly)
+    wire = torch.device("cpu") if dist.get_backend() == "gloo" else device
+
     def exchange(t, outgoing, expect):
         ops, bufs = [], {}
         for dst, items in sorted(outgoing.items()):
             if items:
-                buf = torch.stack(list(items)).contiguous().to(device)
+                buf = torch.stack(list(items)).contiguous().to(wire)
                 ops.append(dist.P2POp(dist.isend, buf, dst))
         for src, n in sorted(expect.items()):
             if n:
-                buf = torch.empty((n,) + tuple(window_shape), dtype=dtype, device=device)
+                buf = torch.empty((n,) + tuple(window_shape), dtype=dtype, device=wire)
                 bufs[src] = buf
                 ops.append(dist.P2POp(dist.irecv, buf, src))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
-        return {src: list(buf.unbind(0)) for src, buf in bufs.items()}
+        return {src: list(buf.to(device).unbind(0)) for src, buf in bufs.items()}
 
     return exchange
 
