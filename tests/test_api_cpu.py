@@ -142,3 +142,31 @@ def test_unet_program_and_flops():
     w = unet.make_weights(cfg)
     w2 = unet.make_weights(cfg)
     assert all(np.array_equal(w[k].numpy(), w2[k].numpy()) for k in w)
+
+
+def test_parent_slab_is_parent_of_window_bbox():
+    """store._fetch_parents reads ONE slab: parent_region(bbox of the windows).
+    It must equal the per-window bounding union of parent regions (the
+    reference's fold, store.py:248-257) for scale / inv_scale / margin deps."""
+    import random as _random
+
+    from paper_2512_08309_b200.grid import Region, WindowLayout, window_region
+    from paper_2512_08309_b200.store import Dependency
+
+    rng = _random.Random(3)
+    for lay in (WindowLayout(256, 128), WindowLayout(64, 32, (5, -7)), WindowLayout(16, 16)):
+        for dep in (Dependency("p", 0, 1, 1), Dependency("p", 3, 16, 1), Dependency("p", 1, 1, 4),
+                    Dependency("p", 2, 7, 1), Dependency("p", 0, 1, 3)):
+            for _ in range(20):
+                idxs = [(rng.randrange(-50, 50), rng.randrange(-50, 50))
+                        for _ in range(rng.randrange(1, 12))]
+                ref = None
+                for idx in idxs:
+                    pr = dep.parent_region(window_region(lay, idx))
+                    ref = pr if ref is None else ref.bounding_union(pr)
+                i_lo, i_hi = min(i for i, _ in idxs), max(i for i, _ in idxs)
+                j_lo, j_hi = min(j for _, j in idxs), max(j for _, j in idxs)
+                box = Region(i_lo * lay.stride + lay.offset[0], j_lo * lay.stride + lay.offset[1],
+                             (i_hi - i_lo) * lay.stride + lay.window,
+                             (j_hi - j_lo) * lay.stride + lay.window)
+                assert dep.parent_region(box) == ref
