@@ -39,3 +39,4 @@ torch.cuda.synchronize()
 pr.disable()
 st = pstats.Stats(pr)
 st.sort_stats("tottime").print_stats(25)
+st.print_callers("built-in method torch.empty")
