@@ -21,6 +21,8 @@ coordinates, so overlapping windows stay seed-consistent.
 
 from __future__ import annotations
 
+import os
+
 import math
 from dataclasses import dataclass, field
 
@@ -550,5 +552,9 @@ def unet_phi_batch(cfg: UNetConfig, src: torch.Tensor, src_region: Region | None
 
 
 def max_windows_per_forward(win: int) -> int:
-    """Windows per UNet forward: ~3 GB per 64-channel activation tensor."""
+    """Windows per UNet forward: ~3 GB per 64-channel activation tensor
+    (IG_UNET_CHUNK overrides, for A/B timing of the chunk size)."""
+    env = os.environ.get("IG_UNET_CHUNK")
+    if env:
+        return max(1, int(env))
     return max(16, int(3.2e9 // (win * win * 64 * 2)))
