@@ -227,6 +227,15 @@ int ig_unet_output(const void* f, int32_t n, int32_t h, int32_t w, int32_t fc,
 int ig_unet_out_head(const void* xa, int32_t n, int32_t h, int32_t w, int32_t cin,
                      const void* w_out, int32_t cout_pad, int32_t channels, const float* x_noisy,
                      float c_skip, float c_out, float* out, void* cuda_stream);
+/* EDM2 self-attention over n windows of hw tokens (NHWC bf16, c channels,
+ * heads of 64): ig_attn_prep unit-RMS-normalises q, k in place per token and
+ * head and writes the normalised v transposed ([n][c/64][64][hw]);
+ * ig_attention computes y = softmax(q k^T / 8) v per head (tcgen05, f32
+ * accumulation and softmax).  hw % 8 == 0 (partial 128-token tiles masked). */
+int ig_attn_prep(void* q, void* k, const void* v, int32_t n, int32_t hw, int32_t c, void* vt,
+                 void* cuda_stream);
+int ig_attention(const void* q, const void* k, const void* vt, int32_t n, int32_t hw, int32_t c,
+                 void* y, void* cuda_stream);
 int ig_avgpool2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,
                      void* out_act, int32_t layout, void* cuda_stream);
 int ig_upsample2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,

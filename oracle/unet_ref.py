@@ -17,7 +17,7 @@ import numpy as np
 import torch
 import torch.nn.functional as F
 
-from paper_2512_08309_b200.unet import (MP_SILU_GAIN, RES_T, build_program, make_weights,
+from paper_2512_08309_b200.unet import (ATTN_T, MP_SILU_GAIN, RES_T, build_program, make_weights,
                                         modulation, precond, round_bf16)
 
 from . import port
@@ -56,6 +56,22 @@ class UNetRef:
             y = y * modulation(self.cfg, self.host, name, sigma)[None, :, None, None]
         return y
 
+    def attention(self, nm, x, sigma):
+        """EDM2 self-attention block (fp32): heads of 64 channels, q/k/v unit-RMS
+        normalised per token, softmax(q k^T / 8) v, 1x1 projection, mp_sum."""
+        n, c, h, w = x.shape
+        qkv = self.conv(nm + ".qkv", x, sigma).reshape(n, 3, c // 64, 64, h * w)
+
+        def nrm(t):
+            return t / (1e-4 + t.norm(dim=2, keepdim=True) / 8.0)
+
+        q, k, v = nrm(qkv[:, 0]), nrm(qkv[:, 1]), nrm(qkv[:, 2])     # (n, heads, 64, hw)
+        p = torch.einsum("nhdq,nhdk->nhqk", q, k / 8.0).softmax(dim=-1)
+        y = torch.einsum("nhqk,nhdk->nhdq", p, v).reshape(n, c, h, w)
+        y = self.conv(nm + ".proj", y, sigma)
+        nrm_t = math.sqrt((1 - ATTN_T) ** 2 + ATTN_T ** 2)
+        return ((1 - ATTN_T) * x + ATTN_T * y) / nrm_t
+
     @torch.no_grad()
     def forward(self, x_in, sigma):
         """x_in (n, cin_pad, H, W) fp32 -> F (n, cout_pad, H, W)."""
@@ -63,6 +79,7 @@ class UNetRef:
         ra, rb = (1 - RES_T) / nrm, RES_T / nrm
         x = self.conv("stem", x_in, sigma)
         skips = [x]
+        prev = None
         for op in self.prog.ops[1:]:
             if op[0] == "enc":
                 nm, has_skip = op[1], op[2]
@@ -70,6 +87,10 @@ class UNetRef:
                 res = self.conv(nm + ".skip", x, sigma) if has_skip else x
                 x = ra * res + rb * self.conv(nm + ".c2", h, sigma)
                 skips.append(x)
+            elif op[0] == "attn":
+                x = self.attention(op[1], x, sigma)
+                if prev == "enc":
+                    skips[-1] = x
             elif op[0] == "down":
                 x = F.avg_pool2d(x, 2)
                 skips.append(x)
@@ -84,6 +105,7 @@ class UNetRef:
                 x = F.interpolate(x, scale_factor=2, mode="nearest")
             elif op[0] == "out":
                 return self.conv("out", mp_silu(x), sigma)
+            prev = op[0]
         raise AssertionError
 
 

@@ -66,6 +66,8 @@ SIGNATURES = {
     "ig_unet_stem": [V, I32, I64, I64, I32, I32, I32, V, I32, V, I64, I64, I32, I32, I32, I32,
                      I32, U64, U64, U32, F32, F32, I32, I32, I32, V, F32, V, V, V, V],
     "ig_unet_out_head": [V, I32, I32, I32, I32, V, I32, I32, V, F32, F32, V, V],
+    "ig_attn_prep": [V, V, V, I32, I32, I32, V, V],
+    "ig_attention": [V, V, V, I32, I32, I32, V, V],
     "ig_avgpool2_bf16": [V, I32, I32, I32, I32, V, V, I32, V],
     "ig_upsample2_bf16": [V, I32, I32, I32, I32, V, I32, V],
 }

@@ -66,6 +66,14 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1, int c2, int c3, int c4) {
   asm volatile(
@@ -2205,6 +2213,309 @@ __global__ void __launch_bounds__(256) unet_out_head_tn_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// EDM2 self-attention (the UNet's lowest level): per head of 64 channels,
+// q, k, v are unit-RMS normalised per token, y = softmax(q k^T / 8) v.
+//
+// attn_prep_kernel: one CTA per (window, head, 128-token block): q, k
+// normalised in place; v normalised and written TRANSPOSED ([n][head][64][HW])
+// so a V tile is a K-major B operand (rows = head dims, K = keys).
+constexpr float ATTN_EPS = 1e-4f;
+
+__global__ void __launch_bounds__(128) attn_prep_kernel(__nv_bfloat16* __restrict__ q,
+                                                        __nv_bfloat16* __restrict__ k,
+                                                        const __nv_bfloat16* __restrict__ v,
+                                                        int n, int hw, int c,
+                                                        __nv_bfloat16* __restrict__ vt) {
+  __shared__ __nv_bfloat16 tile[64][128 + 8];   // [dim][token] (padded)
+  const int heads = c / 64, blocks = (hw + 127) / 128;
+  const int b = blockIdx.x % blocks, hd = (blockIdx.x / blocks) % heads;
+  const int img = blockIdx.x / (blocks * heads);
+  const int tok = b * 128 + threadIdx.x;
+  const bool live = tok < hw;
+  const int64_t base = ((int64_t)img * hw + (live ? tok : 0)) * c + hd * 64;
+  auto norm_row = [&](const __nv_bfloat16* src, float* f) {
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(src) + i);
+      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 t = __bfloat1622float2(p[j]);
+        f[8 * i + 2 * j] = t.x;
+        f[8 * i + 2 * j + 1] = t.y;
+        ss += t.x * t.x + t.y * t.y;
+      }
+    }
+    // EDM2 normalize: x / (eps + ||x|| / sqrt(64))
+    const float inv = 1.f / (ATTN_EPS + sqrtf(ss) * 0.125f);
+#pragma unroll
+    for (int i = 0; i < 64; ++i) f[i] *= inv;
+  };
+  float f[64];
+  for (int which = 0; which < 2 && live; ++which) {
+    __nv_bfloat16* p = (which ? k : q) + base;
+    norm_row(p, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint4 u;
+      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] = __floats2bfloat162_rn(f[8 * i + 2 * j], f[8 * i + 2 * j + 1]);
+      reinterpret_cast<uint4*>(p)[i] = u;
+    }
+  }
+  norm_row(v + base, f);
+#pragma unroll
+  for (int d = 0; d < 64; ++d) tile[d][threadIdx.x] = __float2bfloat16_rn(f[d]);
+  __syncthreads();
+  // coalesced transposed store: 64 rows of (up to) 128 tokens
+  __nv_bfloat16* dst = vt + (((int64_t)img * heads + hd) * 64) * hw + b * 128;
+  const int ntok = hw - b * 128 < 128 ? hw - b * 128 : 128;   // multiple of 8
+  for (int q2 = threadIdx.x; q2 < 64 * 16; q2 += 128) {
+    const int d = q2 / 16, ch = q2 % 16;
+    if (ch * 8 < ntok) {
+      const uint4 u = *reinterpret_cast<const uint4*>(&tile[d][ch * 8]);
+      *reinterpret_cast<uint4*>(dst + (int64_t)d * hw + ch * 8) = u;
+    }
+  }
+}
+
+// attention_kernel: one CTA per (window, head, 128-query tile); tcgen05 with
+// TMEM accumulators, two-pass softmax (pass 1: row max / sum over all keys;
+// pass 2: P = exp(s - m) / l in bf16 -> SMEM -> O += P V), so O never needs
+// rescaling in TMEM.  Warp 0: TMA, warp 1: MMA issue, warps 2-5: softmax /
+// epilogue (thread = query row = TMEM lane).
+//   S = Q K^T: M=128 queries, N=128 keys, K=64 dims (4 x K16); S double-buffered
+//   O += P V:  M=128, N=64 dims, K=128 keys (8 x K16; P and V^T as 2 x 64-key chunks)
+struct AttnSmem {
+  static constexpr int Q = 0;                        // 16 KB  [128 q][64 d]
+  static constexpr int K0 = 16384;                   // 2 x 16 KB [128 keys][64 d]
+  static constexpr int V0 = K0 + 2 * 16384;          // 2 x 16 KB [2 chunks][64 d][64 keys]
+  static constexpr int P0 = V0 + 2 * 16384;          // 2 x 32 KB [2 chunks][128 q][64 keys]
+  static constexpr int BARS = P0 + 2 * 32768;        // barriers
+  static constexpr int BYTES = BARS + 256;
+};
+
+__global__ void __launch_bounds__(192, 1) attention_kernel(
+    const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+    const __grid_constant__ CUtensorMap map_vt, int n, int hw, int heads,
+    __nv_bfloat16* __restrict__ y, int c) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + AttnSmem::BARS);
+  uint64_t* qfull = bars;            // [1]
+  uint64_t* kfull = bars + 1;        // [2]
+  uint64_t* kempty = bars + 3;       // [2]
+  uint64_t* vfull = bars + 5;        // [2]
+  uint64_t* vempty = bars + 7;       // [2]
+  uint64_t* sfull = bars + 9;        // [2]
+  uint64_t* sempty = bars + 11;      // [2]
+  uint64_t* pfull = bars + 13;       // [2]
+  uint64_t* pempty = bars + 15;      // [2]
+  uint64_t* ofull = bars + 17;       // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qtiles = (hw + 127) / 128, ktiles = (hw + 127) / 128;
+  const int qt = blockIdx.x % qtiles, hd = (blockIdx.x / qtiles) % heads;
+  const int img = blockIdx.x / (qtiles * heads);
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_q);
+    prefetch_map(&map_k);
+    prefetch_map(&map_vt);
+    mbar_init(qfull, 1);
+    mbar_init(ofull, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kfull[s], 1);
+      mbar_init(&kempty[s], 1);
+      mbar_init(&vfull[s], 1);
+      mbar_init(&vempty[s], 1);
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], 128);
+      mbar_init(&pfull[s], 128);
+      mbar_init(&pempty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;        // S buffers at cols 0 / 128, O at 256
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      mbar_expect_tx(qfull, 16384);
+      tma_load_3d(sm + AttnSmem::Q, &map_q, qfull, hd * 64, qt * 128, img);
+      // K tiles: pass 1 (0..kt-1) then pass 2 (again); V^T tiles in pass 2
+      for (int i = 0; i < 2 * ktiles; ++i) {
+        const int s = i & 1, ph = (i >> 1) & 1, kt = i % ktiles;
+        mbar_wait(&kempty[s], ph ^ 1);
+        mbar_expect_tx(&kfull[s], 16384);
+        tma_load_3d(sm + AttnSmem::K0 + s * 16384, &map_k, &kfull[s], hd * 64, kt * 128, img);
+        if (i >= ktiles) {
+          const int j = i - ktiles, vs = j & 1, vph = (j >> 1) & 1;
+          mbar_wait(&vempty[vs], vph ^ 1);
+          mbar_expect_tx(&vfull[vs], 16384);
+          const int row = (img * heads + hd) * 64;
+          uint8_t* vd = sm + AttnSmem::V0 + vs * 16384;
+          tma_load_2d(vd, &map_vt, &vfull[vs], kt * 128, row);
+          tma_load_2d(vd + 8192, &map_vt, &vfull[vs], kt * 128 + 64, row);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc_s = idesc_bf16(128, 128);
+    constexpr uint32_t idesc_o = idesc_bf16(128, 64);
+    mbar_wait(qfull, 0);
+    tc_fence_after();
+    const uint64_t qdesc = smem_desc_sw128(smem_u32(sm + AttnSmem::Q));
+    auto issue_s = [&](int i) {
+      const int s = i & 1, ph = (i >> 1) & 1;
+      mbar_wait(&kfull[s], ph);
+      mbar_wait(&sempty[s], ph ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t kdesc = smem_desc_sw128(smem_u32(sm + AttnSmem::K0 + s * 16384));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc_mma(tmem + s * 128, qdesc + 2 * kk, kdesc + 2 * kk, idesc_s, kk ? 1u : 0u);
+        tc_commit(&kempty[s]);
+        tc_commit(&sfull[s]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int j) {
+      const int ps = j & 1, ph = (j >> 1) & 1;
+      mbar_wait(&vfull[ps], ph);
+      mbar_wait(&pfull[ps], ph);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          const uint64_t pdesc =
+              smem_desc_sw128(smem_u32(sm + AttnSmem::P0 + ps * 32768 + ch * 16384));
+          const uint64_t vdesc =
+              smem_desc_sw128(smem_u32(sm + AttnSmem::V0 + ps * 16384 + ch * 8192));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma(tmem + 256, pdesc + 2 * kk, vdesc + 2 * kk, idesc_o, (j | ch | kk) ? 1u : 0u);
+        }
+        tc_commit(&pempty[ps]);
+        tc_commit(&vempty[ps]);
+        if (j == ktiles - 1) tc_commit(ofull);
+      }
+      __syncwarp();
+    };
+    for (int i = 0; i < ktiles; ++i) issue_s(i);             // pass 1
+    issue_s(ktiles);                                          // pass 2: S_0
+    for (int j = 0; j < ktiles; ++j) {
+      if (j + 1 < ktiles) issue_s(ktiles + j + 1);            // S_{j+1} overlaps softmax_j
+      issue_pv(j);
+    }
+  } else {
+    // ---------------- softmax / epilogue (warps 2..5) ----------------
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;                      // query row == TMEM lane
+    const uint32_t lanebase = (uint32_t)(quarter * 32) << 16;
+    const float sc = 0.125f * 1.4426950408889634f;           // 1/sqrt(64) * log2(e)
+    float m = -INFINITY, l = 0.f;
+    // keys past hw (zero-filled K rows of the last tile) are masked out
+    auto load_s = [&](int s, int kt, float* v) {
+      const int kvalid = hw - kt * 128;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        uint32_t r[32];
+        tmem_ld32_nw(tmem + lanebase + s * 128 + b * 32, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          v[b * 32 + i] = (b * 32 + i < kvalid) ? __uint_as_float(r[i]) * sc : -INFINITY;
+      }
+    };
+    // pass 1: row max / sum (log2 domain)
+    for (int i = 0; i < ktiles; ++i) {
+      const int s = i & 1, ph = (i >> 1) & 1;
+      mbar_wait(&sfull[s], ph);
+      tc_fence_after();
+      float v[128];
+      load_s(s, i, v);
+      tc_fence_before();
+      mbar_arrive(&sempty[s]);
+      float mx = m;
+#pragma unroll
+      for (int t = 0; t < 128; ++t) mx = fmaxf(mx, v[t]);
+      float sum = 0.f;
+#pragma unroll
+      for (int t = 0; t < 128; ++t) sum += exp2f(v[t] - mx);
+      l = l * exp2f(m - mx) + sum;
+      m = mx;
+    }
+    const float inv_l = 1.f / l;
+    // pass 2: P = exp2(s - m) / l (bf16) into the K-major SW128 P tile
+    for (int j = 0; j < ktiles; ++j) {
+      const int i = ktiles + j, s = i & 1, ph = (i >> 1) & 1;
+      const int ps = j & 1, pph = (j >> 1) & 1;
+      mbar_wait(&sfull[s], ph);
+      tc_fence_after();
+      float v[128];
+      load_s(s, j, v);
+      tc_fence_before();
+      mbar_arrive(&sempty[s]);
+      mbar_wait(&pempty[ps], pph ^ 1);
+      uint8_t* pbase = sm + AttnSmem::P0 + ps * 32768;
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch)
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) {
+          uint4 u;
+          __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int key = ch * 64 + c8 * 8 + 2 * t;
+            o[t] = __floats2bfloat162_rn(exp2f(v[key] - m) * inv_l, exp2f(v[key + 1] - m) * inv_l);
+          }
+          *reinterpret_cast<uint4*>(pbase + ch * 16384 + row * 128 + ((c8 ^ (row & 7)) * 16)) = u;
+        }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&pfull[ps]);
+    }
+    // epilogue: O (64 cols) -> bf16 -> y[img][token][hd*64 ..]
+    mbar_wait(ofull, 0);
+    tc_fence_after();
+    uint32_t r[64];
+    tmem_ld32_nw(tmem + lanebase + 256, r);
+    tmem_ld32_nw(tmem + lanebase + 288, r + 32);
+    tmem_wait_ld();
+    __nv_bfloat16* dst = y + ((int64_t)img * hw + qt * 128 + row) * c + hd * 64;
+#pragma unroll
+    for (int b = 0; b < 4 && qt * 128 + row < hw; ++b) {
+      uint4 u[2];
+      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(u);
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        o[t] = __floats2bfloat162_rn(__uint_as_float(r[16 * b + 2 * t]),
+                                     __uint_as_float(r[16 * b + 2 * t + 1]));
+      stg_v8(dst + 16 * b, u[0], u[1]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 __global__ void unet_output_kernel(const __nv_bfloat16* __restrict__ f, int n, int h, int w,
                                    int fc, const float* __restrict__ x_noisy, int C,
                                    float c_skip, float c_out, float* __restrict__ out) {
@@ -2942,6 +3253,58 @@ int ig_unet_out_head(const void* xa, int32_t n, int32_t h, int32_t w, int32_t ci
   if (g_variant == 7)
     return launch(unet_out_head_kernel<2, 3>, 2, 3, OutCfg<2>::STRIDE);
   return launch(unet_out_head_kernel<4, 2>, 4, 2, OutCfg<4>::STRIDE);
+}
+
+int ig_attn_prep(void* q, void* k, const void* v, int32_t n, int32_t hw, int32_t c, void* vt,
+                 void* cuda_stream) {
+  IG_REQUIRE(n >= 0 && c % 64 == 0 && c > 0 && hw % 8 == 0 && hw > 0,
+             "attn_prep: needs channels %% 64 == 0 and tokens %% 8 == 0 (c=%d, hw=%d)", c, hw);
+  if (n == 0) return IG_OK;
+  const int64_t ctas = (int64_t)n * (c / 64) * ((hw + 127) / 128);
+  { attn_prep_kernel<<<(unsigned)ctas, 128, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+      reinterpret_cast<__nv_bfloat16*>(q), reinterpret_cast<__nv_bfloat16*>(k),
+      reinterpret_cast<const __nv_bfloat16*>(v), n, hw, c, reinterpret_cast<__nv_bfloat16*>(vt)); note_launch(); }
+  return cuda_check("ig_attn_prep");
+}
+
+int ig_attention(const void* q, const void* k, const void* vt, int32_t n, int32_t hw, int32_t c,
+                 void* y, void* cuda_stream) {
+  IG_REQUIRE(n >= 0 && c % 64 == 0 && c > 0 && hw % 8 == 0 && hw > 0,
+             "attention: needs channels %% 64 == 0 and tokens %% 8 == 0 (c=%d, hw=%d)", c, hw);
+  if (n == 0) return IG_OK;
+  if (!encode_fn()) {
+    set_error("ig_attention: cuTensorMapEncodeTiled unavailable");
+    return IG_ERR_CUDA;
+  }
+  const int heads = c / 64;
+  CUtensorMap mq, mk, mv;
+  if (make_pos_map(&mq, q, n, hw, c, 128) != IG_OK || make_pos_map(&mk, k, n, hw, c, 128) != IG_OK) {
+    set_error("ig_attention: cuTensorMapEncodeTiled(q/k) failed");
+    return IG_ERR_CUDA;
+  }
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)hw, (cuuint64_t)n * heads * 64};
+    cuuint64_t strides[1] = {(cuuint64_t)hw * 2};
+    cuuint32_t box[2] = {64, 64};
+    cuuint32_t es[2] = {1, 1};
+    if (encode_fn()(&mv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(vt), dims, strides,
+                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      set_error("ig_attention: cuTensorMapEncodeTiled(v^T) failed");
+      return IG_ERR_CUDA;
+    }
+  }
+  const int smem = AttnSmem::BYTES + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const int64_t ctas = (int64_t)n * heads * ((hw + 127) / 128);
+  { attention_kernel<<<(unsigned)ctas, 192, smem, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+      mq, mk, mv, n, hw, heads, reinterpret_cast<__nv_bfloat16*>(y), c); note_launch(); }
+  return cuda_check("ig_attention");
 }
 
 int ig_unet_output(const void* f, int32_t n, int32_t h, int32_t w, int32_t fc,

@@ -40,6 +40,9 @@ RES_T = 1.0 / 3.0            # mp_sum blend of the residual branch (EDM2 uses 0.
 RES_RA = (1 - RES_T) / math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
 RES_RB = RES_T / math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
 RES_Q = 2.0                  # ra / rb
+ATTN_T = 0.3                 # EDM2 attn_balance: x = mp_sum(x, attn(x), t=0.3)
+ATTN_RA = (1 - ATTN_T) / math.sqrt((1 - ATTN_T) ** 2 + ATTN_T ** 2)
+ATTN_RB = ATTN_T / math.sqrt((1 - ATTN_T) ** 2 + ATTN_T ** 2)
 FUSED_STEM = True            # input gather fused into the stem GEMM (ig_unet_stem)
 FUSED_UP = True              # 2x upsample folded into the consumer convs' TMA loads
 FUSED_OUT = True             # output conv + preconditioning in one kernel (ig_unet_out_head)
@@ -65,6 +68,8 @@ class UNetConfig:
     weight_seed: int = 0
     emb_dim: int = 64               # Fourier features of c_noise
     cin_pad: int = 64               # input planes padded to one 64-channel K block
+    attn_levels: tuple[int, ...] = (3,)   # EDM2 self-attention after the blocks of these
+    #                                       levels (heads of 64 channels; 32^2 at 256 px)
 
     def sigma_for(self, outer_step: int, steps: int) -> float:
         k = steps - outer_step
@@ -118,6 +123,8 @@ def build_program(cfg: UNetConfig) -> Program:
     def conv(name, cin, cout, taps, modulated=False, cout_pad=0):
         prog.convs[name] = ConvSpec(name, cin, cout, taps, cout_pad or cout, modulated)
 
+    attn = []      # (block name, channels): registered after every other conv so the
+    #                adding attention leaves the other layers' weight draws unchanged
     # encoder; the stem 3x3 conv over in_planes() planes runs tap-packed as a
     # 1x1 GEMM over 9 * in_planes <= cin_pad channels (see ig_unet_gather_input)
     conv("stem", cfg.cin_pad, ch[0], 1)
@@ -133,6 +140,9 @@ def build_program(cfg: UNetConfig) -> Program:
                 conv(nm + ".skip", cur, ch[lv], 1)
             prog.ops.append(("enc", nm, cur != ch[lv]))
             cur = ch[lv]
+            if lv in cfg.attn_levels:
+                prog.ops.append(("attn", nm, lv))
+                attn.append((nm, cur))
             skips.append(cur)
         if lv < L - 1:
             prog.ops.append(("down",))
@@ -147,10 +157,16 @@ def build_program(cfg: UNetConfig) -> Program:
             conv(nm + ".skip", cur + sk, ch[lv], 1)
             prog.ops.append(("dec", nm))
             cur = ch[lv]
+            if lv in cfg.attn_levels:
+                prog.ops.append(("attn", nm, lv))
+                attn.append((nm, cur))
         if lv > 0:
             prog.ops.append(("up",))
     conv("out", cur, cfg.data_channels, 9, cout_pad=16)
     prog.ops.append(("out",))
+    for nm, c in attn:
+        conv(nm + ".qkv", c, 3 * c, 1)      # rows [q (c) | k (c) | v (c)], heads of 64
+        conv(nm + ".proj", c, c, 1)
     assert not skips
     return prog
 
@@ -177,6 +193,12 @@ def conv_flops(cfg: UNetConfig, h: int, w: int, padded: bool = False) -> float:
             total += 2.0 * hh * ww * cfg.in_planes() * cout * 9    # the real 3x3 conv
         else:
             total += 2.0 * hh * ww * cs.cin * cout * cs.taps
+    # attention: q k^T and p v (4 N^2 C per layer; q/k/v/proj are 1x1 convs above)
+    for op in prog.ops:
+        if op[0] == "attn":
+            hh, ww = lv_res[op[2]]
+            tokens = hh * ww
+            total += 4.0 * tokens * tokens * cfg.channels()[op[2]]
     return total
 
 
@@ -327,6 +349,34 @@ class UNetDevice:
         x, xa = self.conv("stem", x_in, None, sigma)
         return self.forward_after_stem(x, xa, sigma)
 
+    def attention(self, nm: str, x: torch.Tensor):
+        """EDM2 self-attention block on x (standard NHWC layout):
+        x' = mp_sum(x, proj(attn(norm(q), norm(k), norm(v))), t=0.3), returns
+        (x', mp_silu(x')).  q/k/v and proj are 1x1 convs on the tensor cores,
+        the projection's epilogue applies the mp_sum and the activation."""
+        n, h, w, c = x.shape
+        hw = h * w
+        wq = self.w[nm + ".qkv"]                         # [3c][1][c] bf16
+        q, k, v = (torch.empty_like(x) for _ in range(3))
+        for j, dst in enumerate((q, k, v)):
+            p = ConvParams(n, h, w, c, 0, c, 1, x.data_ptr(), None,
+                           wq.data_ptr() + j * c * c * 2, None, None, None, 0.0, 1.0, 1.0,
+                           dst.data_ptr(), None)
+            conv_launch(p)
+        vt = torch.empty((n, c // 64, 64, hw), dtype=torch.bfloat16, device=x.device)
+        y = torch.empty_like(x)
+        st = dev.stream_ptr()
+        attn_launch(lambda: (call("ig_attn_prep", q.data_ptr(), k.data_ptr(), v.data_ptr(), n,
+                                  hw, c, vt.data_ptr(), st),
+                             call("ig_attention", q.data_ptr(), k.data_ptr(), vt.data_ptr(), n,
+                                  hw, c, y.data_ptr(), st)))
+        xo, xa = torch.empty_like(x), torch.empty_like(x)
+        p = ConvParams(n, h, w, c, 0, c, 1, y.data_ptr(), None, self.w[nm + ".proj"].data_ptr(),
+                       None, None, x.data_ptr(), float(ATTN_RA), float(ATTN_RB), MP_SILU_GAIN,
+                       xo.data_ptr(), xa.data_ptr())
+        conv_launch(p)
+        return xo, xa
+
     @staticmethod
     def _fusable_pool(h1: torch.Tensor, gut: bool, cout: int) -> bool:
         """The c2 conv producing (x, xa) can also write their 2x2 pool: the
@@ -338,7 +388,7 @@ class UNetDevice:
     def _gutter(self, lv: int, w: int) -> bool:
         """Level lv (width w) keeps its activations in the gutter layout: narrow
         levels below the stem whose convs the CTA-pair kernel covers."""
-        return bool(FUSED_GUTTER and lv >= 1 and w <= 64
+        return bool(FUSED_GUTTER and lv >= 1 and w <= 64 and lv not in self.cfg.attn_levels
                     and self.cfg.channels()[lv] in (64, 128, 256))
 
     def forward_after_stem(self, x: torch.Tensor, xa: torch.Tensor, sigma: float, head=None):
@@ -374,6 +424,10 @@ class UNetDevice:
                 x, xa = self.conv(nm + ".c2", h1, None, sigma, skip=(x,), wskip=wsk,
                                   scale=self._rb(c2.cout_pad), gutter=g, pool=pool)
                 skips.append((x, xa))
+            elif op[0] == "attn":
+                x, xa = self.attention(op[1], x)
+                if ops[k - 1][0] == "enc":
+                    skips[-1] = (x, xa)      # the block output pushed as the skip
             elif op[0] == "down":
                 ng = self._gutter(lv + 1, w // 2)
                 if pool is not None:
@@ -470,6 +524,19 @@ def conv_launch(p: ConvParams):
         b = torch.cuda.Event(enable_timing=True)
         a.record()
     check(lib().ig_conv_tc(p, dev.ptr(_WS) if nbytes else None, dev.stream_ptr()), "ig_conv_tc")
+    if TIMING.on:
+        b.record()
+        TIMING.events.append((a, b))
+
+
+def attn_launch(fn):
+    """Attention kernels under the same per-launch event timer as the convs
+    (bench.py's tensor-core roofline covers both)."""
+    if TIMING.on:
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+    fn()
     if TIMING.on:
         b.record()
         TIMING.events.append((a, b))

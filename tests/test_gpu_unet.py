@@ -616,3 +616,61 @@ def test_out_head_tap_in_n_matches_per_tap():
     for v, o in outs.items():
         assert (o - ref).abs().max().item() < 1e-3 * ref.abs().max().item() + 1e-4, v
     assert (outs[0] - outs[8]).abs().max().item() < 1e-4 * ref.abs().max().item() + 1e-5
+
+
+def _attn_ref(q, k, v, heads):
+    """EDM2 attention in fp32 torch: per head of 64 channels, unit-RMS q, k, v,
+    y = softmax(q k^T / sqrt(64)) v.  q, k, v: (n, hw, c)."""
+    n, hw, c = q.shape
+
+    def nrm(t):
+        t = t.float().reshape(n, hw, heads, 64)
+        return t / (1e-4 + t.norm(dim=-1, keepdim=True) / 8.0)
+
+    qn, kn, vn = nrm(q), nrm(k), nrm(v)
+    s = torch.einsum("nqhd,nkhd->nhqk", qn, kn) / 8.0
+    p = s.softmax(dim=-1)
+    return torch.einsum("nhqk,nkhd->nqhd", p, vn).reshape(n, hw, c), qn, kn, vn
+
+
+@pytest.mark.parametrize("n,hw,c", [(2, 1024, 256), (3, 256, 128), (1, 128, 64),
+                                    (2, 64, 256), (1, 200, 128)])
+def test_attention_kernel_matches_torch(n, hw, c):
+    g = torch.Generator(device=DEV).manual_seed(hw + c + n)
+    q = (torch.randn(n, hw, c, device=DEV, generator=g) * 1.3).bfloat16()
+    k = (torch.randn(n, hw, c, device=DEV, generator=g) * 0.7).bfloat16()
+    v = torch.randn(n, hw, c, device=DEV, generator=g).bfloat16()
+    ref, qn, kn, vn = _attn_ref(q, k, v, c // 64)
+    qd, kd = q.clone(), k.clone()
+    vt = torch.empty(n, c // 64, 64, hw, device=DEV, dtype=torch.bfloat16)
+    y = torch.empty(n, hw, c, device=DEV, dtype=torch.bfloat16)
+    st = torch.cuda.current_stream().cuda_stream
+    call("ig_attn_prep", qd.data_ptr(), kd.data_ptr(), v.data_ptr(), n, hw, c, vt.data_ptr(), st)
+    call("ig_attention", qd.data_ptr(), kd.data_ptr(), vt.data_ptr(), n, hw, c, y.data_ptr(), st)
+    torch.cuda.synchronize()
+    # the prep kernel: normalised q, k in place and v transposed (bf16 rounding)
+    assert (qd.float().reshape(n, hw, c // 64, 64) - qn).abs().max().item() < 2e-2
+    vt_ref = vn.permute(0, 2, 3, 1)
+    assert (vt.float() - vt_ref).abs().max().item() < 2e-2
+    err = (y.float() - ref).abs()
+    assert err.max().item() < 3e-2 * ref.abs().max().item() + 1e-2, err.max().item()
+    assert err.pow(2).mean().sqrt().item() < 5e-3 * ref.pow(2).mean().sqrt().item() + 2e-3
+
+
+@pytest.mark.parametrize("win,nwin", [(128, 2), (256, 1)])
+def test_unet_with_attention_vs_fp32_oracle(win, nwin):
+    """The default 4-level network (EDM2 self-attention at level 3: 16^2 / 32^2
+    tokens) vs the fp32 CPU oracle, under the stated tolerance."""
+    from oracle.unet_ref import unet_phi
+    cfg = unet.UNetConfig()
+    assert 3 in cfg.attn_levels
+    wins, xs = _phi_inputs(cfg, nwin, win, seed=8)
+    wxy = torch.tensor([[b.x0, b.y0] for b in wins], dtype=torch.int64, device=DEV)
+    src = torch.from_numpy(xs).to(DEV)
+    got = unet.unet_phi_batch(cfg, src, None, wxy, win, 1, None, seed=8, steps=2).cpu().numpy()
+    ref_phi = unet_phi(cfg, 2, 8)
+    want = np.stack([ref_phi(xs[k], None, 1, wins[k]) for k in range(len(wins))])
+    std = float(want.std())
+    rms = float(np.sqrt(np.mean((got - want) ** 2))) / std
+    mx = float(np.abs(got - want).max()) / std
+    assert rms < UNET_RMS_TOL and mx < UNET_MAX_TOL, (rms, mx)

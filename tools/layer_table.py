@@ -55,6 +55,13 @@ def layer_ops(cfg, win):
             # c2 with the fused skip GEMM: reads the block input (c1.cin) once more
             seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, 2, c1.cin / c2.cout))
             c = c2.cout
+        elif op[0] == "attn":
+            nm = op[1]
+            for j in "qkv":
+                seq.append(("conv", f"{nm}.{j}", h, c, c, 1, 1, 0))
+            seq.append(("attn_prep", nm + ".prep", h, c, 0, 0, 0, 0))
+            seq.append(("attn", nm + ".attn", h, c, 0, 0, 0, 0))
+            seq.append(("conv", nm + ".proj", h, c, c, 1, 2, 1))
         elif op[0] == "down":
             seq.append(("pool", "down", h, 0, 0, 0, 0, 0))
             h //= 2
@@ -94,8 +101,12 @@ def main():
     for (kind, name, h, cin, cout, taps, outs, res), (kname, us) in zip(seq, last):
         px = n * h * h
         fl = 2.0 * px * cin * cout * taps if kind == "conv" else 0.0
+        if kind == "attn":             # q k^T + p v per window: 4 N^2 C
+            fl = 4.0 * n * (h * h) ** 2 * cin
         if kind == "conv":
             by = px * 2 * (cin + cout * (outs + res))
+        elif kind in ("attn", "attn_prep"):
+            by = px * 2 * cin * 4
         elif kind == "up":
             by = px * 2 * cin * 5            # read h^2 c, write (2h)^2 c
         else:
