@@ -2257,6 +2257,10 @@ __global__ void __launch_bounds__(128) attn_prep_kernel(__nv_bfloat16* __restric
   for (int which = 0; which < 2 && live; ++which) {
     __nv_bfloat16* p = (which ? k : q) + base;
     norm_row(p, f);
+    if (which == 0) {      // q carries the softmax scale: s = q.k / 8 in log2 units
+#pragma unroll
+      for (int i = 0; i < 64; ++i) f[i] *= 0.125f * 1.4426950408889634f;
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       uint4 u;
@@ -2283,59 +2287,104 @@ __global__ void __launch_bounds__(128) attn_prep_kernel(__nv_bfloat16* __restric
 }
 
 // attention_kernel: one CTA per (window, head, 128-query tile); tcgen05 with
-// TMEM accumulators, two-pass softmax (pass 1: row max / sum over all keys;
-// pass 2: P = exp(s - m) / l in bf16 -> SMEM -> O += P V), so O never needs
-// rescaling in TMEM.  Warp 0: TMA, warp 1: MMA issue, warps 2-5: softmax /
-// epilogue (thread = query row = TMEM lane).
+// TMEM accumulators, ONE pass and no running max: q and k are unit-RMS
+// normalised, so |q.k| / 8 <= 8 (Cauchy-Schwarz) and exp(s) <= e^8 ~ 3e3 can
+// neither overflow f32 nor bf16 -- P = exp(s) is accumulated unnormalised
+// (O += P V in TMEM, l = sum P in f32) and y = O / l at the end; no O
+// rescaling ever.  Warp 0: TMA, warp 1: MMA issue, warps 2-9: softmax (two
+// warp groups per TMEM lane quarter, group g owns keys [64g, 64g+64) of
+// every tile) and the epilogue.
 //   S = Q K^T: M=128 queries, N=128 keys, K=64 dims (4 x K16); S double-buffered
 //   O += P V:  M=128, N=64 dims, K=128 keys (8 x K16; P and V^T as 2 x 64-key chunks)
+__device__ __forceinline__ void named_bar_sync(int id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ float ex2_approx(float x) {   // MUFU.EX2, ex2(-inf) = 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 2^x on the FMA pipe (offloads the MUFU): x = n + f, n = rint(x) via the
+// 1.5*2^23 magic constant, f in [-1/2, 1/2], 2^f by its cubic Taylor
+// polynomial (relative error < 7e-4, well inside bf16's 3.9e-3), exponent
+// added into the float's bits.  Inputs below -126 (masked keys) give ~2^-126.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;
+  const float fl = t - 12582912.f;
+  const float f = x - fl;
+  float p = fmaf(0.0555041087f, f, 0.2402265070f);
+  p = fmaf(p, f, 0.6931471806f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
 struct AttnSmem {
-  static constexpr int Q = 0;                        // 16 KB  [128 q][64 d]
-  static constexpr int K0 = 16384;                   // 2 x 16 KB [128 keys][64 d]
+  static constexpr int Q0 = 0;                       // 2 x 16 KB [128 q][64 d]
+  static constexpr int K0 = 2 * 16384;               // 2 x 16 KB [128 keys][64 d]
   static constexpr int V0 = K0 + 2 * 16384;          // 2 x 16 KB [2 chunks][64 d][64 keys]
   static constexpr int P0 = V0 + 2 * 16384;          // 2 x 32 KB [2 chunks][128 q][64 keys]
-  static constexpr int BARS = P0 + 2 * 32768;        // barriers
+  static constexpr int L = P0 + 2 * 32768;           // [4][128] floats: partial row sums
+  static constexpr int BARS = L + 2048;              // barriers
   static constexpr int BYTES = BARS + 256;
 };
 
-__global__ void __launch_bounds__(192, 1) attention_kernel(
+// persistent: CTA b walks work items b, b + grid, ... (item = (window, head,
+// 128-query tile)); the K/V/S/P rings run over the CTA's global key-tile
+// sequence, Q and the O accumulator are double-buffered per item, so the next
+// item's loads and MMAs overlap the previous item's epilogue.
+constexpr int ATT_NG = 4;                            // softmax warp groups (32 keys each)
+
+__global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
     const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
     const __grid_constant__ CUtensorMap map_vt, int n, int hw, int heads,
     __nv_bfloat16* __restrict__ y, int c) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + AttnSmem::BARS);
-  uint64_t* qfull = bars;            // [1]
-  uint64_t* kfull = bars + 1;        // [2]
-  uint64_t* kempty = bars + 3;       // [2]
-  uint64_t* vfull = bars + 5;        // [2]
-  uint64_t* vempty = bars + 7;       // [2]
-  uint64_t* sfull = bars + 9;        // [2]
-  uint64_t* sempty = bars + 11;      // [2]
-  uint64_t* pfull = bars + 13;       // [2]
-  uint64_t* pempty = bars + 15;      // [2]
-  uint64_t* ofull = bars + 17;       // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  float* s_l = reinterpret_cast<float*>(sm + AttnSmem::L);
+  uint64_t* qfull = bars;            // [2]
+  uint64_t* qempty = bars + 2;       // [2]
+  uint64_t* kfull = bars + 4;        // [2]
+  uint64_t* kempty = bars + 6;       // [2]
+  uint64_t* vfull = bars + 8;        // [2]
+  uint64_t* vempty = bars + 10;      // [2]
+  uint64_t* sfull = bars + 12;       // [2]
+  uint64_t* sempty = bars + 14;      // [2]
+  uint64_t* pfull = bars + 16;       // [2]
+  uint64_t* pempty = bars + 18;      // [2]
+  uint64_t* ofull = bars + 20;       // [2]
+  uint64_t* oempty = bars + 22;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qtiles = (hw + 127) / 128, ktiles = (hw + 127) / 128;
-  const int qt = blockIdx.x % qtiles, hd = (blockIdx.x / qtiles) % heads;
-  const int img = blockIdx.x / (qtiles * heads);
+  const int nitems = n * heads * qtiles;
+  const int my_items = blockIdx.x < nitems ? (nitems - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int T = my_items * ktiles;                    // this CTA's key tiles, in order
+  auto item_of = [&](int it, int& img, int& hd, int& qt) {
+    const int w = blockIdx.x + it * gridDim.x;
+    qt = w % qtiles;
+    hd = (w / qtiles) % heads;
+    img = w / (qtiles * heads);
+  };
 
   if (warp == 0 && lane == 0) {
     prefetch_map(&map_q);
     prefetch_map(&map_k);
     prefetch_map(&map_vt);
-    mbar_init(qfull, 1);
-    mbar_init(ofull, 1);
     for (int s = 0; s < 2; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], 128 * ATT_NG);
+      mbar_init(&qfull[s], 1);
+      mbar_init(&qempty[s], 1);
       mbar_init(&kfull[s], 1);
       mbar_init(&kempty[s], 1);
       mbar_init(&vfull[s], 1);
       mbar_init(&vempty[s], 1);
-      mbar_init(&sfull[s], 1);
-      mbar_init(&sempty[s], 128);
-      mbar_init(&pfull[s], 128);
+      mbar_init(&pfull[s], 128 * ATT_NG);
       mbar_init(&pempty[s], 1);
+      mbar_init(&ofull[s], 1);
+      mbar_init(&oempty[s], 128 * ATT_NG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -2348,54 +2397,62 @@ __global__ void __launch_bounds__(192, 1) attention_kernel(
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;        // S buffers at cols 0 / 128, O at 256
+  const uint32_t tmem = *tmem_slot;        // S buffers at cols 0 / 128, O buffers at 256 / 320
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      mbar_expect_tx(qfull, 16384);
-      tma_load_3d(sm + AttnSmem::Q, &map_q, qfull, hd * 64, qt * 128, img);
-      // K tiles: pass 1 (0..kt-1) then pass 2 (again); V^T tiles in pass 2
-      for (int i = 0; i < 2 * ktiles; ++i) {
-        const int s = i & 1, ph = (i >> 1) & 1, kt = i % ktiles;
+      int it = 0, j = 0, img = 0, hd = 0, qt = 0;
+      for (int t = 0; t < T; ++t) {
+        if (j == 0) item_of(it, img, hd, qt);
+        if (j == 0) {
+          const int qb = it & 1, qph = (it >> 1) & 1;
+          mbar_wait(&qempty[qb], qph ^ 1);
+          mbar_expect_tx(&qfull[qb], 16384);
+          tma_load_3d(sm + AttnSmem::Q0 + qb * 16384, &map_q, &qfull[qb], hd * 64, qt * 128, img);
+        }
+        const int s = t & 1, ph = (t >> 1) & 1;
         mbar_wait(&kempty[s], ph ^ 1);
         mbar_expect_tx(&kfull[s], 16384);
-        tma_load_3d(sm + AttnSmem::K0 + s * 16384, &map_k, &kfull[s], hd * 64, kt * 128, img);
-        if (i >= ktiles) {
-          const int j = i - ktiles, vs = j & 1, vph = (j >> 1) & 1;
-          mbar_wait(&vempty[vs], vph ^ 1);
-          mbar_expect_tx(&vfull[vs], 16384);
-          const int row = (img * heads + hd) * 64;
-          uint8_t* vd = sm + AttnSmem::V0 + vs * 16384;
-          tma_load_2d(vd, &map_vt, &vfull[vs], kt * 128, row);
-          tma_load_2d(vd + 8192, &map_vt, &vfull[vs], kt * 128 + 64, row);
-        }
+        tma_load_3d(sm + AttnSmem::K0 + s * 16384, &map_k, &kfull[s], hd * 64, j * 128, img);
+        mbar_wait(&vempty[s], ph ^ 1);
+        mbar_expect_tx(&vfull[s], 16384);
+        const int row = (img * heads + hd) * 64;
+        uint8_t* vd = sm + AttnSmem::V0 + s * 16384;
+        tma_load_2d(vd, &map_vt, &vfull[s], j * 128, row);
+        tma_load_2d(vd + 8192, &map_vt, &vfull[s], j * 128 + 64, row);
+        if (++j == ktiles) { j = 0; ++it; }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     constexpr uint32_t idesc_s = idesc_bf16(128, 128);
     constexpr uint32_t idesc_o = idesc_bf16(128, 64);
-    mbar_wait(qfull, 0);
-    tc_fence_after();
-    const uint64_t qdesc = smem_desc_sw128(smem_u32(sm + AttnSmem::Q));
-    auto issue_s = [&](int i) {
-      const int s = i & 1, ph = (i >> 1) & 1;
+    auto issue_s = [&](int t, int it, int j) {
+      const int qb = it & 1;
+      const int s = t & 1, ph = (t >> 1) & 1;
+      if (j == 0) mbar_wait(&qfull[qb], (it >> 1) & 1);
       mbar_wait(&kfull[s], ph);
       mbar_wait(&sempty[s], ph ^ 1);
       tc_fence_after();
       if (elect_one()) {
+        const uint64_t qdesc = smem_desc_sw128(smem_u32(sm + AttnSmem::Q0 + qb * 16384));
         const uint64_t kdesc = smem_desc_sw128(smem_u32(sm + AttnSmem::K0 + s * 16384));
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           tc_mma(tmem + s * 128, qdesc + 2 * kk, kdesc + 2 * kk, idesc_s, kk ? 1u : 0u);
         tc_commit(&kempty[s]);
         tc_commit(&sfull[s]);
+        if (j == ktiles - 1) tc_commit(&qempty[qb]);
       }
       __syncwarp();
     };
-    auto issue_pv = [&](int j) {
-      const int ps = j & 1, ph = (j >> 1) & 1;
+    auto issue_pv = [&](int t, int it, int j) {
+      const int ob = it & 1;
+      const int ps = t & 1, ph = (t >> 1) & 1;
+      if (j == 0) {
+        mbar_wait(&oempty[ob], ((it >> 1) & 1) ^ 1);
+      }
       mbar_wait(&vfull[ps], ph);
       mbar_wait(&pfull[ps], ph);
       tc_fence_after();
@@ -2408,104 +2465,105 @@ __global__ void __launch_bounds__(192, 1) attention_kernel(
               smem_desc_sw128(smem_u32(sm + AttnSmem::V0 + ps * 16384 + ch * 8192));
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            tc_mma(tmem + 256, pdesc + 2 * kk, vdesc + 2 * kk, idesc_o, (j | ch | kk) ? 1u : 0u);
+            tc_mma(tmem + 256 + ob * 64, pdesc + 2 * kk, vdesc + 2 * kk, idesc_o,
+                   (j | ch | kk) ? 1u : 0u);
         }
         tc_commit(&pempty[ps]);
         tc_commit(&vempty[ps]);
-        if (j == ktiles - 1) tc_commit(ofull);
+        if (j == ktiles - 1) tc_commit(&ofull[ob]);
       }
       __syncwarp();
     };
-    for (int i = 0; i < ktiles; ++i) issue_s(i);             // pass 1
-    issue_s(ktiles);                                          // pass 2: S_0
-    for (int j = 0; j < ktiles; ++j) {
-      if (j + 1 < ktiles) issue_s(ktiles + j + 1);            // S_{j+1} overlaps softmax_j
-      issue_pv(j);
+    if (T > 0) issue_s(0, 0, 0);
+    int it = 0, j = 0, it1 = ktiles > 1 ? 0 : 1, j1 = ktiles > 1 ? 1 : 0;   // (it1, j1): tile t+1
+    for (int t = 0; t < T; ++t) {
+      if (t + 1 < T) issue_s(t + 1, it1, j1);                 // S_{t+1} overlaps softmax_t
+      issue_pv(t, it, j);
+      if (++j == ktiles) { j = 0; ++it; }
+      if (++j1 == ktiles) { j1 = 0; ++it1; }
     }
   } else {
-    // ---------------- softmax / epilogue (warps 2..5) ----------------
+    // ---------------- softmax / epilogue (warps 2 .. 2 + 4*ATT_NG) ----------------
+    // warp group g (4 warps, one per TMEM lane quarter) owns keys [32g, 32g+32)
+    // of every tile and dims [16g, 16g+16) of the output
+    constexpr int KG = 128 / ATT_NG, DG = 64 / ATT_NG;
     const int quarter = warp & 3;
+    const int grp = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;                      // query row == TMEM lane
     const uint32_t lanebase = (uint32_t)(quarter * 32) << 16;
-    const float sc = 0.125f * 1.4426950408889634f;           // 1/sqrt(64) * log2(e)
-    float m = -INFINITY, l = 0.f;
-    // keys past hw (zero-filled K rows of the last tile) are masked out
-    auto load_s = [&](int s, int kt, float* v) {
-      const int kvalid = hw - kt * 128;
+    constexpr uint32_t BAR_N = 128 * ATT_NG;
+    float l = 0.f;
+    int it = 0, j = 0;
+    for (int t = 0; t < T; ++t) {
+      const int s = t & 1, ph = (t >> 1) & 1;
+      mbar_wait(&sfull[s], ph);
+      tc_fence_after();
+      uint32_t r[KG];
+      tmem_ld32_nw(tmem + lanebase + s * 128 + grp * KG, r);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&sempty[s]);
+      const int kvalid = hw - j * 128 - grp * KG;             // keys of this group in range
+      if (kvalid < KG) {                                      // partial last tile: mask
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        uint32_t r[32];
-        tmem_ld32_nw(tmem + lanebase + s * 128 + b * 32, r);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          v[b * 32 + i] = (b * 32 + i < kvalid) ? __uint_as_float(r[i]) * sc : -INFINITY;
+        for (int kk = 0; kk < KG; ++kk)
+          if (kk >= kvalid) r[kk] = __float_as_uint(-INFINITY);
       }
-    };
-    // pass 1: row max / sum (log2 domain)
-    for (int i = 0; i < ktiles; ++i) {
-      const int s = i & 1, ph = (i >> 1) & 1;
-      mbar_wait(&sfull[s], ph);
-      tc_fence_after();
-      float v[128];
-      load_s(s, i, v);
-      tc_fence_before();
-      mbar_arrive(&sempty[s]);
-      float mx = m;
+      // (q carries 1/8 * log2 e, so S is already in ex2 units.  r01: routing
+      // half of these through ex2_poly on the FMA pipe measured slower)
+      float p[KG];
 #pragma unroll
-      for (int t = 0; t < 128; ++t) mx = fmaxf(mx, v[t]);
-      float sum = 0.f;
+      for (int kk = 0; kk < KG; ++kk) p[kk] = ex2_approx(__uint_as_float(r[kk]));
+      float l4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int t = 0; t < 128; ++t) sum += exp2f(v[t] - mx);
-      l = l * exp2f(m - mx) + sum;
-      m = mx;
-    }
-    const float inv_l = 1.f / l;
-    // pass 2: P = exp2(s - m) / l (bf16) into the K-major SW128 P tile
-    for (int j = 0; j < ktiles; ++j) {
-      const int i = ktiles + j, s = i & 1, ph = (i >> 1) & 1;
-      const int ps = j & 1, pph = (j >> 1) & 1;
-      mbar_wait(&sfull[s], ph);
-      tc_fence_after();
-      float v[128];
-      load_s(s, j, v);
-      tc_fence_before();
-      mbar_arrive(&sempty[s]);
-      mbar_wait(&pempty[ps], pph ^ 1);
-      uint8_t* pbase = sm + AttnSmem::P0 + ps * 32768;
+      for (int kk = 0; kk < KG; ++kk) l4[kk & 3] += p[kk];
+      l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+      mbar_wait(&pempty[s], ph ^ 1);
+      // keys [32g, 32g+32): 64-key chunk g/2, 16-byte columns 4*(g%2) .. +3
+      uint8_t* pbase = sm + AttnSmem::P0 + s * 32768 + (grp * KG / 64) * 16384;
+      const int c0 = (grp * KG % 64) / 8;
 #pragma unroll
-      for (int ch = 0; ch < 2; ++ch)
+      for (int c8 = 0; c8 < KG / 8; ++c8) {
+        uint4 u;
+        __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) {
-          uint4 u;
-          __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int key = ch * 64 + c8 * 8 + 2 * t;
-            o[t] = __floats2bfloat162_rn(exp2f(v[key] - m) * inv_l, exp2f(v[key + 1] - m) * inv_l);
-          }
-          *reinterpret_cast<uint4*>(pbase + ch * 16384 + row * 128 + ((c8 ^ (row & 7)) * 16)) = u;
-        }
+        for (int q2 = 0; q2 < 4; ++q2)
+          o[q2] = __floats2bfloat162_rn(p[c8 * 8 + 2 * q2], p[c8 * 8 + 2 * q2 + 1]);
+        *reinterpret_cast<uint4*>(pbase + row * 128 + (((c0 + c8) ^ (row & 7)) * 16)) = u;
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&pfull[ps]);
-    }
-    // epilogue: O (64 cols) -> bf16 -> y[img][token][hd*64 ..]
-    mbar_wait(ofull, 0);
-    tc_fence_after();
-    uint32_t r[64];
-    tmem_ld32_nw(tmem + lanebase + 256, r);
-    tmem_ld32_nw(tmem + lanebase + 288, r + 32);
-    tmem_wait_ld();
-    __nv_bfloat16* dst = y + ((int64_t)img * hw + qt * 128 + row) * c + hd * 64;
+      mbar_arrive(&pfull[s]);
+      if (j == ktiles - 1) {
+        // item done: the groups' partial row sums, then O / l
+        int img, hd, qt;
+        item_of(it, img, hd, qt);
+        const int ob = it & 1;
+        s_l[grp * 128 + row] = l;
+        named_bar_sync(1, BAR_N);
+        float lt = 0.f;
 #pragma unroll
-    for (int b = 0; b < 4 && qt * 128 + row < hw; ++b) {
-      uint4 u[2];
-      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(u);
+        for (int g2 = 0; g2 < ATT_NG; ++g2) lt += s_l[g2 * 128 + row];
+        named_bar_sync(1, BAR_N);                             // s_l read before it is reused
+        const float inv_l = 1.f / lt;
+        l = 0.f;
+        mbar_wait(&ofull[ob], (it >> 1) & 1);
+        tc_fence_after();
+        uint32_t ro[DG];
+        tmem_ld16(tmem + lanebase + 256 + ob * 64 + grp * DG, reinterpret_cast<float*>(ro));
+        tc_fence_before();
+        mbar_arrive(&oempty[ob]);
+        if (qt * 128 + row < hw) {
+          __nv_bfloat16* dst = y + ((int64_t)img * hw + qt * 128 + row) * c + hd * 64 + grp * DG;
+          uint4 u[2];
+          __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(u);
 #pragma unroll
-      for (int t = 0; t < 8; ++t)
-        o[t] = __floats2bfloat162_rn(__uint_as_float(r[16 * b + 2 * t]),
-                                     __uint_as_float(r[16 * b + 2 * t + 1]));
-      stg_v8(dst + 16 * b, u[0], u[1]);
+          for (int q2 = 0; q2 < 8; ++q2)
+            o[q2] = __floats2bfloat162_rn(__uint_as_float(ro[2 * q2]) * inv_l,
+                                          __uint_as_float(ro[2 * q2 + 1]) * inv_l);
+          stg_v8(dst, u[0], u[1]);
+        }
+      }
+      if (++j == ktiles) { j = 0; ++it; }
     }
   }
   tc_fence_before();
@@ -3301,8 +3359,9 @@ int ig_attention(const void* q, const void* k, const void* vt, int32_t n, int32_
     cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  const int64_t ctas = (int64_t)n * heads * ((hw + 127) / 128);
-  { attention_kernel<<<(unsigned)ctas, 192, smem, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+  const int64_t items = (int64_t)n * heads * ((hw + 127) / 128);
+  const int ctas = (int)(items < kNumSMs ? items : kNumSMs);
+  { attention_kernel<<<(unsigned)ctas, 64 + 128 * ATT_NG, smem, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       mq, mk, mv, n, hw, heads, reinterpret_cast<__nv_bfloat16*>(y), c); note_launch(); }
   return cuda_check("ig_attention");
 }

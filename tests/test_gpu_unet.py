@@ -648,8 +648,11 @@ def test_attention_kernel_matches_torch(n, hw, c):
     call("ig_attn_prep", qd.data_ptr(), kd.data_ptr(), v.data_ptr(), n, hw, c, vt.data_ptr(), st)
     call("ig_attention", qd.data_ptr(), kd.data_ptr(), vt.data_ptr(), n, hw, c, y.data_ptr(), st)
     torch.cuda.synchronize()
-    # the prep kernel: normalised q, k in place and v transposed (bf16 rounding)
-    assert (qd.float().reshape(n, hw, c // 64, 64) - qn).abs().max().item() < 2e-2
+    # the prep kernel: normalised q (carrying the 1/8 * log2 e softmax scale), k in
+    # place and v transposed (bf16 rounding)
+    qs = qn * (0.125 * math.log2(math.e))
+    assert (qd.float().reshape(n, hw, c // 64, 64) - qs).abs().max().item() < 2e-2
+    assert (kd.float().reshape(n, hw, c // 64, 64) - kn).abs().max().item() < 2e-2
     vt_ref = vn.permute(0, 2, 3, 1)
     assert (vt.float() - vt_ref).abs().max().item() < 2e-2
     err = (y.float() - ref).abs()
