@@ -197,6 +197,11 @@ typedef struct {
    * cout 64 / 128, 2-D layout). */
   void* pool0;
   void* pool1;
+  /* head_norm != 0: out0 = head_scale * x / (1e-4 + ||x|| / 8) per 64-channel
+   * head of the (scaled) accumulator -- EDM2 attention q / k / v -- instead of
+   * the plain epilogue (cout % 128 == 0, out0 only). */
+  int32_t head_norm;
+  float head_scale;
 } ig_conv_params_t;
 size_t ig_conv_workspace_bytes(void);
 /* 0: automatic; 1: force the per-tap kernel; 2: halo kernel instead of the row ring */
@@ -228,13 +233,15 @@ int ig_unet_out_head(const void* xa, int32_t n, int32_t h, int32_t w, int32_t ci
                      const void* w_out, int32_t cout_pad, int32_t channels, const float* x_noisy,
                      float c_skip, float c_out, float* out, void* cuda_stream);
 /* EDM2 self-attention over n windows of hw tokens (NHWC bf16, c channels,
- * heads of 64): ig_attn_prep unit-RMS-normalises q, k in place per token and
- * head and writes the normalised v transposed ([n][c/64][64][hw]);
- * ig_attention computes y = softmax(q k^T / 8) v per head (tcgen05, f32
- * accumulation and softmax).  hw % 8 == 0 (partial 128-token tiles masked). */
-int ig_attn_prep(void* q, void* k, const void* v, int32_t n, int32_t hw, int32_t c, void* vt,
+ * heads of 64): ig_attn_prep unit-RMS-normalises q, k, v in place per token
+ * and head (q additionally carries the softmax scale 1/8 * log2 e), and writes
+ * the normalised v transposed ([n][c/64][64][hw]) when vt != NULL;
+ * ig_attention computes y = softmax(q k^T / 8) v per head from the prepared
+ * q, k, v (tcgen05, f32 accumulation and softmax; V read as an MN-major
+ * operand).  hw % 8 == 0 (partial 128-token tiles masked). */
+int ig_attn_prep(void* q, void* k, void* v, int32_t n, int32_t hw, int32_t c, void* vt,
                  void* cuda_stream);
-int ig_attention(const void* q, const void* k, const void* vt, int32_t n, int32_t hw, int32_t c,
+int ig_attention(const void* q, const void* k, const void* v, int32_t n, int32_t hw, int32_t c,
                  void* y, void* cuda_stream);
 int ig_avgpool2_bf16(const void* in, int32_t n, int32_t h, int32_t w, int32_t c, void* out,
                      void* out_act, int32_t layout, void* cuda_stream);

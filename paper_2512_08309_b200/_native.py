@@ -31,7 +31,8 @@ class ConvParams(ctypes.Structure):
                 ("bias", V), ("res", V), ("res_a", F32), ("res_b", F32), ("act_gain", F32),
                 ("out0", V), ("out1", V), ("csa", I32), ("csb", I32), ("skip_a", V),
                 ("skip_b", V), ("wskip", V), ("up2", I32), ("up_in", I32),
-                ("gutter", I32), ("pool0", V), ("pool1", V)]
+                ("gutter", I32), ("pool0", V), ("pool1", V), ("head_norm", I32),
+                ("head_scale", F32)]
 
 
 # name -> argtypes (every function returns int32 status unless listed in _RESTYPES)

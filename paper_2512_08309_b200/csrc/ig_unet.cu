@@ -173,6 +173,19 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
   return d;
 }
 
+// MN-major SW128 operand (rows of 128 B = 64 elements along M/N, consecutive
+// rows along K, 8-row atoms 1024 B apart): the natural [K][64] tile a TMA box
+// of 64 elements x K rows writes.  Advance the start by 16 rows (2048 B) per K16.
+__device__ __forceinline__ uint64_t smem_desc_sw128_mn(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
+  d |= (uint64_t)(8192 >> 4) << 16;                // LBO: next 64-element MN block (unused, N=64)
+  d |= (uint64_t)(1024 >> 4) << 32;                // SBO: 8 K-rows x 128 B
+  d |= (uint64_t)1 << 46;                          // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
+  return d;
+}
+
 // instruction descriptor: D f32, A/B bf16, both K-major, M=128, N
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
@@ -202,6 +215,8 @@ struct ConvArgs {
   __nv_bfloat16* pool0;   // fused 2x2 mean pool of out0 -> [n][h/2][w/2][cout] (or null)
   __nv_bfloat16* pool1;   // and its mp_silu
   int pool_gut;           // pooled tensors in the gutter layout
+  int head_norm;          // out0 = head_scale * unit-RMS per 64-channel head (attention q/k/v)
+  float head_scale;
   const __nv_bfloat16* skip_a;
   const __nv_bfloat16* skip_b;
   const __nv_bfloat16* wskip;
@@ -334,6 +349,37 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
       stg_v8(base + o + rs + cout, v0, v1);
     }
   };
+  if constexpr (NC % 64 == 0) {
+    if (a.head_norm) {   // attention q / k / v: EDM2 normalize per head, then scale
+      const float hsc = a.head_scale;
+#pragma unroll 1
+      for (int hb = 0; hb < NC; hb += 64) {
+        uint32_t r[64];
+        tmem_ld32_nw(taddr + c0 + hb, r);
+        tmem_ld32_nw(taddr + c0 + hb + 32, r + 32);
+        tmem_wait_ld();
+        float ss = 0.f;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const float v = __uint_as_float(r[i]) * (s_scale ? s_scale[c0 + hb + i] : 1.f);
+          r[i] = __float_as_uint(v);
+          ss = fmaf(v, v, ss);
+        }
+        const float inv = hsc / (1e-4f + sqrtf(ss) * 0.125f);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint4 o[2];
+          __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(o);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            ob[j] = __floats2bfloat162_rn(__uint_as_float(r[16 * i + 2 * j]) * inv,
+                                          __uint_as_float(r[16 * i + 2 * j + 1]) * inv);
+          stg_v8(out0 + p * cout + c0 + hb + 16 * i, o[0], o[1]);
+        }
+      }
+      return;
+    }
+  }
   constexpr int BC = NC < 32 ? NC : 32;
   const int64_t off = p * cout + c0;
   const int64_t ob0 = out_base(a, p) + c0;
@@ -2224,7 +2270,7 @@ constexpr float ATTN_EPS = 1e-4f;
 
 __global__ void __launch_bounds__(128) attn_prep_kernel(__nv_bfloat16* __restrict__ q,
                                                         __nv_bfloat16* __restrict__ k,
-                                                        const __nv_bfloat16* __restrict__ v,
+                                                        __nv_bfloat16* __restrict__ v,
                                                         int n, int hw, int c,
                                                         __nv_bfloat16* __restrict__ vt) {
   __shared__ __nv_bfloat16 tile[64][128 + 8];   // [dim][token] (padded)
@@ -2270,7 +2316,19 @@ __global__ void __launch_bounds__(128) attn_prep_kernel(__nv_bfloat16* __restric
       reinterpret_cast<uint4*>(p)[i] = u;
     }
   }
-  norm_row(v + base, f);
+  if (live) {
+    norm_row(v + base, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {       // normalised v in place (the attention kernel's B)
+      uint4 u;
+      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int j2 = 0; j2 < 4; ++j2)
+        o[j2] = __floats2bfloat162_rn(f[8 * i + 2 * j2], f[8 * i + 2 * j2 + 1]);
+      reinterpret_cast<uint4*>(v + base)[i] = u;
+    }
+  }
+  if (!vt) return;                      // (transposed copy only on request)
 #pragma unroll
   for (int d = 0; d < 64; ++d) tile[d][threadIdx.x] = __float2bfloat16_rn(f[d]);
   __syncthreads();
@@ -2322,7 +2380,7 @@ __device__ __forceinline__ float ex2_poly(float x) {
 struct AttnSmem {
   static constexpr int Q0 = 0;                       // 2 x 16 KB [128 q][64 d]
   static constexpr int K0 = 2 * 16384;               // 2 x 16 KB [128 keys][64 d]
-  static constexpr int V0 = K0 + 2 * 16384;          // 2 x 16 KB [2 chunks][64 d][64 keys]
+  static constexpr int V0 = K0 + 2 * 16384;          // 2 x 16 KB [128 keys][64 d] (MN-major B)
   static constexpr int P0 = V0 + 2 * 16384;          // 2 x 32 KB [2 chunks][128 q][64 keys]
   static constexpr int L = P0 + 2 * 32768;           // [4][128] floats: partial row sums
   static constexpr int BARS = L + 2048;              // barriers
@@ -2337,7 +2395,7 @@ constexpr int ATT_NG = 4;                            // softmax warp groups (32 
 
 __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
     const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-    const __grid_constant__ CUtensorMap map_vt, int n, int hw, int heads,
+    const __grid_constant__ CUtensorMap map_v, int n, int hw, int heads,
     __nv_bfloat16* __restrict__ y, int c) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -2371,7 +2429,7 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
   if (warp == 0 && lane == 0) {
     prefetch_map(&map_q);
     prefetch_map(&map_k);
-    prefetch_map(&map_vt);
+    prefetch_map(&map_v);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sfull[s], 1);
       mbar_init(&sempty[s], 128 * ATT_NG);
@@ -2417,17 +2475,14 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
         tma_load_3d(sm + AttnSmem::K0 + s * 16384, &map_k, &kfull[s], hd * 64, j * 128, img);
         mbar_wait(&vempty[s], ph ^ 1);
         mbar_expect_tx(&vfull[s], 16384);
-        const int row = (img * heads + hd) * 64;
-        uint8_t* vd = sm + AttnSmem::V0 + s * 16384;
-        tma_load_2d(vd, &map_vt, &vfull[s], j * 128, row);
-        tma_load_2d(vd + 8192, &map_vt, &vfull[s], j * 128 + 64, row);
+        tma_load_3d(sm + AttnSmem::V0 + s * 16384, &map_v, &vfull[s], hd * 64, j * 128, img);
         if (++j == ktiles) { j = 0; ++it; }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     constexpr uint32_t idesc_s = idesc_bf16(128, 128);
-    constexpr uint32_t idesc_o = idesc_bf16(128, 64);
+    constexpr uint32_t idesc_o = idesc_bf16(128, 64) | (1u << 16);   // B (V) MN-major
     auto issue_s = [&](int t, int it, int j) {
       const int qb = it & 1;
       const int s = t & 1, ph = (t >> 1) & 1;
@@ -2461,12 +2516,13 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
         for (int ch = 0; ch < 2; ++ch) {
           const uint64_t pdesc =
               smem_desc_sw128(smem_u32(sm + AttnSmem::P0 + ps * 32768 + ch * 16384));
-          const uint64_t vdesc =
-              smem_desc_sw128(smem_u32(sm + AttnSmem::V0 + ps * 16384 + ch * 8192));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc_mma(tmem + 256 + ob * 64, pdesc + 2 * kk, vdesc + 2 * kk, idesc_o,
-                   (j | ch | kk) ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk) {
+            // V tile [128 keys][64 dims] as an MN-major B: keys 64ch + 16kk .. +16
+            const uint64_t vdesc = smem_desc_sw128_mn(
+                smem_u32(sm + AttnSmem::V0 + ps * 16384 + (ch * 64 + kk * 16) * 128));
+            tc_mma(tmem + 256 + ob * 64, pdesc + 2 * kk, vdesc, idesc_o, (j | ch | kk) ? 1u : 0u);
+          }
         }
         tc_commit(&pempty[ps]);
         tc_commit(&vempty[ps]);
@@ -3058,6 +3114,11 @@ static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   a->up_sa = (p->up_in >> 1) & 1;
   a->pool0 = reinterpret_cast<__nv_bfloat16*>(p->pool0);
   a->pool1 = reinterpret_cast<__nv_bfloat16*>(p->pool1);
+  a->head_norm = p->head_norm != 0;
+  a->head_scale = p->head_scale;
+  IG_REQUIRE(!p->head_norm || (p->cout % 128 == 0 && !p->res && !p->out1 && !p->up2 &&
+                               !p->pool0 && !(p->gutter & 1)),
+             "conv: head_norm needs cout %% 128 == 0, out0 only, no residual / pool / gutter");
   IG_REQUIRE(!p->pool0 || (p->pool1 && p->h % 2 == 0 && p->w % 2 == 0 && !p->up2 && !p->res),
              "conv: fused pool needs pool0 and pool1, an even image and no residual input");
   IG_REQUIRE((p->gutter & ~7) == 0, "conv: unknown gutter bits 0x%x", p->gutter);
@@ -3313,7 +3374,7 @@ int ig_unet_out_head(const void* xa, int32_t n, int32_t h, int32_t w, int32_t ci
   return launch(unet_out_head_kernel<4, 2>, 4, 2, OutCfg<4>::STRIDE);
 }
 
-int ig_attn_prep(void* q, void* k, const void* v, int32_t n, int32_t hw, int32_t c, void* vt,
+int ig_attn_prep(void* q, void* k, void* v, int32_t n, int32_t hw, int32_t c, void* vt,
                  void* cuda_stream) {
   IG_REQUIRE(n >= 0 && c % 64 == 0 && c > 0 && hw % 8 == 0 && hw > 0,
              "attn_prep: needs channels %% 64 == 0 and tokens %% 8 == 0 (c=%d, hw=%d)", c, hw);
@@ -3321,11 +3382,11 @@ int ig_attn_prep(void* q, void* k, const void* v, int32_t n, int32_t hw, int32_t
   const int64_t ctas = (int64_t)n * (c / 64) * ((hw + 127) / 128);
   { attn_prep_kernel<<<(unsigned)ctas, 128, 0, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       reinterpret_cast<__nv_bfloat16*>(q), reinterpret_cast<__nv_bfloat16*>(k),
-      reinterpret_cast<const __nv_bfloat16*>(v), n, hw, c, reinterpret_cast<__nv_bfloat16*>(vt)); note_launch(); }
+      reinterpret_cast<__nv_bfloat16*>(v), n, hw, c, reinterpret_cast<__nv_bfloat16*>(vt)); note_launch(); }
   return cuda_check("ig_attn_prep");
 }
 
-int ig_attention(const void* q, const void* k, const void* vt, int32_t n, int32_t hw, int32_t c,
+int ig_attention(const void* q, const void* k, const void* v, int32_t n, int32_t hw, int32_t c,
                  void* y, void* cuda_stream) {
   IG_REQUIRE(n >= 0 && c % 64 == 0 && c > 0 && hw % 8 == 0 && hw > 0,
              "attention: needs channels %% 64 == 0 and tokens %% 8 == 0 (c=%d, hw=%d)", c, hw);
@@ -3336,22 +3397,10 @@ int ig_attention(const void* q, const void* k, const void* vt, int32_t n, int32_
   }
   const int heads = c / 64;
   CUtensorMap mq, mk, mv;
-  if (make_pos_map(&mq, q, n, hw, c, 128) != IG_OK || make_pos_map(&mk, k, n, hw, c, 128) != IG_OK) {
-    set_error("ig_attention: cuTensorMapEncodeTiled(q/k) failed");
+  if (make_pos_map(&mq, q, n, hw, c, 128) != IG_OK || make_pos_map(&mk, k, n, hw, c, 128) != IG_OK ||
+      make_pos_map(&mv, v, n, hw, c, 128) != IG_OK) {
+    set_error("ig_attention: cuTensorMapEncodeTiled(q/k/v) failed");
     return IG_ERR_CUDA;
-  }
-  {
-    cuuint64_t dims[2] = {(cuuint64_t)hw, (cuuint64_t)n * heads * 64};
-    cuuint64_t strides[1] = {(cuuint64_t)hw * 2};
-    cuuint32_t box[2] = {64, 64};
-    cuuint32_t es[2] = {1, 1};
-    if (encode_fn()(&mv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(vt), dims, strides,
-                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
-      set_error("ig_attention: cuTensorMapEncodeTiled(v^T) failed");
-      return IG_ERR_CUDA;
-    }
   }
   const int smem = AttnSmem::BYTES + 1024;
   static bool attr = false;

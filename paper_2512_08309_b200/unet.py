@@ -41,6 +41,7 @@ RES_RA = (1 - RES_T) / math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
 RES_RB = RES_T / math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
 RES_Q = 2.0                  # ra / rb
 ATTN_T = 0.3                 # EDM2 attn_balance: x = mp_sum(x, attn(x), t=0.3)
+Q_SCALE = 0.125 * math.log2(math.e)   # softmax 1/sqrt(64) in log2 units, carried by q
 ATTN_RA = (1 - ATTN_T) / math.sqrt((1 - ATTN_T) ** 2 + ATTN_T ** 2)
 ATTN_RB = ATTN_T / math.sqrt((1 - ATTN_T) ** 2 + ATTN_T ** 2)
 FUSED_STEM = True            # input gather fused into the stem GEMM (ig_unet_stem)
@@ -358,18 +359,19 @@ class UNetDevice:
         hw = h * w
         wq = self.w[nm + ".qkv"]                         # [3c][1][c] bf16
         q, k, v = (torch.empty_like(x) for _ in range(3))
+        # the conv epilogues normalise each 64-channel head (q also carries the
+        # softmax scale 1/8 * log2 e), so the attention kernel reads them as is
         for j, dst in enumerate((q, k, v)):
             p = ConvParams(n, h, w, c, 0, c, 1, x.data_ptr(), None,
                            wq.data_ptr() + j * c * c * 2, None, None, None, 0.0, 1.0, 1.0,
                            dst.data_ptr(), None)
+            p.head_norm = 1
+            p.head_scale = Q_SCALE if j == 0 else 1.0
             conv_launch(p)
-        vt = torch.empty((n, c // 64, 64, hw), dtype=torch.bfloat16, device=x.device)
         y = torch.empty_like(x)
         st = dev.stream_ptr()
-        attn_launch(lambda: (call("ig_attn_prep", q.data_ptr(), k.data_ptr(), v.data_ptr(), n,
-                                  hw, c, vt.data_ptr(), st),
-                             call("ig_attention", q.data_ptr(), k.data_ptr(), vt.data_ptr(), n,
-                                  hw, c, y.data_ptr(), st)))
+        attn_launch(lambda: call("ig_attention", q.data_ptr(), k.data_ptr(), v.data_ptr(), n,
+                                 hw, c, y.data_ptr(), st))
         xo, xa = torch.empty_like(x), torch.empty_like(x)
         p = ConvParams(n, h, w, c, 0, c, 1, y.data_ptr(), None, self.w[nm + ".proj"].data_ptr(),
                        None, None, x.data_ptr(), float(ATTN_RA), float(ATTN_RB), MP_SILU_GAIN,

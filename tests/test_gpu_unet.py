@@ -641,13 +641,14 @@ def test_attention_kernel_matches_torch(n, hw, c):
     k = (torch.randn(n, hw, c, device=DEV, generator=g) * 0.7).bfloat16()
     v = torch.randn(n, hw, c, device=DEV, generator=g).bfloat16()
     ref, qn, kn, vn = _attn_ref(q, k, v, c // 64)
-    qd, kd = q.clone(), k.clone()
+    qd, kd, vd = q.clone(), k.clone(), v.clone()
     vt = torch.empty(n, c // 64, 64, hw, device=DEV, dtype=torch.bfloat16)
     y = torch.empty(n, hw, c, device=DEV, dtype=torch.bfloat16)
     st = torch.cuda.current_stream().cuda_stream
-    call("ig_attn_prep", qd.data_ptr(), kd.data_ptr(), v.data_ptr(), n, hw, c, vt.data_ptr(), st)
-    call("ig_attention", qd.data_ptr(), kd.data_ptr(), vt.data_ptr(), n, hw, c, y.data_ptr(), st)
+    call("ig_attn_prep", qd.data_ptr(), kd.data_ptr(), vd.data_ptr(), n, hw, c, vt.data_ptr(), st)
+    call("ig_attention", qd.data_ptr(), kd.data_ptr(), vd.data_ptr(), n, hw, c, y.data_ptr(), st)
     torch.cuda.synchronize()
+    assert (vd.float().reshape(n, hw, c // 64, 64) - vn).abs().max().item() < 2e-2
     # the prep kernel: normalised q (carrying the 1/8 * log2 e softmax scale), k in
     # place and v transposed (bf16 rounding)
     qs = qn * (0.125 * math.log2(math.e))
