@@ -197,9 +197,9 @@ typedef struct {
    * cout 64 / 128, 2-D layout). */
   void* pool0;
   void* pool1;
-  /* head_norm != 0: out0 = head_scale * x / (1e-4 + ||x|| / 8) per 64-channel
-   * head of the (scaled) accumulator -- EDM2 attention q / k / v -- instead of
-   * the plain epilogue (cout % 128 == 0, out0 only). */
+  /* head_norm 1 / 2: out0 = head_scale * x / (1e-4 + ||x|| / 8) per 64-channel
+   * head of the (scaled) accumulator, stored bf16 / f16 -- EDM2 attention q, k /
+   * v -- instead of the plain epilogue (cout % 128 == 0, out0 only). */
   int32_t head_norm;
   float head_scale;
 } ig_conv_params_t;
@@ -232,13 +232,15 @@ int ig_unet_output(const void* f, int32_t n, int32_t h, int32_t w, int32_t fc,
 int ig_unet_out_head(const void* xa, int32_t n, int32_t h, int32_t w, int32_t cin,
                      const void* w_out, int32_t cout_pad, int32_t channels, const float* x_noisy,
                      float c_skip, float c_out, float* out, void* cuda_stream);
-/* EDM2 self-attention over n windows of hw tokens (NHWC bf16, c channels,
- * heads of 64): ig_attn_prep unit-RMS-normalises q, k, v in place per token
- * and head (q additionally carries the softmax scale 1/8 * log2 e), and writes
- * the normalised v transposed ([n][c/64][64][hw]) when vt != NULL;
- * ig_attention computes y = softmax(q k^T / 8) v per head from the prepared
- * q, k, v (tcgen05, f32 accumulation and softmax; V read as an MN-major
- * operand).  hw % 8 == 0 (partial 128-token tiles masked). */
+/* EDM2 self-attention over n windows of hw tokens (NHWC, c channels, heads of
+ * 64): ig_attn_prep unit-RMS-normalises q, k (bf16) and v in place per token
+ * and head -- q additionally carries the softmax scale 1/8 * log2 e and v is
+ * rewritten as f16 -- and writes the normalised v transposed ([n][c/64][64][hw],
+ * bf16) when vt != NULL.  (The UNet produces the same operands from the q/k/v
+ * conv epilogues, ig_conv_params_t.head_norm.)  ig_attention computes
+ * y = softmax(q k^T / 8) v per head (bf16 out): tcgen05, S and O in TMEM, P = 2^s
+ * in f16, V read as an MN-major operand, the row sums from a ones block in the
+ * PV MMA.  hw % 8 == 0 (partial 128-token tiles masked). */
 int ig_attn_prep(void* q, void* k, void* v, int32_t n, int32_t hw, int32_t c, void* vt,
                  void* cuda_stream);
 int ig_attention(const void* q, const void* k, const void* v, int32_t n, int32_t hw, int32_t c,

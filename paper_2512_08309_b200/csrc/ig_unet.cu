@@ -17,6 +17,7 @@
 // No reference implementation exists (the reference ships analytic Phi only).
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include "ig_common.cuh"
@@ -369,11 +370,19 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           uint4 o[2];
-          __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(o);
+          if (a.head_norm == 2) {          // f16 (the attention kernel's V operand)
+            __half2* oh = reinterpret_cast<__half2*>(o);
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            ob[j] = __floats2bfloat162_rn(__uint_as_float(r[16 * i + 2 * j]) * inv,
-                                          __uint_as_float(r[16 * i + 2 * j + 1]) * inv);
+            for (int j = 0; j < 8; ++j)
+              oh[j] = __floats2half2_rn(__uint_as_float(r[16 * i + 2 * j]) * inv,
+                                        __uint_as_float(r[16 * i + 2 * j + 1]) * inv);
+          } else {
+            __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(o);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              ob[j] = __floats2bfloat162_rn(__uint_as_float(r[16 * i + 2 * j]) * inv,
+                                            __uint_as_float(r[16 * i + 2 * j + 1]) * inv);
+          }
           stg_v8(out0 + p * cout + c0 + hb + 16 * i, o[0], o[1]);
         }
       }
@@ -2319,12 +2328,11 @@ __global__ void __launch_bounds__(128) attn_prep_kernel(__nv_bfloat16* __restric
   if (live) {
     norm_row(v + base, f);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {       // normalised v in place (the attention kernel's B)
+    for (int i = 0; i < 8; ++i) {       // normalised v in place, f16 (the attention kernel's B)
       uint4 u;
-      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&u);
+      __half2* o = reinterpret_cast<__half2*>(&u);
 #pragma unroll
-      for (int j2 = 0; j2 < 4; ++j2)
-        o[j2] = __floats2bfloat162_rn(f[8 * i + 2 * j2], f[8 * i + 2 * j2 + 1]);
+      for (int j2 = 0; j2 < 4; ++j2) o[j2] = __floats2half2_rn(f[8 * i + 2 * j2], f[8 * i + 2 * j2 + 1]);
       reinterpret_cast<uint4*>(v + base)[i] = u;
     }
   }
@@ -2380,10 +2388,10 @@ __device__ __forceinline__ float ex2_poly(float x) {
 struct AttnSmem {
   static constexpr int Q0 = 0;                       // 2 x 16 KB [128 q][64 d]
   static constexpr int K0 = 2 * 16384;               // 2 x 16 KB [128 keys][64 d]
-  static constexpr int V0 = K0 + 2 * 16384;          // 2 x 16 KB [128 keys][64 d] (MN-major B)
-  static constexpr int P0 = V0 + 2 * 16384;          // 2 x 32 KB [2 chunks][128 q][64 keys]
-  static constexpr int L = P0 + 2 * 32768;           // [4][128] floats: partial row sums
-  static constexpr int BARS = L + 2048;              // barriers
+  static constexpr int V0 = K0 + 2 * 16384;          // 2 x 16 KB [128 keys][64 d] f16 (MN-major B)
+  static constexpr int ONES = V0 + 2 * 16384;        // 16 KB of f16 ones: B columns 64..127
+  static constexpr int P0 = ONES + 16384;            // 2 x 32 KB [2 chunks][128 q][64 keys] f16
+  static constexpr int BARS = P0 + 2 * 32768;        // barriers
   static constexpr int BYTES = BARS + 256;
 };
 
@@ -2400,7 +2408,6 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + AttnSmem::BARS);
-  float* s_l = reinterpret_cast<float*>(sm + AttnSmem::L);
   uint64_t* qfull = bars;            // [2]
   uint64_t* qempty = bars + 2;       // [2]
   uint64_t* kfull = bars + 4;        // [2]
@@ -2455,7 +2462,14 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;        // S buffers at cols 0 / 128, O buffers at 256 / 320
+  const uint32_t tmem = *tmem_slot;        // S buffers at cols 0 / 128, O buffers at 256 / 384
+  // the ones block: PV with N = 128 puts sum_k P[q][k] (the softmax denominator,
+  // accumulated in f32 by the tensor core) in O columns 64..127
+  for (int i = threadIdx.x; i < 16384 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(sm + AttnSmem::ONES)[i] =
+        make_uint4(0x3C003C00u, 0x3C003C00u, 0x3C003C00u, 0x3C003C00u);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -2482,7 +2496,9 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     constexpr uint32_t idesc_s = idesc_bf16(128, 128);
-    constexpr uint32_t idesc_o = idesc_bf16(128, 64) | (1u << 16);   // B (V) MN-major
+    // f16 A (P) and B (V, MN-major), f32 accumulate, N = 64 dims + 64 ones
+    constexpr uint32_t idesc_o = (1u << 4) | (1u << 16) | ((uint32_t)(128 >> 3) << 17) |
+                                 ((uint32_t)(128 >> 4) << 24);
     auto issue_s = [&](int t, int it, int j) {
       const int qb = it & 1;
       const int s = t & 1, ph = (t >> 1) & 1;
@@ -2518,10 +2534,13 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
               smem_desc_sw128(smem_u32(sm + AttnSmem::P0 + ps * 32768 + ch * 16384));
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            // V tile [128 keys][64 dims] as an MN-major B: keys 64ch + 16kk .. +16
-            const uint64_t vdesc = smem_desc_sw128_mn(
-                smem_u32(sm + AttnSmem::V0 + ps * 16384 + (ch * 64 + kk * 16) * 128));
-            tc_mma(tmem + 256 + ob * 64, pdesc + 2 * kk, vdesc, idesc_o, (j | ch | kk) ? 1u : 0u);
+            // V tile [128 keys][64 dims] as an MN-major B: keys 64ch + 16kk .. +16;
+            // the second 64-column MN block (LBO) is the ones block at the same rows
+            const uint32_t vaddr = smem_u32(sm + AttnSmem::V0 + ps * 16384 + (ch * 64 + kk * 16) * 128);
+            const uint32_t lbo = (uint32_t)(AttnSmem::ONES - (AttnSmem::V0 + ps * 16384));
+            const uint64_t vdesc = (smem_desc_sw128_mn(vaddr) & ~(0x3FFFull << 16)) |
+                                   ((uint64_t)((lbo >> 4) & 0x3FFF) << 16);
+            tc_mma(tmem + 256 + ob * 128, pdesc + 2 * kk, vdesc, idesc_o, (j | ch | kk) ? 1u : 0u);
           }
         }
         tc_commit(&pempty[ps]);
@@ -2547,8 +2566,6 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
     const int grp = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;                      // query row == TMEM lane
     const uint32_t lanebase = (uint32_t)(quarter * 32) << 16;
-    constexpr uint32_t BAR_N = 128 * ATT_NG;
-    float l = 0.f;
     int it = 0, j = 0;
     for (int t = 0; t < T; ++t) {
       const int s = t & 1, ph = (t >> 1) & 1;
@@ -2565,15 +2582,10 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
         for (int kk = 0; kk < KG; ++kk)
           if (kk >= kvalid) r[kk] = __float_as_uint(-INFINITY);
       }
-      // (q carries 1/8 * log2 e, so S is already in ex2 units.  r01: routing
-      // half of these through ex2_poly on the FMA pipe measured slower)
-      float p[KG];
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk) p[kk] = ex2_approx(__uint_as_float(r[kk]));
-      float l4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk) l4[kk & 3] += p[kk];
-      l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+      // (q carries 1/8 * log2 e, so S is already in ex2 units; P = 2^s computed in
+      // f32 (ex2.approx.f16x2 is two MUFU ops on sm_100 anyway and would round the
+      // argument to f16), stored f16; the row sums come from the ones block of the
+      // PV MMA.  r01: half of the exps as an FMA-pipe polynomial measured slower)
       mbar_wait(&pempty[s], ph ^ 1);
       // keys [32g, 32g+32): 64-key chunk g/2, 16-byte columns 4*(g%2) .. +3
       uint8_t* pbase = sm + AttnSmem::P0 + s * 32768 + (grp * KG / 64) * 16384;
@@ -2581,33 +2593,29 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
 #pragma unroll
       for (int c8 = 0; c8 < KG / 8; ++c8) {
         uint4 u;
-        __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&u);
+        __half2* h2 = reinterpret_cast<__half2*>(&u);
 #pragma unroll
         for (int q2 = 0; q2 < 4; ++q2)
-          o[q2] = __floats2bfloat162_rn(p[c8 * 8 + 2 * q2], p[c8 * 8 + 2 * q2 + 1]);
+          h2[q2] = __floats2half2_rn(ex2_approx(__uint_as_float(r[c8 * 8 + 2 * q2])),
+                                     ex2_approx(__uint_as_float(r[c8 * 8 + 2 * q2 + 1])));
         *reinterpret_cast<uint4*>(pbase + row * 128 + (((c0 + c8) ^ (row & 7)) * 16)) = u;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&pfull[s]);
       if (j == ktiles - 1) {
-        // item done: the groups' partial row sums, then O / l
+        // item done: O / l (l = O column 64, the ones block)
         int img, hd, qt;
         item_of(it, img, hd, qt);
         const int ob = it & 1;
-        s_l[grp * 128 + row] = l;
-        named_bar_sync(1, BAR_N);
-        float lt = 0.f;
-#pragma unroll
-        for (int g2 = 0; g2 < ATT_NG; ++g2) lt += s_l[g2 * 128 + row];
-        named_bar_sync(1, BAR_N);                             // s_l read before it is reused
-        const float inv_l = 1.f / lt;
-        l = 0.f;
         mbar_wait(&ofull[ob], (it >> 1) & 1);
         tc_fence_after();
         uint32_t ro[DG];
-        tmem_ld16(tmem + lanebase + 256 + ob * 64 + grp * DG, reinterpret_cast<float*>(ro));
+        float lrow[16];
+        tmem_ld16(tmem + lanebase + 256 + ob * 128 + grp * DG, reinterpret_cast<float*>(ro));
+        tmem_ld16(tmem + lanebase + 256 + ob * 128 + 64, lrow);
         tc_fence_before();
         mbar_arrive(&oempty[ob]);
+        const float inv_l = 1.f / lrow[0];
         if (qt * 128 + row < hw) {
           __nv_bfloat16* dst = y + ((int64_t)img * hw + qt * 128 + row) * c + hd * 64 + grp * DG;
           uint4 u[2];
@@ -3114,7 +3122,8 @@ static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   a->up_sa = (p->up_in >> 1) & 1;
   a->pool0 = reinterpret_cast<__nv_bfloat16*>(p->pool0);
   a->pool1 = reinterpret_cast<__nv_bfloat16*>(p->pool1);
-  a->head_norm = p->head_norm != 0;
+  a->head_norm = p->head_norm;
+  IG_REQUIRE(p->head_norm >= 0 && p->head_norm <= 2, "conv: head_norm must be 0, 1 or 2");
   a->head_scale = p->head_scale;
   IG_REQUIRE(!p->head_norm || (p->cout % 128 == 0 && !p->res && !p->out1 && !p->up2 &&
                                !p->pool0 && !(p->gutter & 1)),

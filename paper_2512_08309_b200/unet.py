@@ -365,7 +365,7 @@ class UNetDevice:
             p = ConvParams(n, h, w, c, 0, c, 1, x.data_ptr(), None,
                            wq.data_ptr() + j * c * c * 2, None, None, None, 0.0, 1.0, 1.0,
                            dst.data_ptr(), None)
-            p.head_norm = 1
+            p.head_norm = 2 if j == 2 else 1          # v in f16 (the PV MMA's operand)
             p.head_scale = Q_SCALE if j == 0 else 1.0
             conv_launch(p)
         y = torch.empty_like(x)
