@@ -59,7 +59,6 @@ def layer_ops(cfg, win):
             nm = op[1]
             for j in "qkv":
                 seq.append(("conv", f"{nm}.{j}", h, c, c, 1, 1, 0))
-            seq.append(("attn_prep", nm + ".prep", h, c, 0, 0, 0, 0))
             seq.append(("attn", nm + ".attn", h, c, 0, 0, 0, 0))
             seq.append(("conv", nm + ".proj", h, c, c, 1, 2, 1))
         elif op[0] == "down":
