@@ -106,6 +106,25 @@ def upload(arr: np.ndarray) -> torch.Tensor:
     return _staging.upload(a)
 
 
+_reserved = 0
+
+
+def reserve(nbytes: int):
+    """Grow the CUDA caching allocator to `nbytes` once (allocate + free): a
+    bounded window cache then fills from cached segments instead of calling
+    cudaMalloc in the middle of a query (a new segment stalled a cfg4 query by
+    ~45 ms, tools/cfg4_tail.py).  The memory stays with torch's allocator."""
+    global _reserved
+    device()
+    free, _ = torch.cuda.mem_get_info()
+    nbytes = min(int(nbytes), int(0.8 * (free + torch.cuda.memory_reserved())))
+    if nbytes <= _reserved:
+        return
+    t = torch.empty(nbytes, dtype=torch.uint8, device=device())
+    del t
+    _reserved = nbytes
+
+
 def upload_i64(values) -> torch.Tensor:
     return upload(np.asarray(values, dtype=np.int64))
 
