@@ -148,6 +148,108 @@ __global__ void __launch_bounds__(256) phi_analytic_kernel(int kind, int radius,
   }
 }
 
+// Tiled form of phi_analytic_kernel: one CTA = one band of `band` rows of one
+// (window, channel) plane, full window width.  The clamped source rows
+// (band + 2r) are staged in SMEM once; the blur is evaluated separably with the
+// reference's own rounding sequence (transforms.py:29-51 sums axis -2 first,
+// and each column sum is divided by k before the horizontal sum), so
+//   D[y][x'] = rdiv(sum_dy S[y+dy][x'], k)     (once per pixel, not per tap)
+//   blur     = rdiv(sum_dx D[y][clamp(x+dx)], k)
+// is the same operation sequence per output as the direct form above:
+// bit-identical, with 2(2r+1) adds + 2 divisions per pixel instead of
+// (2r+1)^2 + 2r+2 and 32-bit indexing throughout.
+template <typename T>
+__global__ void __launch_bounds__(256) phi_tile_kernel(int kind, int radius, T a_coef, T b_coef,
+                                                       int lam_zero, SrcView src,
+                                                       const int64_t* __restrict__ wxy, int win,
+                                                       int band, CondView cond,
+                                                       T* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char phi_smem[];
+  const bool blur_on = !(kind == IG_PHI_IDENTITY || lam_zero) && radius > 0;
+  const int r = blur_on ? radius : 0;
+  const int C = src.channels;
+  const int k = blockIdx.y / C, c = blockIdx.y - k * C;
+  const int y0 = blockIdx.x * band;
+  const int rows = min(band, win - y0);
+  const int srows = rows + 2 * r;
+  T* S = reinterpret_cast<T*>(phi_smem);                  // (band + 2r) x win, clamped rows
+  T* D = S + (size_t)(band + 2 * r) * win;                // band x win column sums / k
+  const T kdiv = (T)(2 * r + 1);
+  const T* base;
+  int64_t rs;
+  if (src.batched) {
+    base = reinterpret_cast<const T*>(src.base) + ((int64_t)k * C + c) * win * win;
+    rs = win;
+  } else {
+    base = reinterpret_cast<const T*>(src.base) +
+           ((int64_t)c * src.h + (wxy[2 * k + 1] - src.y0)) * src.w + (wxy[2 * k] - src.x0);
+    rs = src.w;
+  }
+  {
+    // 8 independent loads in flight per thread before the SMEM stores
+    const int total = srows * win;
+    for (int e0 = threadIdx.x; e0 < total; e0 += 8 * 256) {
+      T v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * 256;
+        if (e < total) {
+          const int i = e / win, x = e - i * win;
+          v[u] = base[(int64_t)min(max(y0 - r + i, 0), win - 1) * rs + x];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (e0 + u * 256 < total) S[e0 + u * 256] = v[u];
+    }
+  }
+  __syncthreads();
+  if (blur_on) {
+    int yl = threadIdx.x / win, x = threadIdx.x - (threadIdx.x / win) * win;
+    for (; yl < rows;) {
+      T vacc = (T)0;
+      for (int dy = 0; dy <= 2 * r; ++dy) vacc = radd(vacc, S[(yl + dy) * win + x]);
+      D[yl * win + x] = rdiv(vacc, kdiv);
+      x += 256;
+      while (x >= win) { x -= win; ++yl; }
+    }
+    __syncthreads();
+  }
+  int slow = 0;
+  T* obase = out + (((int64_t)k * C + c) * win + y0) * win;
+  int yl = threadIdx.x / win, x = threadIdx.x - (threadIdx.x / win) * win;
+  for (; yl < rows;) {
+    const T xv = S[(yl + r) * win + x];
+    T res;
+    if (kind == IG_PHI_IDENTITY || lam_zero) {
+      res = xv;
+    } else {
+      T blur = xv;
+      if (r > 0) {
+        T hacc = (T)0;
+        for (int dx = -r; dx <= r; ++dx) hacc = radd(hacc, D[yl * win + min(max(x + dx, 0), win - 1)]);
+        blur = rdiv(hacc, kdiv);
+      }
+      res = radd(rmul(a_coef, xv), rmul(b_coef, blur));
+    }
+    if (kind == IG_PHI_COND_AFFINE && cond.parent != nullptr) {
+      const int64_t X = wxy[2 * k] + x, Y = wxy[2 * k + 1] + y0 + yl;
+      const int64_t cx = floordiv(X, cond.scale) - cond.x0;
+      const int64_t cy = floordiv(Y, cond.scale) - cond.y0;
+      const T* par = reinterpret_cast<const T*>(cond.parent);
+      const int64_t plane = (int64_t)cond.w * cond.h;
+      T m = (T)1;
+      if (cond.mask_channel >= 0) m = par[cond.mask_channel * plane + cy * cond.w + cx];
+      T target = par[cy * cond.w + cx];
+      if (cond.fill && m < (T)1) target = (T)noise_value(cond.prefix, X, Y, 0u, &slow);
+      res = radd(res, rmul(m, rsub(target, res)));
+    }
+    obase[yl * win + x] = res;
+    x += 256;
+    while (x >= win) { x -= win; ++yl; }
+  }
+}
+
 // =====================================================================
 // K5 blend  (store.py:428-436 _accumulate, sampler.py:151-154, store.py:549-554)
 // Gather form: each output pixel walks its covering windows in canonical
@@ -161,37 +263,93 @@ __global__ void __launch_bounds__(256) blend_kernel(const T* const* __restrict__
                                                     const T* __restrict__ weight, int64_t rx0,
                                                     int64_t ry0, int rw, int rh, int divide,
                                                     T* __restrict__ out) {
+  // one output row per blockIdx.y, 256 columns per thread-row pass: the window
+  // rows covering the row (j range, local y) are per-block constants and the
+  // per-pixel window columns come from 32-bit quotient/remainder arithmetic
+  // (no 64-bit division per pixel).  Same per-pixel accumulation order as the
+  // reference's scatter-add: windows in canonical (j asc, i asc) order from +0.
   const int64_t npix = (int64_t)rw * rh;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const int py = (int)(p / rw), px = (int)(p - (int64_t)py * rw);
-    const int64_t X = rx0 + px, Y = ry0 + py;
-    int64_t ilo = ceildiv(X - ox - win + 1, stride), ihi = floordiv(X - ox, stride);
-    int64_t jlo = ceildiv(Y - oy - win + 1, stride), jhi = floordiv(Y - oy, stride);
-    ilo = ilo > i0 ? ilo : i0;
-    jlo = jlo > j0 ? jlo : j0;
-    ihi = ihi < i0 + ni - 1 ? ihi : i0 + ni - 1;
-    jhi = jhi < j0 + nj - 1 ? jhi : j0 + nj - 1;
-    const int out_planes = mode == 1 ? channels + 1 : channels;
-    if (mode == 1) {
-      T wsum = (T)0;
-      for (int64_t j = jlo; j <= jhi; ++j)
-        for (int64_t i = ilo; i <= ihi; ++i) {
-          const T* d = win_data[(j - j0) * ni + (i - i0)];
+  for (int py = blockIdx.y; py < rh; py += gridDim.y) {
+  const int64_t Y = ry0 + py;
+  int64_t jlo = ceildiv(Y - oy - win + 1, stride), jhi = floordiv(Y - oy, stride);
+  jlo = jlo > j0 ? jlo : j0;
+  jhi = jhi < j0 + nj - 1 ? jhi : j0 + nj - 1;
+  const int nrows = jhi >= jlo ? (int)(jhi - jlo + 1) : 0;
+  // column origin of this block's first pixel relative to the layout
+  const int px_begin = blockIdx.x * 1024;
+  const int64_t X0 = rx0 + px_begin;
+  const int64_t base = floordiv(X0 - ox, stride);             // window column index of X0
+  const int r0 = (int)((X0 - ox) - base * stride);           // 0 .. stride-1
+  const int out_planes = mode == 1 ? channels + 1 : channels;
+  for (int px = px_begin + threadIdx.x; px < rw && px < px_begin + 1024; px += blockDim.x) {
+    const int t = r0 + (px - px_begin);
+    const int q = t / stride, rr = t - q * stride;            // X - ox = (base + q) * stride + rr
+    // covering windows i = base + q - m with lx = rr + m * stride < win, m >= 0
+    int mmax = (win - 1 - rr) / stride;                       // largest m with lx < win
+    const int64_t ihi_raw = base + q;
+    int64_t ilo = ihi_raw - mmax, ihi = ihi_raw;
+    if (ilo < i0) ilo = i0;
+    if (ihi > i0 + ni - 1) ihi = i0 + ni - 1;
+    const int64_t p = (int64_t)py * rw + px;
+    // window columns relative to the table: ii = i - i0 in [iilo, iihi]
+    const int iilo = (int)(ilo - i0), iihi = (int)(ihi - i0), ihr = (int)(ihi_raw - i0);
+    if (mode == 1 && channels <= 4) {
+      // one pass: the weight sum and every channel's weighted sum, each in the
+      // canonical (j asc, i asc) order (the chains are independent)
+      T wsum = (T)0, acc[4] = {(T)0, (T)0, (T)0, (T)0};
+      for (int jj = 0; jj < nrows; ++jj) {
+        const int64_t j = jlo + jj;
+        const int ly = (int)(Y - (j * stride + oy));
+        const T* wrow = weight + (int64_t)ly * win;
+        const T* const* dptr = win_data + (j - j0) * ni;
+        for (int ii = iilo; ii <= iihi; ++ii) {
+          const T* d = dptr[ii];
           if (!d) continue;
-          const int lx = (int)(X - (i * stride + ox)), ly = (int)(Y - (j * stride + oy));
-          wsum = radd(wsum, weight[ly * win + lx]);
+          const int lx = rr + (ihr - ii) * stride;
+          const T wv = wrow[lx];
+          wsum = radd(wsum, wv);
+          const T* dp = d + (int64_t)ly * win + lx;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (c < channels) acc[c] = radd(acc[c], rmul(wv, dp[(int64_t)c * win * win]));
         }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c >= channels) break;
+        if (divide)
+          out[(int64_t)c * npix + p] = wsum > (T)0 ? rdiv(acc[c], wsum) : (T)0;
+        else
+          out[(int64_t)c * npix + p] = acc[c];
+      }
+      if (!divide) out[(int64_t)channels * npix + p] = wsum;
+    } else if (mode == 1) {
+      T wsum = (T)0;
+      for (int jj = 0; jj < nrows; ++jj) {
+        const int64_t j = jlo + jj;
+        const int ly = (int)(Y - (j * stride + oy));
+        const T* wrow = weight + (int64_t)ly * win;
+        const T* const* dptr = win_data + (j - j0) * ni;
+        for (int64_t i = ilo; i <= ihi; ++i) {
+          if (!dptr[i - i0]) continue;
+          const int lx = rr + (int)(ihi_raw - i) * stride;
+          wsum = radd(wsum, wrow[lx]);
+        }
+      }
       for (int c = 0; c < channels; ++c) {
         T acc = (T)0;
-        for (int64_t j = jlo; j <= jhi; ++j)
+        for (int jj = 0; jj < nrows; ++jj) {
+          const int64_t j = jlo + jj;
+          const int ly = (int)(Y - (j * stride + oy));
+          const T* wrow = weight + (int64_t)ly * win;
+          const T* const* dptr = win_data + (j - j0) * ni;
           for (int64_t i = ilo; i <= ihi; ++i) {
-            const T* d = win_data[(j - j0) * ni + (i - i0)];
+            const T* d = dptr[i - i0];
             if (!d) continue;
-            const int lx = (int)(X - (i * stride + ox)), ly = (int)(Y - (j * stride + oy));
-            const int64_t o = ((int64_t)c * win + ly) * win + lx;
-            acc = radd(acc, rmul(weight[ly * win + lx], d[o]));
+            const int lx = rr + (int)(ihi_raw - i) * stride;
+            acc = radd(acc, rmul(wrow[lx], d[((int64_t)c * win + ly) * win + lx]));
           }
+        }
         if (divide)
           out[(int64_t)c * npix + p] = wsum > (T)0 ? rdiv(acc, wsum) : (T)0;
         else
@@ -201,17 +359,150 @@ __global__ void __launch_bounds__(256) blend_kernel(const T* const* __restrict__
     } else {
       for (int c = 0; c < out_planes; ++c) {
         T acc = (T)0;
-        for (int64_t j = jlo; j <= jhi; ++j)
+        for (int jj = 0; jj < nrows; ++jj) {
+          const int64_t j = jlo + jj;
+          const int ly = (int)(Y - (j * stride + oy));
+          const T* const* dptr = win_data + (j - j0) * ni;
           for (int64_t i = ilo; i <= ihi; ++i) {
-            const T* d = win_data[(j - j0) * ni + (i - i0)];
+            const T* d = dptr[i - i0];
             if (!d) continue;
-            const int lx = (int)(X - (i * stride + ox)), ly = (int)(Y - (j * stride + oy));
+            const int lx = rr + (int)(ihi_raw - i) * stride;
             acc = radd(acc, d[((int64_t)c * win + ly) * win + lx]);
           }
+        }
         out[(int64_t)c * npix + p] = acc;
       }
     }
   }
+  }   // rows
+}
+
+// Fast path for window == 2 * stride (every sampler layout): the pixels of
+// one stride x stride CELL of the layout lattice are covered by the same four
+// windows, (cj-1, ci-1), (cj-1, ci), (cj, ci-1), (cj, ci) in canonical order,
+// at fixed local offsets.  One CTA = P passes of (256 / (stride/4)) rows of one
+// cell; a thread handles 4 consecutive pixels per pass with 16-byte loads.
+// Every load of every pass is issued before the first add (absent windows and
+// out-of-region passes load a valid dummy address and are masked afterwards),
+// so a warp keeps P * 4 * (1 + C) 16-byte requests in flight -- the kernel is
+// latency-bound otherwise (ncu: long-scoreboard stalls, 2.6 TB/s).  Same
+// per-pixel sums in the same order as blend_kernel (absent windows skipped).
+template <typename T>
+__device__ __forceinline__ void ld4(const T* p, T (&v)[4]) {
+  if (sizeof(T) == 4) {
+    const float4 f = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  } else {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+}
+
+template <typename T, int C>
+constexpr int blend_cells_passes() { return sizeof(T) * C <= 8 ? 2 : 1; }
+
+template <typename T, int C>
+__global__ void __launch_bounds__(256) blend_cells_kernel(
+    const T* const* __restrict__ win_data, int64_t i0, int64_t j0, int ni, int nj, int win,
+    int stride, int64_t ox, int64_t oy, const T* __restrict__ weight, int64_t rx0,
+    int64_t ry0, int rw, int rh, int divide, int64_t ci_lo, int64_t cj_lo, int ncx,
+    T* __restrict__ out) {
+  constexpr int P = blend_cells_passes<T, C>();
+  __shared__ const T* s_wp[4];
+  const int64_t npix = (int64_t)rw * rh;
+  const int q4 = stride / 4;                          // quads per cell row
+  const int rows_per_pass = 256 / q4;                 // cell rows per pass of the CTA
+  const int rows_per_cta = P * rows_per_pass;
+  const int blocks_per_cell = stride / rows_per_cta;
+  const int cell = blockIdx.x / blocks_per_cell;
+  const int rb = blockIdx.x - cell * blocks_per_cell;
+  const int64_t ci = ci_lo + cell % ncx, cj = cj_lo + cell / ncx;
+  if (threadIdx.x < 4) {        // the 4 candidate windows (canonical order), once per CTA
+    const int64_t j = cj - 1 + (threadIdx.x >> 1), i = ci - 1 + (threadIdx.x & 1);
+    const bool in = j >= j0 && j < j0 + nj && i >= i0 && i < i0 + ni;
+    s_wp[threadIdx.x] = in ? win_data[(j - j0) * ni + (i - i0)] : nullptr;
+  }
+  __syncthreads();
+  const T* wp[4] = {s_wp[0], s_wp[1], s_wp[2], s_wp[3]};
+  const int v = (threadIdx.x % q4) * 4;                        // first column of the quad
+  const int plane = win * win;
+  T wv[P][4][4], dv[P][4][C][4];
+  int py[P], px[P];
+  bool ok[P];
+#pragma unroll
+  for (int pass = 0; pass < P; ++pass) {
+    const int u = rb * rows_per_cta + pass * rows_per_pass + threadIdx.x / q4;   // cell row
+    py[pass] = (int)(cj * stride + oy + u - ry0);
+    px[pass] = (int)(ci * stride + ox + v - rx0);
+    ok[pass] = !(py[pass] < 0 || py[pass] >= rh || px[pass] + 3 < 0 || px[pass] >= rw);
+#pragma unroll
+    for (int w4 = 0; w4 < 4; ++w4) {
+      const int lofs = (u + (1 - (w4 >> 1)) * stride) * win + v + (1 - (w4 & 1)) * stride;
+      ld4(weight + lofs, wv[pass][w4]);
+      const bool use = ok[pass] && wp[w4] != nullptr;
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        ld4(use ? wp[w4] + (int64_t)c * plane + lofs : weight + lofs, dv[pass][w4][c]);
+    }
+  }
+#pragma unroll
+  for (int pass = 0; pass < P; ++pass) {
+    if (!ok[pass]) continue;
+    T wsum[4] = {(T)0, (T)0, (T)0, (T)0};
+    T acc[C][4];
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[c][e] = (T)0;
+#pragma unroll
+    for (int w4 = 0; w4 < 4; ++w4) {
+      if (!wp[w4]) continue;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) wsum[e] = radd(wsum[e], wv[pass][w4][e]);
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          acc[c][e] = radd(acc[c][e], rmul(wv[pass][w4][e], dv[pass][w4][c][e]));
+    }
+    const bool full = px[pass] >= 0 && px[pass] + 3 < rw;
+    const int64_t p = (int64_t)py[pass] * rw + px[pass];
+#pragma unroll
+    for (int c = 0; c <= C; ++c) {
+      if (c == C && divide) break;
+      T o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (c == C) o[e] = wsum[e];
+        else if (divide) o[e] = wsum[e] > (T)0 ? rdiv(acc[c < C ? c : 0][e], wsum[e]) : (T)0;
+        else o[e] = acc[c < C ? c : 0][e];
+      }
+      T* dst = out + (int64_t)c * npix + p;
+      if (full && sizeof(T) == 4 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        *reinterpret_cast<float4*>(dst) = make_float4((float)o[0], (float)o[1], (float)o[2],
+                                                      (float)o[3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (px[pass] + e >= 0 && px[pass] + e < rw) dst[e] = o[e];
+      }
+    }
+  }
+}
+
+template <typename T, int C>
+static void launch_blend_cells(const void* const* win_data, int64_t i0, int64_t j0, int ni,
+                               int nj, int window, int stride, int64_t ox, int64_t oy,
+                               const void* weight, int64_t rx0, int64_t ry0, int rw, int rh,
+                               int divide, int64_t ci_lo, int64_t cj_lo, int ncx, int64_t cells,
+                               void* out, cudaStream_t st) {
+  const int rows_per_cta = blend_cells_passes<T, C>() * (256 / (stride / 4));
+  const int64_t ctas = cells * (stride / rows_per_cta);
+  blend_cells_kernel<T, C><<<(unsigned)ctas, 256, 0, st>>>(
+      (const T* const*)win_data, i0, j0, ni, nj, window, stride, ox, oy, (const T*)weight, rx0,
+      ry0, rw, rh, divide, ci_lo, cj_lo, ncx, (T*)out);
+  note_launch();
 }
 
 template <typename T>
@@ -530,9 +821,29 @@ int ig_phi_analytic(int32_t kind, int32_t radius, double lam, int32_t dtype, con
   SrcView s{src, src_batched, src_x0, src_y0, src_w, src_h, channels};
   CondView c{cond_parent, cond_x0, cond_y0, cond_w, cond_h, cond_c, cond_scale < 1 ? 1 : cond_scale,
              cond_mask_channel, cond_fill, noise_prefix(cond_seed, 101u)};
+  const int lam_zero = (lam == 0.0);
+  // tiled path: bands of up to 16 rows whose staged rows fit 48 KB of SMEM
+  {
+    const int r = (kind == IG_PHI_IDENTITY || lam_zero) ? 0 : radius;
+    const size_t es = dtype == IG_DTYPE_F32 ? 4 : 8;
+    int band = 16;
+    while (band > 1 && (size_t)(2 * band + 2 * r) * window * es > 48 * 1024) band /= 2;
+    const size_t smem = (size_t)(2 * band + 2 * r) * window * es;
+    if (smem <= 48 * 1024 && (int64_t)n * channels <= 65535) {
+      const dim3 grid((unsigned)((window + band - 1) / band), (unsigned)(n * channels));
+      if (dtype == IG_DTYPE_F32)
+        { phi_tile_kernel<float><<<grid, 256, smem, as_stream(cuda_stream)>>>(
+            kind, radius, (float)(1.0 - lam), (float)lam, lam_zero, s, wxy, window, band, c,
+            (float*)out); note_launch(); }
+      else
+        { phi_tile_kernel<double><<<grid, 256, smem, as_stream(cuda_stream)>>>(
+            kind, radius, 1.0 - lam, lam, lam_zero, s, wxy, window, band, c, (double*)out);
+          note_launch(); }
+      return cuda_check("ig_phi_analytic");
+    }
+  }
   const int64_t total = (int64_t)n * channels * window * window;
   const int grid = grid_for(total, 256);
-  const int lam_zero = (lam == 0.0);
   if (dtype == IG_DTYPE_F32)
     { phi_analytic_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
         kind, radius, (float)(1.0 - lam), (float)lam, lam_zero, s, wxy, n, window, c,
@@ -552,7 +863,43 @@ int ig_blend(const void* const* win_data, int64_t i0, int64_t j0, int32_t ni, in
   IG_REQUIRE(mode == 0 || mode == 1, "blend: bad mode");
   IG_REQUIRE(!(divide && mode == 0), "blend: divide needs weighted mode");
   IG_REQUIRE(mode == 0 || weight != nullptr, "blend: weighted mode needs a weight table");
-  const int grid = grid_for((int64_t)rw * rh, 256);
+  // cell fast path: window == 2 * stride, weighted, <= 4 channels, stride % 4 == 0,
+  // 16-byte aligned window rows; whole passes of (256 / (stride/4)) rows per cell
+  // (2 passes when T * C <= 8 bytes)
+  if (mode == 1 && window == 2 * stride && channels >= 1 && channels <= 4 && stride % 4 == 0 &&
+      256 % (stride / 4) == 0) {
+    const int es = dtype == IG_DTYPE_F32 ? 4 : 8;
+    const int passes = es * channels <= 8 ? 2 : 1;
+    const int64_t ci_lo = floordiv(rx0 - off_x, stride), ci_hi = floordiv(rx0 + rw - 1 - off_x, stride);
+    const int64_t cj_lo = floordiv(ry0 - off_y, stride), cj_hi = floordiv(ry0 + rh - 1 - off_y, stride);
+    const int ncx = (int)(ci_hi - ci_lo + 1), ncy = (int)(cj_hi - cj_lo + 1);
+    const int rows_per_cta = passes * (256 / (stride / 4));
+    const int64_t cells = (int64_t)ncx * ncy;
+    if (stride % rows_per_cta == 0 && cells * (stride / rows_per_cta) < (1ll << 31)) {
+      cudaStream_t st = as_stream(cuda_stream);
+#define IG_BLEND_CELLS(T, C)                                                                   \
+  launch_blend_cells<T, C>(win_data, i0, j0, ni, nj, window, stride, off_x, off_y, weight, rx0, \
+                           ry0, rw, rh, divide, ci_lo, cj_lo, ncx, cells, out, st)
+      if (dtype == IG_DTYPE_F32) {
+        switch (channels) {
+          case 1: IG_BLEND_CELLS(float, 1); break;
+          case 2: IG_BLEND_CELLS(float, 2); break;
+          case 3: IG_BLEND_CELLS(float, 3); break;
+          default: IG_BLEND_CELLS(float, 4); break;
+        }
+      } else {
+        switch (channels) {
+          case 1: IG_BLEND_CELLS(double, 1); break;
+          case 2: IG_BLEND_CELLS(double, 2); break;
+          case 3: IG_BLEND_CELLS(double, 3); break;
+          default: IG_BLEND_CELLS(double, 4); break;
+        }
+      }
+#undef IG_BLEND_CELLS
+      return cuda_check("ig_blend");
+    }
+  }
+  const dim3 grid((unsigned)((rw + 1023) / 1024), (unsigned)(rh < 65535 ? rh : 65535));
   if (dtype == IG_DTYPE_F32)
     { blend_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
         (const float* const*)win_data, i0, j0, ni, nj, window, stride, off_x, off_y, channels,
