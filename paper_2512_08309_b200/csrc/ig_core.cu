@@ -158,15 +158,19 @@ __global__ void __launch_bounds__(256) phi_analytic_kernel(int kind, int radius,
 // is the same operation sequence per output as the direct form above:
 // bit-identical, with 2(2r+1) adds + 2 divisions per pixel instead of
 // (2r+1)^2 + 2r+2 and 32-bit indexing throughout.
-template <typename T>
+// Threads own fixed columns (TX = min(win, 256) lanes across, TY row groups)
+// and walk rows, so the clamped neighbour columns are computed once per
+// column, not per pixel.  R >= 0: the effective radius as a template constant
+// (the sampler's radius 0 / 1 cases); R = -1: runtime radius.
+template <typename T, int R>
 __global__ void __launch_bounds__(256) phi_tile_kernel(int kind, int radius, T a_coef, T b_coef,
                                                        int lam_zero, SrcView src,
                                                        const int64_t* __restrict__ wxy, int win,
                                                        int band, CondView cond,
                                                        T* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char phi_smem[];
-  const bool blur_on = !(kind == IG_PHI_IDENTITY || lam_zero) && radius > 0;
-  const int r = blur_on ? radius : 0;
+  const bool plain = kind == IG_PHI_IDENTITY || lam_zero;
+  const int r = R >= 0 ? R : (plain ? 0 : radius);     // host passes R = effective radius
   const int C = src.channels;
   const int k = blockIdx.y / C, c = blockIdx.y - k * C;
   const int y0 = blockIdx.x * band;
@@ -175,6 +179,9 @@ __global__ void __launch_bounds__(256) phi_tile_kernel(int kind, int radius, T a
   T* S = reinterpret_cast<T*>(phi_smem);                  // (band + 2r) x win, clamped rows
   T* D = S + (size_t)(band + 2 * r) * win;                // band x win column sums / k
   const T kdiv = (T)(2 * r + 1);
+  const int TX = win < 256 ? win : 256, TY = 256 / TX;
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  const bool active = ty < TY;
   const T* base;
   int64_t rs;
   if (src.batched) {
@@ -185,68 +192,75 @@ __global__ void __launch_bounds__(256) phi_tile_kernel(int kind, int radius, T a
            ((int64_t)c * src.h + (wxy[2 * k + 1] - src.y0)) * src.w + (wxy[2 * k] - src.x0);
     rs = src.w;
   }
-  {
+  if (active) {
     // 8 independent loads in flight per thread before the SMEM stores
-    const int total = srows * win;
-    for (int e0 = threadIdx.x; e0 < total; e0 += 8 * 256) {
-      T v[8];
+    for (int x = tx; x < win; x += TX)
+      for (int i0 = ty; i0 < srows; i0 += 8 * TY) {
+        T v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = e0 + u * 256;
-        if (e < total) {
-          const int i = e / win, x = e - i * win;
-          v[u] = base[(int64_t)min(max(y0 - r + i, 0), win - 1) * rs + x];
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * TY;
+          if (i < srows) v[u] = base[(int64_t)min(max(y0 - r + i, 0), win - 1) * rs + x];
         }
-      }
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (e0 + u * 256 < total) S[e0 + u * 256] = v[u];
-    }
+        for (int u = 0; u < 8; ++u)
+          if (i0 + u * TY < srows) S[(i0 + u * TY) * win + x] = v[u];
+      }
   }
   __syncthreads();
-  if (blur_on) {
-    int yl = threadIdx.x / win, x = threadIdx.x - (threadIdx.x / win) * win;
-    for (; yl < rows;) {
-      T vacc = (T)0;
-      for (int dy = 0; dy <= 2 * r; ++dy) vacc = radd(vacc, S[(yl + dy) * win + x]);
-      D[yl * win + x] = rdiv(vacc, kdiv);
-      x += 256;
-      while (x >= win) { x -= win; ++yl; }
-    }
+  if (r > 0) {
+    if (active)
+      for (int x = tx; x < win; x += TX)
+        for (int yl = ty; yl < rows; yl += TY) {
+          T vacc = (T)0;
+          for (int dy = 0; dy <= 2 * r; ++dy) vacc = radd(vacc, S[(yl + dy) * win + x]);
+          D[yl * win + x] = rdiv(vacc, kdiv);
+        }
     __syncthreads();
   }
+  if (!active) return;
   int slow = 0;
   T* obase = out + (((int64_t)k * C + c) * win + y0) * win;
-  int yl = threadIdx.x / win, x = threadIdx.x - (threadIdx.x / win) * win;
-  for (; yl < rows;) {
-    const T xv = S[(yl + r) * win + x];
-    T res;
-    if (kind == IG_PHI_IDENTITY || lam_zero) {
-      res = xv;
-    } else {
-      T blur = xv;
-      if (r > 0) {
-        T hacc = (T)0;
-        for (int dx = -r; dx <= r; ++dx) hacc = radd(hacc, D[yl * win + min(max(x + dx, 0), win - 1)]);
-        blur = rdiv(hacc, kdiv);
+  for (int x = tx; x < win; x += TX) {
+    int xm[R > 0 ? 2 * R + 1 : 1];
+    if (R > 0) {
+#pragma unroll
+      for (int d = 0; d < (R > 0 ? 2 * R + 1 : 1); ++d) xm[d] = min(max(x + d - R, 0), win - 1);
+    }
+    for (int yl = ty; yl < rows; yl += TY) {
+      const T xv = S[(yl + r) * win + x];
+      T res;
+      if (plain) {
+        res = xv;
+      } else {
+        T blur = xv;
+        if (r > 0) {
+          T hacc = (T)0;
+          if (R > 0) {
+#pragma unroll
+            for (int d = 0; d < (R > 0 ? 2 * R + 1 : 1); ++d) hacc = radd(hacc, D[yl * win + xm[d]]);
+          } else {
+            for (int dx = -r; dx <= r; ++dx)
+              hacc = radd(hacc, D[yl * win + min(max(x + dx, 0), win - 1)]);
+          }
+          blur = rdiv(hacc, kdiv);
+        }
+        res = radd(rmul(a_coef, xv), rmul(b_coef, blur));
       }
-      res = radd(rmul(a_coef, xv), rmul(b_coef, blur));
+      if (kind == IG_PHI_COND_AFFINE && cond.parent != nullptr) {
+        const int64_t X = wxy[2 * k] + x, Y = wxy[2 * k + 1] + y0 + yl;
+        const int64_t cx = floordiv(X, cond.scale) - cond.x0;
+        const int64_t cy = floordiv(Y, cond.scale) - cond.y0;
+        const T* par = reinterpret_cast<const T*>(cond.parent);
+        const int64_t plane = (int64_t)cond.w * cond.h;
+        T m = (T)1;
+        if (cond.mask_channel >= 0) m = par[cond.mask_channel * plane + cy * cond.w + cx];
+        T target = par[cy * cond.w + cx];
+        if (cond.fill && m < (T)1) target = (T)noise_value(cond.prefix, X, Y, 0u, &slow);
+        res = radd(res, rmul(m, rsub(target, res)));
+      }
+      obase[yl * win + x] = res;
     }
-    if (kind == IG_PHI_COND_AFFINE && cond.parent != nullptr) {
-      const int64_t X = wxy[2 * k] + x, Y = wxy[2 * k + 1] + y0 + yl;
-      const int64_t cx = floordiv(X, cond.scale) - cond.x0;
-      const int64_t cy = floordiv(Y, cond.scale) - cond.y0;
-      const T* par = reinterpret_cast<const T*>(cond.parent);
-      const int64_t plane = (int64_t)cond.w * cond.h;
-      T m = (T)1;
-      if (cond.mask_channel >= 0) m = par[cond.mask_channel * plane + cy * cond.w + cx];
-      T target = par[cy * cond.w + cx];
-      if (cond.fill && m < (T)1) target = (T)noise_value(cond.prefix, X, Y, 0u, &slow);
-      res = radd(res, rmul(m, rsub(target, res)));
-    }
-    obase[yl * win + x] = res;
-    x += 256;
-    while (x >= win) { x -= win; ++yl; }
   }
 }
 
@@ -638,6 +652,138 @@ __global__ void laplacian_merge_kernel(const double* __restrict__ low,
   }
 }
 
+// Fused widen + blur3 (one box_mean radius-1 pass, or none) + block_mean for
+// the Laplacian low band (transforms.py:54-67, 89-114): one CTA = a TH x TW
+// tile of one plane (multiples of the factor), staged once in SMEM as float64
+// with a clamped 1-pixel halo.  The blur is the separable sequence of
+// box_mean_kernel (column sums / 3, then row sum / 3) and the block means the
+// sequence of block_mean_f64_kernel, so the low band is bit-identical to the
+// three-kernel path while the input is read once and only `low` is written.
+template <typename TI>
+__global__ void __launch_bounds__(256, 4) blur_block_mean_tile_kernel(
+    const TI* __restrict__ in, int h, int w, int r, int f, int TH, int TW,
+    double* __restrict__ low) {
+  extern __shared__ __align__(16) unsigned char bbm_smem[];
+  double* S = reinterpret_cast<double*>(bbm_smem);             // (TH+2r) x (TW+2r)
+  double* D = S + (size_t)(TH + 2 * r) * (TW + 2 * r);        // TH x (TW+2r); then row sums
+  const int pl = blockIdx.z;
+  const int ty0 = blockIdx.y * TH, tx0 = blockIdx.x * TW;
+  const int rows = min(TH, h - ty0), cols = min(TW, w - tx0);
+  const int SW = cols + 2 * r, SH = rows + 2 * r;
+  const TI* P = in + (int64_t)pl * h * w;
+  {
+    const int total = SH * SW;
+    for (int e0 = threadIdx.x; e0 < total; e0 += 8 * 256) {
+      TI v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * 256;
+        if (e < total) {
+          const int i = e / SW, j = e - i * SW;
+          const int gy = min(max(ty0 - r + i, 0), h - 1), gx = min(max(tx0 - r + j, 0), w - 1);
+          v[u] = P[(int64_t)gy * w + gx];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (e0 + u * 256 < total) S[e0 + u * 256] = (double)v[u];
+    }
+  }
+  __syncthreads();
+  // B: rows x cols; after a blur it is stored with one pad double per f-wide
+  // segment (seg stride f+1) so the row-sum lanes below hit distinct banks
+  double* B = S;
+  const bool pad = r > 0 && (size_t)rows * (cols + cols / f) <= (size_t)SH * SW;
+  const int segw = pad ? f + 1 : f, ldb = (cols / f) * segw;
+  if (r > 0) {
+    const double k = (double)(2 * r + 1);
+    for (int e = threadIdx.x; e < rows * SW; e += 256) {
+      const int i = e / SW, j = e - i * SW;
+      double vacc = 0.0;
+      for (int dy = 0; dy <= 2 * r; ++dy) vacc = radd(vacc, S[(i + dy) * SW + j]);
+      D[e] = rdiv(vacc, k);
+    }
+    __syncthreads();
+    // B overwrites S: S is dead once D exists (the barrier above)
+    for (int e = threadIdx.x; e < rows * cols; e += 256) {
+      const int i = e / cols, j = e - i * cols;
+      double hacc = 0.0;
+      for (int dx = 0; dx <= 2 * r; ++dx) hacc = radd(hacc, D[i * SW + j + dx]);
+      const int seg = j / f;
+      B[i * ldb + seg * segw + (j - seg * f)] = rdiv(hacc, k);
+    }
+    __syncthreads();
+  }
+  // row sums of every (block, block row) -> D, then the block means
+  // (block fastest across lanes: row sum t = rr * nblk + blk)
+  const int nbx = cols / f, nby = rows / f, nblk = nbx * nby;
+  for (int t = threadIdx.x; t < nblk * f; t += 256) {
+    const int rr = t / nblk, blk = t - rr * nblk;
+    const int by = blk / nbx, bx = blk - by * nbx;
+    const double* row = B + (by * f + rr) * ldb + bx * segw;
+    D[t] = np_pairwise<double>([&](int i) { return row[i]; }, 0, f);
+  }
+  __syncthreads();
+  const int lw = w / f;
+  for (int blk = threadIdx.x; blk < nblk; blk += 256) {
+    const int by = blk / nbx, bx = blk - by * nbx;
+    double s = 0.0;
+    for (int rr = 0; rr < f; ++rr) s = radd(s, D[rr * nblk + blk]);
+    low[((int64_t)pl * (h / f) + ty0 / f + by) * lw + tx0 / f + bx] = rdiv(s, (double)(f * f));
+  }
+}
+
+// Residual / merge on a 2-D grid: blockIdx.y = plane row, 4 pixels per thread
+// with a stride of 256 (coalesced), 32-bit indexing, shift for power-of-two f.
+template <typename TX>
+__global__ void __launch_bounds__(256) laplacian_residual_rows_kernel(
+    const TX* __restrict__ x, const double* __restrict__ low, int planes, int h, int w, int f,
+    double* __restrict__ high) {
+  const int lw = w / f;
+  const int sh = (f & (f - 1)) == 0 ? __ffs(f) - 1 : -1;
+  for (int64_t prow = blockIdx.y; prow < (int64_t)planes * h; prow += gridDim.y) {
+    const int pl = (int)(prow / h), y = (int)(prow - (int64_t)pl * h);
+    const double* lrow = low + ((int64_t)pl * (h / f) + (sh >= 0 ? y >> sh : y / f)) * lw;
+    const int64_t base = prow * w;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int xx = blockIdx.x * 1024 + e * 256 + threadIdx.x;
+      if (xx < w)
+        high[base + xx] = rsub((double)x[base + xx], lrow[sh >= 0 ? xx >> sh : xx / f]);
+    }
+  }
+}
+
+template <typename TO>
+__global__ void __launch_bounds__(256) laplacian_merge_rows_kernel(
+    const double* __restrict__ low, const double* __restrict__ high, int planes, int h, int w,
+    int f, int square_out, TO* __restrict__ out) {
+  const int lw = w / f;
+  const int sh = (f & (f - 1)) == 0 ? __ffs(f) - 1 : -1;
+  for (int64_t prow = blockIdx.y; prow < (int64_t)planes * h; prow += gridDim.y) {
+    const int pl = (int)(prow / h), y = (int)(prow - (int64_t)pl * h);
+    const double* lrow = low + ((int64_t)pl * (h / f) + (sh >= 0 ? y >> sh : y / f)) * lw;
+    const int64_t base = prow * w;
+    double hv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int xx = blockIdx.x * 1024 + e * 256 + threadIdx.x;
+      hv[e] = xx < w ? high[base + xx] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int xx = blockIdx.x * 1024 + e * 256 + threadIdx.x;
+      if (xx >= w) continue;
+      TO v = (TO)radd(lrow[sh >= 0 ? xx >> sh : xx / f], hv[e]);
+      if (square_out) {
+        const TO sg = v > (TO)0 ? (TO)1 : (v < (TO)0 ? (TO)-1 : (v == (TO)0 ? (TO)0 : v));
+        v = rmul(rmul(sg, v), v);
+      }
+      out[base + xx] = v;
+    }
+  }
+}
+
 template <typename T>
 __global__ void signed_pow_kernel(const T* __restrict__ in, int64_t n, int op, T* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -831,14 +977,23 @@ int ig_phi_analytic(int32_t kind, int32_t radius, double lam, int32_t dtype, con
     const size_t smem = (size_t)(2 * band + 2 * r) * window * es;
     if (smem <= 48 * 1024 && (int64_t)n * channels <= 65535) {
       const dim3 grid((unsigned)((window + band - 1) / band), (unsigned)(n * channels));
-      if (dtype == IG_DTYPE_F32)
-        { phi_tile_kernel<float><<<grid, 256, smem, as_stream(cuda_stream)>>>(
-            kind, radius, (float)(1.0 - lam), (float)lam, lam_zero, s, wxy, window, band, c,
-            (float*)out); note_launch(); }
-      else
-        { phi_tile_kernel<double><<<grid, 256, smem, as_stream(cuda_stream)>>>(
-            kind, radius, 1.0 - lam, lam, lam_zero, s, wxy, window, band, c, (double*)out);
-          note_launch(); }
+      cudaStream_t st = as_stream(cuda_stream);
+#define IG_PHI_TILE(T, R, A, B, O)                                                              \
+  phi_tile_kernel<T, R><<<grid, 256, smem, st>>>(kind, radius, A, B, lam_zero, s, wxy, window, \
+                                                 band, c, (T*)out)
+      if (dtype == IG_DTYPE_F32) {
+        const float A = (float)(1.0 - lam), B = (float)lam;
+        if (r == 0) IG_PHI_TILE(float, 0, A, B, out);
+        else if (r == 1) IG_PHI_TILE(float, 1, A, B, out);
+        else IG_PHI_TILE(float, -1, A, B, out);
+      } else {
+        const double A = 1.0 - lam, B = lam;
+        if (r == 0) IG_PHI_TILE(double, 0, A, B, out);
+        else if (r == 1) IG_PHI_TILE(double, 1, A, B, out);
+        else IG_PHI_TILE(double, -1, A, B, out);
+      }
+#undef IG_PHI_TILE
+      note_launch();
       return cuda_check("ig_phi_analytic");
     }
   }
@@ -946,6 +1101,23 @@ int ig_blur_block_mean_f64(const void* in, int32_t in_dtype, int32_t planes, int
              "spatial dims %dx%d not divisible by factor %d", h, w, factor);
   const int64_t total = (int64_t)planes * h * w;
   cudaStream_t st = as_stream(cuda_stream);
+  if (total == 0) return IG_OK;
+  // fused single-pass path (blur_iters <= 1)
+  if (blur_iters <= 1 && planes <= 65535) {
+    const int r = blur_iters;
+    const int TH = factor * ((16 + factor - 1) / factor), TW = factor * ((128 + factor - 1) / factor);
+    const size_t smem = ((size_t)(TH + 2 * r) * (TW + 2 * r) + (size_t)TH * (TW + 2 * r)) * 8;
+    if (smem <= 48 * 1024) {
+      const dim3 grid((unsigned)((w + TW - 1) / TW), (unsigned)((h + TH - 1) / TH), (unsigned)planes);
+      if (in_dtype == IG_DTYPE_F32)
+        { blur_block_mean_tile_kernel<float><<<grid, 256, smem, st>>>((const float*)in, h, w, r,
+                                                                      factor, TH, TW, low); note_launch(); }
+      else
+        { blur_block_mean_tile_kernel<double><<<grid, 256, smem, st>>>((const double*)in, h, w, r,
+                                                                       factor, TH, TW, low); note_launch(); }
+      return cuda_check("ig_blur_block_mean_f64");
+    }
+  }
   const int grid = grid_for(total, 256);
   double* a = scratch;
   double* b = scratch + total;
@@ -964,6 +1136,18 @@ int ig_blur_block_mean_f64(const void* in, int32_t in_dtype, int32_t planes, int
 
 int ig_laplacian_residual(const void* x, int32_t x_dtype, const double* low, int32_t planes,
                           int32_t h, int32_t w, int32_t factor, double* high, void* cuda_stream) {
+  if ((int64_t)planes * h * w == 0) return IG_OK;
+  {
+    const dim3 grid((unsigned)((w + 1023) / 1024),
+                    (unsigned)((int64_t)planes * h < 65535 ? (int64_t)planes * h : 65535));
+    if (x_dtype == IG_DTYPE_F32)
+      { laplacian_residual_rows_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+          (const float*)x, low, planes, h, w, factor, high); note_launch(); }
+    else
+      { laplacian_residual_rows_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+          (const double*)x, low, planes, h, w, factor, high); note_launch(); }
+    return cuda_check("ig_laplacian_residual");
+  }
   const int64_t total = (int64_t)planes * h * w;
   const int grid = grid_for(total, 256);
   if (x_dtype == IG_DTYPE_F32)
@@ -978,6 +1162,18 @@ int ig_laplacian_residual(const void* x, int32_t x_dtype, const double* low, int
 int ig_laplacian_merge(const double* low, const double* high, int32_t planes, int32_t h,
                        int32_t w, int32_t factor, int32_t out_dtype, int32_t square_out,
                        void* out, void* cuda_stream) {
+  if ((int64_t)planes * h * w == 0) return IG_OK;
+  {
+    const dim3 grid((unsigned)((w + 1023) / 1024),
+                    (unsigned)((int64_t)planes * h < 65535 ? (int64_t)planes * h : 65535));
+    if (out_dtype == IG_DTYPE_F32)
+      { laplacian_merge_rows_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+          low, high, planes, h, w, factor, square_out, (float*)out); note_launch(); }
+    else
+      { laplacian_merge_rows_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+          low, high, planes, h, w, factor, square_out, (double*)out); note_launch(); }
+    return cuda_check("ig_laplacian_merge");
+  }
   const int64_t total = (int64_t)planes * h * w;
   const int grid = grid_for(total, 256);
   if (out_dtype == IG_DTYPE_F32)
