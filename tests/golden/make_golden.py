@@ -268,6 +268,75 @@ def gen_store():
     _save("store", meta, arrays)
 
 
+CLI_CONFIGS = {
+    "base": {"seed": 7, "stages": [{"steps": 2, "window": 16, "stride": 8,
+                                    "denoiser": {"kind": "shrink_smooth", "radius": 1,
+                                                 "lambdas": [0.6, 0.4]}}]},
+    "identity": {"seed": 3, "stages": [{"steps": 1, "window": 16, "stride": 16, "epsilon": 1.0,
+                                        "denoiser": {"kind": "identity"}}]},
+    "f64_multistep": {"seed": 11, "dtype": "float64",
+                      "stages": [{"steps": 2, "window": 32, "stride": 16, "channels": 2,
+                                  "denoiser": {"kind": "multistep", "inner_steps": 3,
+                                               "radius": 2}}]},
+    "two_stage": {"seed": 5, "user_map": {"kind": "procedural", "cell": 8},
+                  "stages": [{"steps": 1, "window": 16, "stride": 8, "corruption": [0.25]},
+                             {"steps": 2, "window": 16, "stride": 8, "scale": 4, "patch": 4,
+                              "denoiser": {"kind": "cond_affine", "lambdas": [0.7, 0.3]}}]},
+}
+CLI_GEN = [("base", "-8,4,32x24"), ("identity", "0,0,16x16"), ("f64_multistep", "5,-40,48x20"),
+           ("two_stage", "-20,12,40x40")]
+
+
+def gen_cli():
+    """The reference CLI (cli.py) run in-process: gen rasters (file bytes and
+    the stats line), render PGMs (plain / signed-square / hillshade) of a
+    seeded raster, verify-mode check names and bench generator-call lines."""
+    import contextlib
+    import io
+    import tempfile
+
+    from infigrid import cli
+    meta = {"configs": CLI_CONFIGS, "gen": [], "verify": {}, "bench": []}
+    arrays = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        def run(argv):
+            buf = io.StringIO()
+            with contextlib.redirect_stdout(buf):
+                rc = cli.main(argv)
+            return rc, buf.getvalue()
+
+        paths = {}
+        for name, doc in CLI_CONFIGS.items():
+            paths[name] = os.path.join(tmp, name + ".json")
+            with open(paths[name], "w") as f:
+                json.dump(doc, f)
+        for k, (name, region) in enumerate(CLI_GEN):
+            out = os.path.join(tmp, f"g{k}.bin")
+            rc, text = run(["gen", paths[name], region, out])
+            assert rc == 0, (name, rc)
+            arrays[f"gen{k}"] = np.frombuffer(open(out, "rb").read(), dtype=np.uint8)
+            meta["gen"].append({"config": name, "region": region, "stdout": text})
+        rng = np.random.default_rng(123)
+        raster = os.path.join(tmp, "r.bin")
+        field = np.cumsum(rng.normal(size=(1, 37, 53)), axis=2).astype(np.float32)
+        pipeline.save_raster(raster, field)
+        arrays["render_in"] = field
+        for tag, extra in (("plain", []), ("ssq", ["--signed-square"]), ("hill", ["--hillshade"]),
+                           ("ssq_hill", ["--signed-square", "--hillshade"])):
+            out = os.path.join(tmp, tag + ".pgm")
+            rc, _ = run(["render", raster, out] + extra)
+            assert rc == 0, tag
+            arrays["pgm_" + tag] = np.frombuffer(open(out, "rb").read(), dtype=np.uint8)
+        for mode in ("oracle", "order", "cost", "transforms"):
+            rc, text = run(["verify", paths["base"], mode])
+            meta["verify"][mode] = {"rc": rc, "stdout": text}
+        for size, trials in ((16, 2), (32, 3)):
+            rc, text = run(["bench", paths["base"], "--size", str(size), "--trials", str(trials)])
+            calls = [ln for ln in text.splitlines() if "denoiser-calls" in ln]
+            meta["bench"].append({"size": size, "trials": trials, "calls": calls})
+    _save("cli", meta, arrays)
+
+
 if __name__ == "__main__":
     info = dict(python=sys.version.split()[0], numpy=np.__version__,
                 machine=platform.machine(), processor=platform.processor(),
@@ -280,3 +349,4 @@ if __name__ == "__main__":
     gen_denoise()
     gen_pipeline()
     gen_store()
+    gen_cli()

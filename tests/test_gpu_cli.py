@@ -1,0 +1,116 @@
+"""CLI on the device path against the reference CLI's own outputs
+(tests/golden/cli.npz, made by tests/golden/make_golden.py running the
+reference): ``gen`` rasters byte-identical, the stats line identical,
+``verify`` lines identical (including the printed max_rel_dev of the dense
+float64 check), ``bench`` generator-call lines identical."""
+
+import contextlib
+import io
+import json
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from paper_2512_08309_b200 import cli, dense  # noqa: E402
+from paper_2512_08309_b200.denoise import DenoiserSpec  # noqa: E402
+from paper_2512_08309_b200.grid import Region, WindowLayout  # noqa: E402
+from paper_2512_08309_b200.pipeline import load_raster, save_raster  # noqa: E402
+
+
+def _run(argv):
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        rc = cli.main(argv)
+    return rc, buf.getvalue()
+
+
+@pytest.fixture(scope="module")
+def cli_golden(golden, tmp_path_factory):
+    meta, z = golden("cli")
+    d = tmp_path_factory.mktemp("cfg")
+    paths = {}
+    for name, doc in meta["configs"].items():
+        paths[name] = str(d / f"{name}.json")
+        with open(paths[name], "w") as f:
+            json.dump(doc, f)
+    return meta, z, paths
+
+
+def test_gen_byte_identical(cli_golden, tmp_path):
+    meta, z, paths = cli_golden
+    for k, g in enumerate(meta["gen"]):
+        out = str(tmp_path / f"g{k}.bin")
+        rc, text = _run(["gen", paths[g["config"]], g["region"], out])
+        assert rc == 0, g
+        assert open(out, "rb").read() == z[f"gen{k}"].tobytes(), g
+        assert text == g["stdout"], g
+
+
+def test_gen_repeat_and_identity(cli_golden, tmp_path):
+    _, _, paths = cli_golden
+    a, b = str(tmp_path / "a.bin"), str(tmp_path / "b.bin")
+    assert cli.main(["gen", paths["base"], "-8,4,32x24", a]) == 0
+    assert cli.main(["gen", paths["base"], "-8,4,32x24", b]) == 0
+    assert open(a, "rb").read() == open(b, "rb").read()
+
+
+def test_render_signed_square_golden(cli_golden, tmp_path):
+    _, z, _ = cli_golden
+    raster = str(tmp_path / "r.bin")
+    save_raster(raster, z["render_in"])
+    for tag, extra in (("ssq", ["--signed-square"]),
+                       ("ssq_hill", ["--signed-square", "--hillshade"])):
+        out = str(tmp_path / f"{tag}.pgm")
+        assert cli.main(["render", raster, out] + extra) == 0
+        assert open(out, "rb").read() == z["pgm_" + tag].tobytes(), tag
+
+
+@pytest.mark.parametrize("mode", ["oracle", "order", "cost", "transforms"])
+def test_verify_lines_identical(cli_golden, mode):
+    meta, _, paths = cli_golden
+    rc, text = _run(["verify", paths["base"], mode])
+    assert rc == meta["verify"][mode]["rc"] == 0
+    assert text == meta["verify"][mode]["stdout"]
+
+
+def test_verify_other_configs_pass(cli_golden):
+    _, _, paths = cli_golden
+    for name in ("f64_multistep", "identity"):
+        for mode in ("oracle", "cost"):
+            rc, text = _run(["verify", paths[name], mode])
+            assert rc == 0, (name, mode, text)
+            assert all(ln.startswith("PASS ") for ln in text.strip().splitlines())
+
+
+def test_bench_call_lines(cli_golden):
+    meta, _, paths = cli_golden
+    for b in meta["bench"]:
+        rc, text = _run(["bench", paths["base"], "--size", str(b["size"]),
+                         "--trials", str(b["trials"])])
+        assert rc == 0
+        assert [ln for ln in text.splitlines() if "denoiser-calls" in ln] == b["calls"]
+        assert f"bench trials={b['trials']} region={b['size']}x{b['size']}" in text
+
+
+def test_dense_trajectory_equals_f64_store():
+    """The f64 shadow-mode store equals the dense f64 definition exactly."""
+    from paper_2512_08309_b200 import SamplerConfig, SamplerState, TileStore
+    spec = DenoiserSpec(kind="shrink_smooth", radius=2, lambdas=(0.7, 0.5, 0.3))
+    cfg = SamplerConfig(steps=3, layout=WindowLayout(32, 16, (5, -3)), denoiser=spec,
+                        seed=21, channels=2, dtype=np.float64)
+    state = SamplerState(cfg, TileStore())
+    target = Region(-40, 17, 75, 50)
+    ref = dense.dense_trajectory(21, 3, cfg.layout_for(0), cfg.weight_for(0).astype(np.float64),
+                                 spec, target, 2)
+    for t in range(3):
+        assert np.array_equal(state.query(t, target), ref[t].crop(target)), t
+
+
+def test_dense_helpers():
+    lay = WindowLayout(16, 8)
+    r = Region(-5, 3, 20, 9)
+    from paper_2512_08309_b200.grid import windows_overlapping
+    assert dense.brute_force_windows(lay, r, 6) == set(windows_overlapping(lay, r))
+    assert dense.count_denoiser_calls_naive(2, lay, Region(0, 0, 16, 16)) == 9 + 9 * 9
