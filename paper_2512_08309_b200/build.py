@@ -74,6 +74,17 @@ def build(verbose: bool = False, force: bool = False) -> str:
                 raise RuntimeError(f"nvcc failed on {name}")
             changed = True
         objs.append(obj)
+    # relink whenever the library was linked from a different object set (a
+    # source reverted to an already-cached object compiles nothing, but the
+    # library must still be relinked from it)
+    stamp = LIB + ".objs"
+    want = "\n".join(os.path.basename(o) for o in objs)
+    try:
+        with open(stamp) as f:
+            if f.read() != want:
+                changed = True
+    except OSError:
+        changed = True
     if changed:
         cmd = [nvcc] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcuda"]
         if verbose:
@@ -82,6 +93,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
             raise RuntimeError("link of libinfigrid_b200.so failed")
+        with open(stamp, "w") as f:
+            f.write(want)
     return LIB
 
 
