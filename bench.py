@@ -160,6 +160,9 @@ def run_gpu(args):
         torch.cuda.synchronize()
 
     sharded = args.workload == "cfg5"
+    # cfg5 halo exchange: "ipc" (peer-memory reads fused into the blend, the
+    # default) or "nccl" (send/recv of the boundary windows)
+    SHARD_EXCHANGE = os.environ.get("IG_SHARD_EXCHANGE", "ipc")
     if sharded:
         from paper_2512_08309_b200 import shard
         big = args.region if args.region else 16384
@@ -168,13 +171,20 @@ def run_gpu(args):
         st = ig.SamplerState(scfg, ig.TileStore())
         if sharded:
             # one big region split in strips over the ranks, owner-computes
-            # windows + NCCL halo exchange of boundary Phi (bitwise = 1 GPU)
+            # windows + halo exchange of boundary Phi (bitwise = 1 GPU)
             R = ig.Region(big * step - 10 ** 6, 10 ** 5, big, big)
             p = shard.plan([WindowLayout(WINDOW, STRIDE)] * T, R, world)
-            xch = shard.p2p_exchange(dist, torch.device("cuda", local), (1, WINDOW, WINDOW),
-                                     torch.float32) if world > 1 else \
-                (lambda t, out, exp: {})
+            if world == 1:
+                xch = lambda t, out, exp: {}          # noqa: E731
+            elif SHARD_EXCHANGE == "ipc":
+                # boundary Phi read in place by the neighbours' blends over NVLink
+                xch = shard.ipc_exchange(dist, (1, WINDOW, WINDOW), torch.float32)
+            else:
+                xch = shard.p2p_exchange(dist, torch.device("cuda", local), (1, WINDOW, WINDOW),
+                                         torch.float32)
             out = shard.run(p, rank, shard.StoreExecutor(st), xch)
+            if hasattr(xch, "close"):
+                xch.close()                         # all ranks done reading peer windows
             return out.cpu().numpy() if e2e else out
         r = _region(step, rank, world)
         if e2e:
@@ -262,9 +272,11 @@ def run_gpu(args):
         "config": {
             "workload": (("cfg5: one %dx%d region per step, 256-px windows stride 128, 2-step "
                           "sampler, UNet Phi (base %d, mults %s), owner-computes window rows "
-                          "sharded over %d GPU(s) with P2P halo exchange of boundary Phi "
-                          "(bitwise equal to 1 GPU)" % (big, big, ucfg.base, list(ucfg.mults),
-                                                        world)) if sharded else
+                          "sharded over %d GPU(s), boundary Phi exchanged by %s "
+                          "(bitwise equal to 1 GPU)" % (
+                              big, big, ucfg.base, list(ucfg.mults), world,
+                              "peer-memory reads in the blend (CUDA IPC)"
+                              if SHARD_EXCHANGE == "ipc" else "NCCL send/recv")) if sharded else
                          ("cfg2: InfiniteDiffusion 2048x2048 region, 256-px windows stride 128, "
                           "2-step consistency sampler, UNet Phi (EDM2-style, base %d, mults %s, "
                           "%d block/level), 1 region per GPU per step" % (
@@ -278,7 +290,8 @@ def run_gpu(args):
             "phi_calls_per_region": calls,
             "mpx_per_s": round(px_total / (ms_max / 1e3) / 1e6, 3),
             "e2e_mpx_per_s": round(px_total / (e2e_ms / 1e3) / 1e6, 3),
-            "parallelism": (f"row-strip shards x{world} + halo exchange" if sharded else
+            "parallelism": (f"row-strip shards x{world} + {SHARD_EXCHANGE} halo exchange"
+                            if sharded else
                             f"independent regions x{world} (no data-path collective)"),
             "l2": "inputs larger than L2: every step streams GBs of fresh activations",
         },

@@ -101,6 +101,21 @@ int ig_blend(const void* const* win_data, int64_t i0, int64_t j0, int32_t ni, in
 int ig_divide_weighted(const void* raw, int32_t channels, int64_t npix, int32_t dtype,
                        void* out, void* cuda_stream);
 
+/* ---- peer-memory halo exchange (cfg5 sharding) -------------------
+ * Replaces the send/recv of boundary Phi windows (shard.py p2p_exchange) by
+ * mapping the producer's allocation: export on the producer, open on the
+ * consumer (peer access enabled lazily from the consumer's current device), and
+ * the consumer's ig_blend reads the windows in place over NVLink.
+ * handle64: 64-byte cudaIpcMemHandle_t of the allocation containing dev_ptr;
+ * offset: dev_ptr - allocation base.  ig_ipc_open returns the mapped base. */
+int ig_ipc_export(const void* dev_ptr, uint8_t* handle64, int64_t* offset);
+int ig_ipc_open(const uint8_t* handle64, void** base_out);
+int ig_ipc_close(void* base);
+/* dedicated exchange buffer (plain cudaMalloc, outside torch's caching pool, so
+ * a peer maps only the exchanged windows) */
+int ig_ipc_alloc(int64_t bytes, void** ptr_out);
+int ig_ipc_free(void* ptr);
+
 /* ---- K6 elevation transforms ---------------------------------------------- */
 int ig_box_mean(const void* in, int32_t planes, int32_t h, int32_t w, int32_t radius,
                 int32_t dtype, void* out, void* cuda_stream);

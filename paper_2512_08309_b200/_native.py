@@ -46,6 +46,11 @@ SIGNATURES = {
     "ig_blend": [V, I64, I64, I32, I32, I32, I32, I64, I64, I32, I32, V, I64, I64, I32, I32,
                  I32, I32, V, V],
     "ig_divide_weighted": [V, I32, I64, I32, V, V],
+    "ig_ipc_export": [V, V, V],
+    "ig_ipc_open": [V, V],
+    "ig_ipc_close": [V],
+    "ig_ipc_alloc": [I64, V],
+    "ig_ipc_free": [V],
     "ig_box_mean": [V, I32, I32, I32, I32, I32, V, V],
     "ig_blur_block_mean_f64": [V, I32, I32, I32, I32, I32, I32, V, V, V],
     "ig_laplacian_residual": [V, I32, V, I32, I32, I32, I32, V, V],

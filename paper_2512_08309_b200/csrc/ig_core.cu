@@ -9,6 +9,8 @@
 #include <atomic>
 #include <cstring>
 
+#include <cuda.h>
+
 #include "ig_common.cuh"
 #include "ig_noise.cuh"
 
@@ -1273,6 +1275,92 @@ int ig_raster_map(const float* raster, int32_t rc, int32_t rh, int32_t rw, int32
   { raster_map_kernel<<<grid_for(total, 256), 256, 0, as_stream(cuda_stream)>>>(
       raster, rc, rh, rw, mode, x0, y0, w, h, channels, out); note_launch(); }
   return cuda_check("ig_raster_map");
+}
+
+// ---------------------------------------------------------------------------
+// Peer-memory halo exchange: a rank exports the device
+// allocation holding its Phi windows as a CUDA IPC handle; a neighbour maps it
+// (peer access enabled lazily from ITS current device, so its blend kernel
+// reads the windows straight over NVLink -- the "exchange" is the blend's own
+// loads, no send/recv copy).  Handles refer to the whole allocation, so the
+// window's byte offset inside it travels alongside.
+int ig_ipc_export(const void* dev_ptr, uint8_t* handle64, int64_t* offset) {
+  IG_REQUIRE(dev_ptr != nullptr && handle64 != nullptr && offset != nullptr,
+             "ipc_export: null argument");
+  // driver entry point fetched at run time (no link-time libcuda dependency:
+  // the library must load on a host without a driver)
+  using AddrRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static AddrRangeFn addr_range = nullptr;
+  if (!addr_range) {
+    cudaDriverEntryPointQueryResult q;
+    void* fp = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      set_error("ipc_export: cuMemGetAddressRange unavailable");
+      return IG_ERR_CUDA;
+    }
+    addr_range = reinterpret_cast<AddrRangeFn>(fp);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (addr_range(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS) {
+    set_error("ipc_export: pointer %p is not a device allocation", dev_ptr);
+    return IG_ERR_ARG;
+  }
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) {
+    set_error("ipc_export: cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    return IG_ERR_CUDA;
+  }
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle64, &h, 64);
+  *offset = (int64_t)((CUdeviceptr)dev_ptr - base);
+  return IG_OK;
+}
+
+int ig_ipc_open(const uint8_t* handle64, void** base_out) {
+  IG_REQUIRE(handle64 != nullptr && base_out != nullptr, "ipc_open: null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  cudaError_t e = cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    set_error("ipc_open: cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    return IG_ERR_CUDA;
+  }
+  return IG_OK;
+}
+
+// Dedicated exchange allocation (outside any caching allocator): an IPC handle
+// maps the WHOLE allocation containing a pointer, so exporting a window that
+// lives inside a multi-GB pool segment would map the pool on every peer.
+int ig_ipc_alloc(int64_t bytes, void** ptr_out) {
+  IG_REQUIRE(bytes > 0 && ptr_out != nullptr, "ipc_alloc: bad size");
+  cudaError_t e = cudaMalloc(ptr_out, (size_t)bytes);
+  if (e != cudaSuccess) {
+    set_error("ipc_alloc: cudaMalloc(%lld): %s", (long long)bytes, cudaGetErrorString(e));
+    return IG_ERR_CUDA;
+  }
+  return IG_OK;
+}
+
+int ig_ipc_free(void* ptr) {
+  cudaError_t e = cudaFree(ptr);
+  if (e != cudaSuccess) {
+    set_error("ipc_free: %s", cudaGetErrorString(e));
+    return IG_ERR_CUDA;
+  }
+  return IG_OK;
+}
+
+int ig_ipc_close(void* base) {
+  cudaError_t e = cudaIpcCloseMemHandle(base);
+  if (e != cudaSuccess) {
+    set_error("ipc_close: cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    return IG_ERR_CUDA;
+  }
+  return IG_OK;
 }
 
 }  // extern "C"

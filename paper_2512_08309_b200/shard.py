@@ -187,6 +187,116 @@ def p2p_exchange(dist, device, window_shape, dtype):
     return exchange
 
 
+class PeerWindow:
+    """One window living in ANOTHER rank's device allocation, mapped into this
+    process through CUDA IPC.  The store only ever uses a window through its
+    device address (the blend's pointer table), so this is all it carries."""
+
+    is_peer = True
+
+    def __init__(self, ptr: int, shape, dtype):
+        self._ptr = ptr
+        self.shape = tuple(shape)
+        self.dtype = dtype
+
+    def data_ptr(self) -> int:
+        return self._ptr
+
+
+class _DeviceBuffer:
+    """A raw device allocation seen as a torch tensor (CUDA array interface)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def ipc_exchange(dist, window_shape, dtype):
+    """Halo exchange over peer memory (NVLink on B200): no inter-GPU copy.
+
+    Per step every producer packs its outgoing windows (all destinations) into
+    ONE dedicated device allocation (ig_ipc_alloc, outside torch's caching
+    pool -- an IPC handle maps the whole allocation it points into) with an
+    on-device copy, exports its handle, and all ranks exchange the small
+    metadata in one all_gather_object.  Each consumer maps the allocation
+    (ig_ipc_open enables peer access from its own device) and installs the
+    windows as PeerWindow views: its blend kernel reads the boundary windows
+    in place, over NVLink, in the canonical (j, i) order -- the exchange is
+    fused into the blend's loads.
+
+    Ordering: producers synchronise their device before publishing; consumers
+    launch their blends only after the gather.  Lifetime: every step's buffer
+    stays allocated (the windows of step t are parents of step t-1 and the
+    final query reads step 0's) until ``exchange.close()`` -- device sync +
+    barrier (all ranks done reading), then unmap and free."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from . import _device as dev
+    from . import _native
+
+    L = _native.lib()
+    rank = dist.get_rank()
+    typestr = np.dtype(str(dtype).replace("torch.", "")).str
+    wbytes = int(np.prod(window_shape)) * torch.empty((), dtype=dtype).element_size()
+    owned: list[int] = []                 # our exchange buffers
+    mapped: dict[bytes, int] = {}         # peer handle -> mapped base
+
+    def exchange(t, outgoing, expect):
+        items = [(dst, x) for dst in sorted(outgoing) for x in outgoing[dst]]
+        mine = {}
+        if items:
+            p = ctypes.c_void_p()
+            _native.check(L.ig_ipc_alloc(len(items) * wbytes, ctypes.byref(p)), "ig_ipc_alloc")
+            owned.append(p.value)
+            buf = torch.as_tensor(_DeviceBuffer(p.value, (len(items),) + tuple(window_shape),
+                                                typestr), device=dev.device())
+            for k, (dst, x) in enumerate(items):
+                buf[k].copy_(x)
+            h = (ctypes.c_uint8 * 64)()
+            off = ctypes.c_int64()
+            _native.check(L.ig_ipc_export(ctypes.c_void_p(p.value), h, ctypes.byref(off)),
+                          "ig_ipc_export")
+            for k, (dst, _) in enumerate(items):
+                mine.setdefault(dst, []).append((bytes(h), off.value + k * wbytes))
+        torch.cuda.synchronize()          # published windows are complete
+        meta = [None] * dist.get_world_size()
+        dist.all_gather_object(meta, mine)
+        got = {}
+        for src, n in expect.items():
+            entries = meta[src].get(rank, []) if n else []
+            if len(entries) != n:
+                raise RuntimeError(f"ipc_exchange: rank {src} published {len(entries)} windows "
+                                   f"for rank {rank}, expected {n}")
+            views = []
+            for hb, off in entries:
+                base = mapped.get(hb)
+                if base is None:
+                    q = ctypes.c_void_p()
+                    _native.check(L.ig_ipc_open((ctypes.c_uint8 * 64).from_buffer_copy(hb),
+                                                ctypes.byref(q)), "ig_ipc_open")
+                    base = mapped[hb] = q.value
+                views.append(PeerWindow(base + off, window_shape, dtype))
+            got[src] = views
+        return got
+
+    def close():
+        torch.cuda.synchronize()
+        dist.barrier()                   # every consumer is done reading
+        for base in mapped.values():
+            _native.check(L.ig_ipc_close(ctypes.c_void_p(base)), "ig_ipc_close")
+        mapped.clear()
+        dist.barrier()                   # every peer has unmapped our buffers
+        for ptr in owned:
+            _native.check(L.ig_ipc_free(ctypes.c_void_p(ptr)), "ig_ipc_free")
+        owned.clear()
+
+    exchange.close = close
+    return exchange
+
+
 def local_exchange(mailbox: dict, rank: int):
     """In-process exchange used to emulate ranks sequentially (one GPU):
     senders deposit, receivers collect (ranks must run in dependency order

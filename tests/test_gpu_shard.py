@@ -40,3 +40,66 @@ def test_sharded_equals_single(kind, steps, H, s, world, region):
     got = np.concatenate([s_.cpu().numpy() for s_ in strips], axis=1)
     np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
     assert sum(st.total_denoiser_calls() for st in states) == single.total_denoiser_calls()
+
+
+# ---------------------------------------------------------------------------
+# Peer-memory halo exchange (shard.ipc_exchange): real processes, each with its
+# own CUDA context; on the round-end box they share one GPU (CUDA IPC works
+# between processes on the same device exactly as across NVLink peers; no
+# kernel waits on another rank -- publication is host-ordered after a device
+# sync).  The gathered strips must be bitwise equal to a one-process query and
+# the boundary windows must have been read in place (PeerWindow slots).
+
+def _ipc_worker(rank, world, port_, kind, steps, H, s, region, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        cfg = _cfg(kind, steps, H, s)
+        st = ig.SamplerState(cfg, ig.TileStore())
+        p = shard.plan([WindowLayout(H, s)] * steps, Region(*region), world)
+        xch = shard.ipc_exchange(dist, (1, H, H), torch.float32)
+        strip = shard.run(p, rank, shard.StoreExecutor(st), xch).cpu().numpy()
+        peers = sum(1 for t in range(steps)
+                    for slot in st.store._tensor(st.handles[t]).lru.values()
+                    if getattr(slot.data, "is_peer", False))
+        xch.close()
+        q.put((rank, strip, st.total_denoiser_calls(), peers))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,steps,H,s,world,region", [
+    ("shrink", 2, 16, 8, 2, (-37, 11, 70, 90)),
+    ("shrink", 3, 16, 8, 3, (0, 0, 64, 96)),
+    ("unet", 2, 64, 32, 2, (0, 0, 128, 192)),
+])
+def test_ipc_exchange_bitwise(kind, steps, H, s, world, region):
+    import multiprocessing as mp
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port_ = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(k, world, port_, kind, steps, H, s, region, q))
+             for k in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    cfg = _cfg(kind, steps, H, s)
+    single = ig.SamplerState(cfg, ig.TileStore())
+    want = single.query(0, Region(*region))
+    got = np.concatenate([r_[1] for r_ in res], axis=1)
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+    assert sum(r_[2] for r_ in res) == single.total_denoiser_calls()   # no Phi twice
+    assert sum(r_[3] for r_ in res) > 0          # boundary windows were read in place
