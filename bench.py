@@ -166,6 +166,8 @@ def run_gpu(args):
     if sharded:
         from paper_2512_08309_b200 import shard
         big = args.region if args.region else 16384
+        if world > 1 and SHARD_EXCHANGE == "ipc" and not shard.ipc_supported(dist):
+            SHARD_EXCHANGE = "nccl"            # peers not mappable here: send/recv
 
     def one_step(step, e2e):
         st = ig.SamplerState(scfg, ig.TileStore())

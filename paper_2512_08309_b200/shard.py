@@ -297,6 +297,62 @@ def ipc_exchange(dist, window_shape, dtype):
     return exchange
 
 
+_IPC_OK: dict = {}
+
+
+def ipc_supported(dist) -> bool:
+    """Collective capability probe (once per process group): every rank maps a
+    small buffer of every other rank through CUDA IPC.  All ranks get the same
+    answer, so a launcher that hides peer devices makes every rank fall back to
+    the send/recv exchange instead of failing mid-step."""
+    key = id(dist.group.WORLD)
+    if key in _IPC_OK:
+        return _IPC_OK[key]
+    import ctypes
+
+    import torch
+
+    from . import _native
+
+    ok, ptr, opened = True, None, []
+    try:
+        L = _native.lib()
+        p = ctypes.c_void_p()
+        _native.check(L.ig_ipc_alloc(4096, ctypes.byref(p)), "ig_ipc_alloc")
+        ptr = p.value
+        h = (ctypes.c_uint8 * 64)()
+        off = ctypes.c_int64()
+        _native.check(L.ig_ipc_export(ctypes.c_void_p(ptr), h, ctypes.byref(off)), "ig_ipc_export")
+        mine = bytes(h)
+    except Exception:  # noqa: BLE001 -- any failure means "not supported"
+        ok, mine = False, b""
+    torch.cuda.synchronize()
+    handles = [None] * dist.get_world_size()
+    dist.all_gather_object(handles, mine)
+    if ok:
+        try:
+            for r, hb in enumerate(handles):
+                if r == dist.get_rank():
+                    continue
+                if not hb:
+                    raise RuntimeError("peer could not export")
+                q = ctypes.c_void_p()
+                _native.check(L.ig_ipc_open((ctypes.c_uint8 * 64).from_buffer_copy(hb),
+                                            ctypes.byref(q)), "ig_ipc_open")
+                opened.append(q.value)
+        except Exception:  # noqa: BLE001
+            ok = False
+    votes = [None] * dist.get_world_size()
+    dist.all_gather_object(votes, ok)
+    for base in opened:
+        L.ig_ipc_close(ctypes.c_void_p(base))
+    dist.barrier()
+    if ptr is not None:
+        L.ig_ipc_free(ctypes.c_void_p(ptr))
+    _IPC_OK[key] = all(votes)
+    return _IPC_OK[key]
+
+
 def local_exchange(mailbox: dict, rank: int):
     """In-process exchange used to emulate ranks sequentially (one GPU):
     senders deposit, receivers collect (ranks must run in dependency order

@@ -63,6 +63,7 @@ def _ipc_worker(rank, world, port_, kind, steps, H, s, region, q):
         cfg = _cfg(kind, steps, H, s)
         st = ig.SamplerState(cfg, ig.TileStore())
         p = shard.plan([WindowLayout(H, s)] * steps, Region(*region), world)
+        assert shard.ipc_supported(dist)
         xch = shard.ipc_exchange(dist, (1, H, H), torch.float32)
         strip = shard.run(p, rank, shard.StoreExecutor(st), xch).cpu().numpy()
         peers = sum(1 for t in range(steps)
