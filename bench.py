@@ -84,7 +84,7 @@ class ClockSampler:
                     self.samples.append([v.strip() for v in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.5)
+            self._stop.wait(0.02)         # back to back: the timed region may be < 1 s
 
     def __enter__(self):
         self._t.start()
