@@ -62,6 +62,18 @@ def test_unet_hierarchy_vs_oracle():
                                     dtype=np.dtype(np.float32))
     elev = transforms.laplacian_decode_signed_square(transforms.laplacian_stabilize(pair, 1))
     assert elev.shape == (128, 128) and np.isfinite(elev).all()
+    # final elevations (metres, the reference's signed-square convention) against the same
+    # decode of the fp32 oracle's channels: stated tolerance RMS <= 3% and max-abs <= 25%
+    # of the oracle elevation's standard deviation (bf16 activations, fp32 accumulation)
+    low_r = transforms.block_mean(want[0].astype(np.float64), 8)
+    pair_r = transforms.LaplacianPair(low=low_r, high=want[1].astype(np.float64), factor=8,
+                                      dtype=np.dtype(np.float32))
+    elev_r = transforms.laplacian_decode_signed_square(transforms.laplacian_stabilize(pair_r, 1))
+    d = elev.astype(np.float64) - elev_r.astype(np.float64)
+    std_m = float(elev_r.std())
+    rms_m, max_m = float(np.sqrt(np.mean(d ** 2))), float(np.abs(d).max())
+    print(f"elevation vs oracle: rms {rms_m:.4g} m, max-abs {max_m:.4g} m, oracle std {std_m:.4g} m")
+    assert rms_m <= RMS_TOL * std_m and max_m <= MAX_TOL * std_m, (rms_m, max_m, std_m)
     # seed consistency through the whole hierarchy: a sub-region from a fresh store
     store2, h2 = _gpu_pipeline()
     sub = store2.read_values(h2, Region(32, 64, 64, 32))
