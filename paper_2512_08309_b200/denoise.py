@@ -23,6 +23,7 @@ from . import _device as dev
 from ._native import PHI_COND_AFFINE, PHI_IDENTITY, PHI_SHRINK_SMOOTH, call
 from .errors import CoverageError, ShapeError
 from .grid import Region, WindowIndex, WindowLayout, window_region
+from .noise import STREAM_CONDITIONING  # noqa: F401  (re-exported as in denoise.py:19)
 
 KINDS = ("identity", "shrink_smooth", "cond_affine", "multistep", "unet")
 _KIND_CODE = {"identity": PHI_IDENTITY, "shrink_smooth": PHI_SHRINK_SMOOTH,

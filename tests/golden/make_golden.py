@@ -337,6 +337,29 @@ def gen_cli():
     _save("cli", meta, arrays)
 
 
+def gen_api():
+    """The reference's public API surface: package __all__, every public
+    module-level name per submodule, class members and parameter names."""
+    import importlib
+    import inspect
+    surface = {"all": list(infigrid.__all__), "modules": {}, "classes": {}, "params": {}}
+    for m in ("grid", "noise", "sampler", "store", "pipeline", "transforms", "denoise", "errors"):
+        mod = importlib.import_module("infigrid." + m)
+        surface["modules"][m] = sorted(
+            n for n in dir(mod) if not n.startswith("_")
+            and getattr(getattr(mod, n), "__module__", "infigrid." + m) == "infigrid." + m)
+    for n in infigrid.__all__:
+        o = getattr(infigrid, n)
+        if inspect.isclass(o):
+            surface["classes"][n] = sorted(k for k in dir(o) if not k.startswith("_"))
+        elif callable(o):
+            surface["params"][n] = [(p.name, repr(p.default) if p.default is not p.empty else None)
+                                    for p in inspect.signature(o).parameters.values()]
+    with open(os.path.join(HERE, "api_surface.json"), "w") as f:
+        json.dump(surface, f, indent=1, sort_keys=True)
+    print("wrote api_surface.json")
+
+
 if __name__ == "__main__":
     info = dict(python=sys.version.split()[0], numpy=np.__version__,
                 machine=platform.machine(), processor=platform.processor(),
@@ -350,3 +373,4 @@ if __name__ == "__main__":
     gen_pipeline()
     gen_store()
     gen_cli()
+    gen_api()

@@ -170,3 +170,26 @@ def test_parent_slab_is_parent_of_window_bbox():
                              (i_hi - i_lo) * lay.stride + lay.window,
                              (j_hi - j_lo) * lay.stride + lay.window)
                 assert dep.parent_region(box) == ref
+
+
+def test_api_surface_matches_reference():
+    """Every public name of the reference package (tests/golden/api_surface.json,
+    made by running the reference) exists here: package __all__, each
+    submodule's public names, class members, and function parameter names and
+    defaults in order."""
+    import importlib
+    import inspect
+    import json
+
+    import paper_2512_08309_b200 as ours
+    surf = json.load(open(os.path.join(ROOT, "tests", "golden", "api_surface.json")))
+    assert [n for n in surf["all"] if not hasattr(ours, n)] == []
+    for m, names in surf["modules"].items():
+        mod = importlib.import_module("paper_2512_08309_b200." + m)
+        assert [n for n in names if not hasattr(mod, n)] == [], m
+    for c, members in surf["classes"].items():
+        assert [k for k in members if not hasattr(getattr(ours, c), k)] == [], c
+    for f, params in surf["params"].items():
+        got = [(p.name, repr(p.default) if p.default is not p.empty else None)
+               for p in inspect.signature(getattr(ours, f)).parameters.values()]
+        assert got[:len(params)] == [tuple(p) for p in params], f
