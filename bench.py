@@ -68,8 +68,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, active=True):
         self.index = index
+        self.active = active          # rank 0 only: N ranks polling NVML would contend
         self.samples = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -87,12 +88,14 @@ class ClockSampler:
             self._stop.wait(0.02)         # back to back: the timed region may be < 1 s
 
     def __enter__(self):
-        self._t.start()
+        if self.active:
+            self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=6)
+        if self.active:
+            self._t.join(timeout=6)
 
     def summary(self):
         if not self.samples:
@@ -201,7 +204,7 @@ def run_gpu(args):
     # ---- device-timed region (value), with per-conv-launch events (roofline)
     unet.TIMING.enable(stream)
     l0 = _native.launch_count()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, active=(rank == 0)) as clk:
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
