@@ -2566,6 +2566,30 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
     const int grp = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;                      // query row == TMEM lane
     const uint32_t lanebase = (uint32_t)(quarter * 32) << 16;
+    auto item_epilogue = [&](int e) {     // y = O / l of item e (l = O column 64)
+      int img, hd, qt;
+      item_of(e, img, hd, qt);
+      const int ob = e & 1;
+      mbar_wait(&ofull[ob], (e >> 1) & 1);
+      tc_fence_after();
+      uint32_t ro[DG];
+      float lrow[16];
+      tmem_ld16(tmem + lanebase + 256 + ob * 128 + grp * DG, reinterpret_cast<float*>(ro));
+      tmem_ld16(tmem + lanebase + 256 + ob * 128 + 64, lrow);
+      tc_fence_before();
+      mbar_arrive(&oempty[ob]);
+      const float inv_l = 1.f / lrow[0];
+      if (qt * 128 + row < hw) {
+        __nv_bfloat16* dst = y + ((int64_t)img * hw + qt * 128 + row) * c + hd * 64 + grp * DG;
+        uint4 u[2];
+        __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(u);
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2)
+          o[q2] = __floats2bfloat162_rn(__uint_as_float(ro[2 * q2]) * inv_l,
+                                        __uint_as_float(ro[2 * q2 + 1]) * inv_l);
+        stg_v8(dst, u[0], u[1]);
+      }
+    };
     int it = 0, j = 0;
     for (int t = 0; t < T; ++t) {
       const int s = t & 1, ph = (t >> 1) & 1;
@@ -2602,33 +2626,13 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&pfull[s]);
-      if (j == ktiles - 1) {
-        // item done: O / l (l = O column 64, the ones block)
-        int img, hd, qt;
-        item_of(it, img, hd, qt);
-        const int ob = it & 1;
-        mbar_wait(&ofull[ob], (it >> 1) & 1);
-        tc_fence_after();
-        uint32_t ro[DG];
-        float lrow[16];
-        tmem_ld16(tmem + lanebase + 256 + ob * 128 + grp * DG, reinterpret_cast<float*>(ro));
-        tmem_ld16(tmem + lanebase + 256 + ob * 128 + 64, lrow);
-        tc_fence_before();
-        mbar_arrive(&oempty[ob]);
-        const float inv_l = 1.f / lrow[0];
-        if (qt * 128 + row < hw) {
-          __nv_bfloat16* dst = y + ((int64_t)img * hw + qt * 128 + row) * c + hd * 64 + grp * DG;
-          uint4 u[2];
-          __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(u);
-#pragma unroll
-          for (int q2 = 0; q2 < 8; ++q2)
-            o[q2] = __floats2bfloat162_rn(__uint_as_float(ro[2 * q2]) * inv_l,
-                                          __uint_as_float(ro[2 * q2 + 1]) * inv_l);
-          stg_v8(dst, u[0], u[1]);
-        }
-      }
+      // the O / l epilogue of item it-1 runs after this item's FIRST tile, not
+      // right after the item's last one: the last PV then completes under this
+      // tile's softmax instead of idling all 16 warps (O is double-buffered)
+      if (j == 0 && it > 0) item_epilogue(it - 1);
       if (++j == ktiles) { j = 0; ++it; }
     }
+    if (my_items > 0) item_epilogue(my_items - 1);
   }
   tc_fence_before();
   __syncthreads();
