@@ -2216,6 +2216,20 @@ __global__ void __launch_bounds__(256) unet_out_head_tn_kernel(
     const uint32_t sbase = smem_u32(buf + sb * STRIDE);
     int img, y0, x0;
     tile_xy(tile, img, y0, x0);
+    // x_noisy of this thread's phase-2 outputs, loaded before the MMA phase so its
+    // HBM latency is hidden (ncu: 33% of the stall samples sat on this load)
+    constexpr int NQ = (S * 128 * C + 255) / 256;
+    float xn[NQ];
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const int q = threadIdx.x + k * 256;
+      xn[k] = 0.f;
+      if (q < S * 128 * C) {
+        const int c = q / (S * 128), rem = q - c * S * 128;
+        const int i = rem / 128, x = rem - i * 128;
+        xn[k] = __ldg(x_noisy + (((int64_t)img * C + c) * h + y0 + i) * w + x0 + x);
+      }
+    }
     mbar_wait(&bar[sb], (uint32_t)((it >> 1) & 1));
     // 1. partials: IR rows x 9 blocks of 16 input pixels, spread over the 8 warps
     for (int blk = warp; blk < IR * 9; blk += 8) {
@@ -2254,7 +2268,10 @@ __global__ void __launch_bounds__(256) unet_out_head_tn_kernel(
       tma_load_4d(buf + sb * STRIDE, &map_xa, &bar[sb], 0, nx - 1, ny - 1, ni);
     }
     // 2. each output sums its 9 taps: output (i, x) <- input (i+dy, x+dx) (halo coords)
-    for (int q = threadIdx.x; q < S * 128 * C; q += 256) {
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      const int q = threadIdx.x + k * 256;
+      if (q >= S * 128 * C) break;
       const int c = q / (S * 128), rem = q - c * S * 128;
       const int i = rem / 128, x = rem - i * 128;
       float sum = 0.f;
@@ -2262,7 +2279,7 @@ __global__ void __launch_bounds__(256) unet_out_head_tn_kernel(
       for (int tap = 0; tap < 9; ++tap)
         sum += part[((i + tap / 3) * PX + x + tap % 3) * TP + c * 9 + tap];
       const int64_t idx = (((int64_t)img * C + c) * h + y0 + i) * w + x0 + x;
-      out[idx] = __fadd_rn(__fmul_rn(c_skip, __ldg(x_noisy + idx)), __fmul_rn(c_out, sum));
+      out[idx] = __fadd_rn(__fmul_rn(c_skip, xn[k]), __fmul_rn(c_out, sum));
     }
     __syncthreads();   // partials consumed before the next tile overwrites them
   }
