@@ -781,6 +781,7 @@ struct HaloArgs {
   int hbufs;         // halo buffers in the ring (CTA-pair kernel: 2 or 3)
   int sbufs;         // CTA-pair kernel: separate ring for the 1x1 skip chunks (0: they
                      // ride in the halo ring)
+  int l2pf;          // CTA-pair kernel: L2-prefetch the next tile's halo boxes
 };
 
 template <int N, int ROWS>
@@ -1060,6 +1061,15 @@ __device__ __forceinline__ void tma2_load_4d(void* dst, const CUtensorMap* map, 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
       : "memory");
 }
+// L2 prefetch of a tensor-map box (no SMEM, no barrier): the producer warms L2
+// with the halo box of its NEXT tile so that tile's real TMA load is an L2 hit
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2,
+                                                int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
 __device__ __forceinline__ void tma2_load_5d(void* dst, const CUtensorMap* map, uint32_t bar,
                                              int c0, int c1, int c2, int c3, int c4) {
   asm volatile(
@@ -1220,6 +1230,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         const int r = tile - img * tiles_per_img;
         const int ty = r / ha.tiles_x;
         const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
+        if constexpr (!GUT) {
+          // warm L2 with the next tile's halo boxes: with two halo buffers a box is
+          // loaded only one tile ahead, too little to hide an HBM round trip
+          // (ncu, enc0.0.c1: epilogue idle on tfull 28%, DRAM at 46% of peak)
+          const int prn = pr + pstride;
+          if (prn < npairs && ha.l2pf) {
+            const int tn = 2 * prn + (int)rank;
+            const int imgn = tn / tiles_per_img;
+            const int rn = tn - imgn * tiles_per_img;
+            const int tyn = rn / ha.tiles_x;
+            const int x0n = (rn - tyn * ha.tiles_x) * 128, y0n = tyn * ROWS;
+            if (imgn < args.n) {
+              for (int kc = 0; kc < kchunks; ++kc) {
+                if (kc < args.kchunks_a) {
+                  if (!args.up_a) tma_prefetch_4d(&map_a, kc * 64, x0n - 1, y0n - 1, imgn);
+                } else {
+                  tma_prefetch_4d(&map_b, (kc - args.kchunks_a) * 64, x0n - 1, y0n - 1, imgn);
+                }
+              }
+            }
+          }
+        }
         for (int kc = 0; kc < nchunks; ++kc) {
           const bool sring = SB && kc >= kchunks;    // skip chunk in its own ring
           uint64_t* fb = sring ? &sfull[ss] : &hfull[hs];
@@ -3041,6 +3073,10 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   }
   HaloArgs ha;
   ha.c = a;
+  // single-chunk N = 64 layers only (their one halo box per tile is the whole load;
+  // r01 A/B: enc0.0.c2 452 -> 420 us; multi-chunk and N = 128 layers measured
+  // slower with it); variant 12: off
+  ha.l2pf = g_variant != 12 && N == 64 && a.kchunks_a + a.kchunks_b == 1;
   if (GUT) {
     ha.tiles_x = 1;
     ha.tiles_y = (a.gP + ROWS * 128 - 1) / (ROWS * 128);
