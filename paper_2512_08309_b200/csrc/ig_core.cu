@@ -618,49 +618,6 @@ __global__ void block_mean_f64_kernel(const double* __restrict__ in, int planes,
   }
 }
 
-template <typename TX>
-__global__ void laplacian_residual_kernel(const TX* __restrict__ x, const double* __restrict__ low,
-                                          int planes, int h, int w, int f,
-                                          double* __restrict__ high) {
-  const int64_t total = (int64_t)planes * h * w;
-  const int lh = h / f, lw = w / f;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t pl = idx / ((int64_t)h * w);
-    const int rem = (int)(idx - pl * h * w);
-    const int y = rem / w, xx = rem - y * w;
-    high[idx] = rsub((double)x[idx], low[(pl * lh + y / f) * lw + xx / f]);
-  }
-}
-
-template <typename TO>
-__global__ void laplacian_merge_kernel(const double* __restrict__ low,
-                                       const double* __restrict__ high, int planes, int h, int w,
-                                       int f, int square_out, TO* __restrict__ out) {
-  const int64_t total = (int64_t)planes * h * w;
-  const int lh = h / f, lw = w / f;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t pl = idx / ((int64_t)h * w);
-    const int rem = (int)(idx - pl * h * w);
-    const int y = rem / w, xx = rem - y * w;
-    TO v = (TO)radd(low[(pl * lh + y / f) * lw + xx / f], high[idx]);
-    if (square_out) {
-      // signed_square: np.sign(x) * x * x  (left to right)
-      const TO sg = v > (TO)0 ? (TO)1 : (v < (TO)0 ? (TO)-1 : (v == (TO)0 ? (TO)0 : v));
-      v = rmul(rmul(sg, v), v);
-    }
-    out[idx] = v;
-  }
-}
-
-// Fused widen + blur3 (one box_mean radius-1 pass, or none) + block_mean for
-// the Laplacian low band (transforms.py:54-67, 89-114): one CTA = a TH x TW
-// tile of one plane (multiples of the factor), staged once in SMEM as float64
-// with a clamped 1-pixel halo.  The blur is the separable sequence of
-// box_mean_kernel (column sums / 3, then row sum / 3) and the block means the
-// sequence of block_mean_f64_kernel, so the low band is bit-identical to the
-// three-kernel path while the input is read once and only `low` is written.
 template <typename TI>
 __global__ void __launch_bounds__(256, 4) blur_block_mean_tile_kernel(
     const TI* __restrict__ in, int h, int w, int r, int f, int TH, int TW,
@@ -1150,15 +1107,6 @@ int ig_laplacian_residual(const void* x, int32_t x_dtype, const double* low, int
           (const double*)x, low, planes, h, w, factor, high); note_launch(); }
     return cuda_check("ig_laplacian_residual");
   }
-  const int64_t total = (int64_t)planes * h * w;
-  const int grid = grid_for(total, 256);
-  if (x_dtype == IG_DTYPE_F32)
-    { laplacian_residual_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        (const float*)x, low, planes, h, w, factor, high); note_launch(); }
-  else
-    { laplacian_residual_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        (const double*)x, low, planes, h, w, factor, high); note_launch(); }
-  return cuda_check("ig_laplacian_residual");
 }
 
 int ig_laplacian_merge(const double* low, const double* high, int32_t planes, int32_t h,
@@ -1176,15 +1124,6 @@ int ig_laplacian_merge(const double* low, const double* high, int32_t planes, in
           low, high, planes, h, w, factor, square_out, (double*)out); note_launch(); }
     return cuda_check("ig_laplacian_merge");
   }
-  const int64_t total = (int64_t)planes * h * w;
-  const int grid = grid_for(total, 256);
-  if (out_dtype == IG_DTYPE_F32)
-    { laplacian_merge_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        low, high, planes, h, w, factor, square_out, (float*)out); note_launch(); }
-  else
-    { laplacian_merge_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-        low, high, planes, h, w, factor, square_out, (double*)out); note_launch(); }
-  return cuda_check("ig_laplacian_merge");
 }
 
 int ig_signed_pow(const void* in, int64_t n, int32_t op, int32_t dtype, void* out,

@@ -2419,21 +2419,6 @@ __device__ __forceinline__ float ex2_approx(float x) {   // MUFU.EX2, ex2(-inf) 
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA pipe (offloads the MUFU): x = n + f, n = rint(x) via the
-// 1.5*2^23 magic constant, f in [-1/2, 1/2], 2^f by its cubic Taylor
-// polynomial (relative error < 7e-4, well inside bf16's 3.9e-3), exponent
-// added into the float's bits.  Inputs below -126 (masked keys) give ~2^-126.
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;
-  const float fl = t - 12582912.f;
-  const float f = x - fl;
-  float p = fmaf(0.0555041087f, f, 0.2402265070f);
-  p = fmaf(p, f, 0.6931471806f);
-  p = fmaf(p, f, 1.0f);
-  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
-}
-
 struct AttnSmem {
   static constexpr int Q0 = 0;                       // 2 x 16 KB [128 q][64 d]
   static constexpr int K0 = 2 * 16384;               // 2 x 16 KB [128 keys][64 d]
