@@ -130,8 +130,18 @@ def upload_i64(values) -> torch.Tensor:
 
 
 def download(t: torch.Tensor) -> np.ndarray:
-    traffic["d2h"] += t.numel() * t.element_size()
-    return t.detach().to("cpu").numpy()
+    """Device tensor -> numpy.  Large results land in a pinned block of torch's
+    caching host allocator (direct DMA instead of the driver's pageable staging
+    path); the returned array is a view that keeps the block alive, and the block
+    goes back to the cache when the caller drops it."""
+    nbytes = t.numel() * t.element_size()
+    traffic["d2h"] += nbytes
+    t = t.detach()
+    if t.is_cuda and nbytes >= (1 << 20):
+        host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        host.copy_(t)
+        return host.numpy()
+    return t.to("cpu").numpy()
 
 
 def ptr(t) -> int:
