@@ -495,17 +495,30 @@ _WS = None
 
 class _ConvTimer:
     """Optional CUDA-event bracketing of every ig_conv_tc launch (bench.py's
-    roofline: per-launch device time on the launching stream)."""
+    roofline: per-launch device time on the launching stream).  Events come
+    from a pool created up front: constructing two torch.cuda.Event objects per
+    launch inside the timed region cost ~1% of the bench step on the host."""
 
     def __init__(self):
         self.on = False
         self.events = []
+        self._pool = []
+        self._next = 0
 
-    def enable(self, stream=None):
-        self.on, self.events = True, []
+    def enable(self, stream=None, reserve=4096):
+        while len(self._pool) < reserve:
+            self._pool.append(torch.cuda.Event(enable_timing=True))
+        self.on, self.events, self._next = True, [], 0
+
+    def pair(self):
+        if self._next + 2 > len(self._pool):
+            self._pool.extend(torch.cuda.Event(enable_timing=True) for _ in range(256))
+        a, b = self._pool[self._next], self._pool[self._next + 1]
+        self._next += 2
+        return a, b
 
     def disable(self):
-        self.on, self.events = False, []
+        self.on, self.events, self._next = False, [], 0
 
     def collect(self):
         torch.cuda.synchronize()
@@ -522,8 +535,7 @@ def conv_launch(p: ConvParams):
     if nbytes and (_WS is None or _WS.numel() < nbytes):
         _WS = torch.empty(nbytes, dtype=torch.uint8, device=dev.device())
     if TIMING.on:
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
+        a, b = TIMING.pair()
         a.record()
     check(lib().ig_conv_tc(p, dev.ptr(_WS) if nbytes else None, dev.stream_ptr()), "ig_conv_tc")
     if TIMING.on:
@@ -535,8 +547,7 @@ def attn_launch(fn):
     """Attention kernels under the same per-launch event timer as the convs
     (bench.py's tensor-core roofline covers both)."""
     if TIMING.on:
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
+        a, b = TIMING.pair()
         a.record()
     fn()
     if TIMING.on:
