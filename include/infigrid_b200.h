@@ -222,6 +222,11 @@ size_t ig_conv_workspace_bytes(void);
 /* 0: automatic; 1: force the per-tap kernel; 2: halo kernel instead of the row ring */
 int ig_conv_set_variant(int force_per_tap);
 int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream);
+/* The EDM2 attention block's q / k / v 1x1 projections in one launch: wgt =
+ * [3 cout][ca] bf16 (rows q | k | v), out0 = q (head_scale applied), k_out, v_out
+ * (v as f16); head_norm must be 1, cout 256, taps 1.  Same results as three
+ * ig_conv_tc calls with head_norm 1 / 1 / 2 (bit-identical). */
+int ig_conv_qkv(const ig_conv_params_t* p, void* k_out, void* v_out, void* cuda_stream);
 /* UNet helpers (NHWC bf16 activations):
  * ig_unet_gather_input: tap-packed stem input [n][w][w][cin_pad] from window
  *   crops (+ renoise, conditioning planes, mask, constant plane) and x_noisy;

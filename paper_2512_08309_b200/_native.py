@@ -64,6 +64,7 @@ SIGNATURES = {
     "ig_conv_workspace_bytes": [],
     "ig_conv_set_variant": [I32],
     "ig_conv_tc": [POINTER(ConvParams), V, V],
+    "ig_conv_qkv": [POINTER(ConvParams), V, V, V],
     "ig_conv_simt": [POINTER(ConvParams), V],
     "ig_unet_gather_input": [V, I32, I64, I64, I32, I32, I32, V, I32, V, I64, I64, I32, I32,
                              I32, I32, I32, U64, U64, U32, F32, F32, I32, V, I32, I32, I32, V,

@@ -218,6 +218,8 @@ struct ConvArgs {
   int pool_gut;           // pooled tensors in the gutter layout
   int head_norm;          // out0 = head_scale * unit-RMS per 64-channel head (attention q/k/v)
   float head_scale;
+  int groups;             // conv_tc_kernel: 1, or 3 = fused q / k / v (weights [3 cout][K],
+  __nv_bfloat16* outg[3]; //   group g -> outg[g]; q: head_scale, v: f16; see ig_conv_qkv)
   const __nv_bfloat16* skip_a;
   const __nv_bfloat16* skip_b;
   const __nv_bfloat16* wskip;
@@ -531,7 +533,12 @@ __global__ void __launch_bounds__(320, 1)
       // ---------------- TMA producer ----------------
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x) {
+      const int total = args.num_tiles * args.groups;
+      for (int gt = blockIdx.x; gt < total; gt += gridDim.x) {
+        // groups > 1: the groups of one pixel tile are consecutive work items,
+        // so concurrently running CTAs read its A boxes from L2
+        const int tile = gt / args.groups;
+        const int wrow = (gt - tile * args.groups) * N;
         const int img = tile / args.tiles_per_img;
         const int r = tile - img * args.tiles_per_img;
         int x0, y0;
@@ -558,7 +565,7 @@ __global__ void __launch_bounds__(320, 1)
               tma_load_4d(a_dst, &map_b, &full[stage], (kc - args.kchunks_a) * 64, x0 + dx,
                           y0 + dy, img);
             const int kglob = tap * (args.ca + args.cb) + kc * 64;
-            tma_load_2d(sB + stage * Cfg::B_BYTES, &map_w, &full[stage], kglob, 0);
+            tma_load_2d(sB + stage * Cfg::B_BYTES, &map_w, &full[stage], kglob, wrow);
           } else {
             const int ks = kb - kmain;   // skip chunk: centre tap of the skip sources
             if (ks < args.kskip_a)
@@ -581,7 +588,8 @@ __global__ void __launch_bounds__(320, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+      const int total = args.num_tiles * args.groups;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -616,13 +624,24 @@ __global__ void __launch_bounds__(320, 1)
     constexpr int NC = N >= 64 ? N / 2 : N;
     const float* sc = args.scale ? s_scale : nullptr;
     int it = 0;
-    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+    const int total = args.num_tiles * args.groups;
+    for (int gt = blockIdx.x; gt < total; gt += gridDim.x, ++it) {
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
+      const int tile = gt / args.groups;
       const int64_t p = (int64_t)tile * 128 + m;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * N;
-      if (N >= 64 || half == 0) epi_span<NC>(args, sc, p, half * NC, taddr);
+      if (args.groups > 1) {
+        const int g = gt - tile * args.groups;
+        ConvArgs ga = args;
+        ga.out0 = args.outg[g];
+        ga.head_norm = g == 2 ? 2 : 1;
+        ga.head_scale = g == 0 ? args.head_scale : 1.f;
+        epi_span<NC>(ga, sc, p, half * NC, taddr);
+      } else if (N >= 64 || half == 0) {
+        epi_span<NC>(args, sc, p, half * NC, taddr);
+      }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
@@ -2843,8 +2862,8 @@ static int make_act_map(CUtensorMap* m, const void* base, int n, int h, int w, i
   return make_act_map_box(m, base, n, h, w, c, bw, bh);
 }
 
-static int make_w_map(CUtensorMap* m, const void* base, int ktot, int cout) {
-  cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)cout};
+static int make_w_map(CUtensorMap* m, const void* base, int ktot, int cout, int groups = 1) {
+  cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)cout * groups};
   cuuint64_t strides[1] = {(cuuint64_t)ktot * 2};
   cuuint32_t box[2] = {64, (cuuint32_t)cout};
   cuuint32_t es[2] = {1, 1};
@@ -2871,7 +2890,7 @@ static int launch_conv_tc(const ig_conv_params_t* p, const ConvArgs& a, cudaStre
   } else {
     mb = ma;
   }
-  if (make_w_map(&mw, p->wgt, p->taps * (p->ca + p->cb), p->cout) != IG_OK) {
+  if (make_w_map(&mw, p->wgt, p->taps * (p->ca + p->cb), p->cout, a.groups) != IG_OK) {
     set_error("ig_conv_tc: cuTensorMapEncodeTiled(weights) failed");
     return IG_ERR_CUDA;
   }
@@ -2889,7 +2908,8 @@ static int launch_conv_tc(const ig_conv_params_t* p, const ConvArgs& a, cudaStre
     cudaFuncSetAttribute(conv_tc_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr_set = true;
   }
-  const int grid = a.num_tiles < kNumSMs ? a.num_tiles : kNumSMs;
+  const int work = a.num_tiles * a.groups;
+  const int grid = work < kNumSMs ? work : kNumSMs;
   { conv_tc_kernel<N><<<grid, 320, Cfg::SMEM, st>>>(ma, mb, mw, msa, msb, mws, a); note_launch(); }
   return cuda_check("ig_conv_tc");
 }
@@ -3167,6 +3187,8 @@ static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   a->head_norm = p->head_norm;
   IG_REQUIRE(p->head_norm >= 0 && p->head_norm <= 2, "conv: head_norm must be 0, 1 or 2");
   a->head_scale = p->head_scale;
+  a->groups = 1;
+  a->outg[0] = a->outg[1] = a->outg[2] = nullptr;
   IG_REQUIRE(!p->head_norm || (p->cout % 128 == 0 && !p->res && !p->out1 && !p->up2 &&
                                !p->pool0 && !(p->gutter & 1)),
              "conv: head_norm needs cout %% 128 == 0, out0 only, no residual / pool / gutter");
@@ -3295,6 +3317,31 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
       set_error("ig_conv_tc: unsupported cout %d", p->cout);
       return IG_ERR_UNSUPPORTED;
   }
+}
+
+// The attention block's three 1x1 projections as ONE launch: p->wgt holds
+// [3 cout][ca] (rows q | k | v), p->out0 receives q, k_out / v_out k and v;
+// p->head_scale applies to q, v is written as f16.  Per pixel tile the three
+// groups are consecutive work items of the persistent grid (3x the tiles of
+// one projection: fewer wave-quantisation tails and one prologue instead of
+// three); bit-identical to three ig_conv_tc calls with head_norm 1 / 1 / 2.
+int ig_conv_qkv(const ig_conv_params_t* p, void* k_out, void* v_out, void* cuda_stream) {
+  ConvArgs a;
+  int rc = conv_args(p, &a, true);
+  if (rc) return rc;
+  IG_REQUIRE(p->taps == 1 && p->cb == 0 && p->csa == 0 && p->up_in == 0 && !p->gutter &&
+                 !p->scale && !p->bias && p->cout == 256 && p->out0 && k_out && v_out,
+             "ig_conv_qkv: 1x1 conv, cout 256, no bias / scale / skip / gutter, three outputs");
+  IG_REQUIRE(p->head_norm == 1, "ig_conv_qkv: head_norm must be 1 (q and k; v is f16)");
+  if (!encode_fn()) {
+    set_error("ig_conv_qkv: cuTensorMapEncodeTiled unavailable");
+    return IG_ERR_CUDA;
+  }
+  a.groups = 3;
+  a.outg[0] = reinterpret_cast<__nv_bfloat16*>(p->out0);
+  a.outg[1] = reinterpret_cast<__nv_bfloat16*>(k_out);
+  a.outg[2] = reinterpret_cast<__nv_bfloat16*>(v_out);
+  return launch_conv_tc<256>(p, a, reinterpret_cast<cudaStream_t>(cuda_stream));
 }
 
 int ig_conv_simt(const ig_conv_params_t* p, void* cuda_stream) {

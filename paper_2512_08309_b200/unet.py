@@ -53,6 +53,7 @@ FUSED_GUTTER = True          # narrow levels (w <= 64) in the gutter layout (1-D
 # the MMAs, is then the per-tile critical path (a second round of tanh /
 # shuffles / stores per column pair), which costs more than the pool kernel.
 FUSED_POOL = False
+FUSED_QKV = True             # attention q / k / v projections as one ig_conv_qkv launch
 
 
 @dataclass(frozen=True)
@@ -361,13 +362,19 @@ class UNetDevice:
         q, k, v = (torch.empty_like(x) for _ in range(3))
         # the conv epilogues normalise each 64-channel head (q also carries the
         # softmax scale 1/8 * log2 e), so the attention kernel reads them as is
-        for j, dst in enumerate((q, k, v)):
-            p = ConvParams(n, h, w, c, 0, c, 1, x.data_ptr(), None,
-                           wq.data_ptr() + j * c * c * 2, None, None, None, 0.0, 1.0, 1.0,
-                           dst.data_ptr(), None)
-            p.head_norm = 2 if j == 2 else 1          # v in f16 (the PV MMA's operand)
-            p.head_scale = Q_SCALE if j == 0 else 1.0
-            conv_launch(p)
+        if FUSED_QKV and c == 256:                      # one launch, 3x the work items
+            p = ConvParams(n, h, w, c, 0, c, 1, x.data_ptr(), None, wq.data_ptr(), None, None,
+                           None, 0.0, 1.0, 1.0, q.data_ptr(), None)
+            p.head_norm, p.head_scale = 1, Q_SCALE
+            conv_launch(p, qkv=(k, v))
+        else:
+            for j, dst in enumerate((q, k, v)):
+                p = ConvParams(n, h, w, c, 0, c, 1, x.data_ptr(), None,
+                               wq.data_ptr() + j * c * c * 2, None, None, None, 0.0, 1.0, 1.0,
+                               dst.data_ptr(), None)
+                p.head_norm = 2 if j == 2 else 1      # v in f16 (the PV MMA's operand)
+                p.head_scale = Q_SCALE if j == 0 else 1.0
+                conv_launch(p)
         y = torch.empty_like(x)
         st = dev.stream_ptr()
         attn_launch(lambda: call("ig_attention", q.data_ptr(), k.data_ptr(), v.data_ptr(), n,
@@ -529,7 +536,8 @@ class _ConvTimer:
 TIMING = _ConvTimer()
 
 
-def conv_launch(p: ConvParams):
+def conv_launch(p: ConvParams, qkv=None):
+    """ig_conv_tc(p); qkv = (k, v): ig_conv_qkv (p.out0 = q, weights [3c][c])."""
     global _WS
     nbytes = int(lib().ig_conv_workspace_bytes())
     if nbytes and (_WS is None or _WS.numel() < nbytes):
@@ -537,7 +545,12 @@ def conv_launch(p: ConvParams):
     if TIMING.on:
         a, b = TIMING.pair()
         a.record()
-    check(lib().ig_conv_tc(p, dev.ptr(_WS) if nbytes else None, dev.stream_ptr()), "ig_conv_tc")
+    if qkv is not None:
+        check(lib().ig_conv_qkv(p, qkv[0].data_ptr(), qkv[1].data_ptr(), dev.stream_ptr()),
+              "ig_conv_qkv")
+    else:
+        check(lib().ig_conv_tc(p, dev.ptr(_WS) if nbytes else None, dev.stream_ptr()),
+              "ig_conv_tc")
     if TIMING.on:
         b.record()
         TIMING.events.append((a, b))

@@ -678,3 +678,37 @@ def test_unet_with_attention_vs_fp32_oracle(win, nwin):
     rms = float(np.sqrt(np.mean((got - want) ** 2))) / std
     mx = float(np.abs(got - want).max()) / std
     assert rms < UNET_RMS_TOL and mx < UNET_MAX_TOL, (rms, mx)
+
+
+@pytest.mark.parametrize("n,h,w", [(2, 32, 32), (3, 16, 16), (1, 8, 16)])
+def test_conv_qkv_fused_equals_three_launches(n, h, w):
+    """ig_conv_qkv (one launch, groups q | k | v) is bit-identical to three
+    ig_conv_tc launches with head_norm 1 / 1 / 2 (same MMAs, same epilogue)."""
+    c = 256
+    g = torch.Generator(device=DEV).manual_seed(n * 100 + h)
+    x = torch.randn(n, h, w, c, device=DEV, generator=g).bfloat16()
+    wq = (torch.randn(3 * c, c, device=DEV, generator=g) / 16).bfloat16()
+    st = torch.cuda.current_stream().cuda_stream
+    sep = [torch.empty_like(x) for _ in range(3)]
+    for j, dst in enumerate(sep):
+        p = ConvParams(n, h, w, c, 0, c, 1, x.data_ptr(), None, wq.data_ptr() + j * c * c * 2,
+                       None, None, None, 0.0, 1.0, 1.0, dst.data_ptr(), None)
+        p.head_norm = 2 if j == 2 else 1
+        p.head_scale = unet.Q_SCALE if j == 0 else 1.0
+        check(lib().ig_conv_tc(p, None, st), "ig_conv_tc")
+    fused = [torch.empty_like(x) for _ in range(3)]
+    p = ConvParams(n, h, w, c, 0, c, 1, x.data_ptr(), None, wq.data_ptr(), None, None, None,
+                   0.0, 1.0, 1.0, fused[0].data_ptr(), None)
+    p.head_norm, p.head_scale = 1, unet.Q_SCALE
+    check(lib().ig_conv_qkv(p, fused[1].data_ptr(), fused[2].data_ptr(), st), "ig_conv_qkv")
+    torch.cuda.synchronize()
+    for a, b in zip(sep, fused):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    # and the values are the normalised projections (fp32 torch reference)
+    y = x.float().reshape(-1, c) @ wq.float().t()
+    qn = y[:, :c].reshape(-1, 4, 64)
+    qn = qn / (1e-4 + qn.norm(dim=-1, keepdim=True) / 8.0) * unet.Q_SCALE
+    assert (fused[0].float().reshape(-1, 4, 64) - qn).abs().max().item() < 3e-2
+    # wrong arguments fail loudly
+    p.head_norm = 2
+    assert lib().ig_conv_qkv(p, fused[1].data_ptr(), fused[2].data_ptr(), st) != 0

@@ -57,8 +57,11 @@ def layer_ops(cfg, win):
             c = c2.cout
         elif op[0] == "attn":
             nm = op[1]
-            for j in "qkv":
-                seq.append(("conv", f"{nm}.{j}", h, c, c, 1, 1, 0))
+            if unet.FUSED_QKV and c == 256:          # one ig_conv_qkv launch
+                seq.append(("conv", nm + ".qkv", h, c, 3 * c, 1, 1, 0))
+            else:
+                for j in "qkv":
+                    seq.append(("conv", f"{nm}.{j}", h, c, c, 1, 1, 0))
             seq.append(("attn", nm + ".attn", h, c, 0, 0, 0, 0))
             seq.append(("conv", nm + ".proj", h, c, c, 1, 2, 1))
         elif op[0] == "down":
