@@ -2453,6 +2453,9 @@ struct AttnSmem {
 // sequence, Q and the O accumulator are double-buffered per item, so the next
 // item's loads and MMAs overlap the previous item's epilogue.
 constexpr int ATT_NG = 4;                            // softmax warp groups (32 keys each)
+#ifndef ATT_PV_N
+#define ATT_PV_N 80                                  // PV MMA width: 64 dims + ones columns
+#endif
 
 __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
     const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
@@ -2549,8 +2552,10 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     constexpr uint32_t idesc_s = idesc_bf16(128, 128);
-    // f16 A (P) and B (V, MN-major), f32 accumulate, N = 64 dims + 64 ones
-    constexpr uint32_t idesc_o = (1u << 4) | (1u << 16) | ((uint32_t)(128 >> 3) << 17) |
+    // f16 A (P) and B (V, MN-major), f32 accumulate, N = 64 dims + 16 ones: the
+    // denominator needs one column, N = 80 is the narrowest legal M=128 shape past
+    // 64 (N = 128 spent 37.5% of the PV MMA cycles on 48 duplicate sums)
+    constexpr uint32_t idesc_o = (1u << 4) | (1u << 16) | ((uint32_t)(ATT_PV_N >> 3) << 17) |
                                  ((uint32_t)(128 >> 4) << 24);
     auto issue_s = [&](int t, int it, int j) {
       const int qb = it & 1;
