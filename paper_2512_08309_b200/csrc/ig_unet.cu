@@ -3226,7 +3226,8 @@ size_t ig_conv_workspace_bytes(void) { return 0; }
 // 0: automatic; 1: per-tap kernel only; 2: halo kernel instead of the row
 // ring; 3: one-CTA halo kernel instead of CTA pairs; 4: CTA pairs with three
 // halo buffers; 5: two-row instead of four-row CTA-pair tiles for cout 64;
-// 6: separate skip-chunk ring (tests / A-B timing)
+// 6: separate skip-chunk ring; 15: two-row tiles for the single-chunk cout 64
+// layers (tests / A-B timing)
 int ig_conv_set_variant(int variant) {
   g_variant = variant;
   return IG_OK;
@@ -3269,10 +3270,13 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
     }
   }
   if (pair) {   // measured faster than the row ring too (r01: enc0.0.c1 395 vs 446 us)
-    // cout 64: 4-row tiles (a 6 x 130 halo box feeds 144 MMAs) for the
-    // multi-chunk layers (r01: dec0.0.c1 976 -> 707 us); single-chunk layers
-    // measured marginally faster with 2-row tiles
-    const bool deep = a.kchunks_a + a.kchunks_b >= 2 || a.kskip_a + a.kskip_b >= 3;
+    // cout 64: 4-row tiles (a 6 x 130 halo box feeds 144 MMAs; r01: dec0.0.c1
+    // 976 -> 707 us), since the halo L2 prefetch also for the single-chunk layers
+    // (enc0.0.c1 347 -> 324, enc0.0.c2 418 -> 389, dec0.1.c2 548 -> 493 us per
+    // 64 windows).  Variant 15: the earlier rule, four rows only for the
+    // multi-chunk layers.
+    const bool deep = g_variant != 15 || a.kchunks_a + a.kchunks_b >= 2 ||
+                      a.kskip_a + a.kskip_b >= 3;
     if (p->cout == 64 && deep && p->h % 4 == 0 && g_variant != 5 &&
         ((int64_t)p->n * (p->w / 128) * (p->h / 4)) % 2 == 0)
       return launch_conv_halo2<64, 4, false>(p, a, st);
