@@ -18,9 +18,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--windows", type=int, default=64)
 ap.add_argument("--full", action="store_true")
 ap.add_argument("--variant", type=int, default=0, help="ig_conv_set_variant (A/B timing)")
+ap.add_argument("--fused-pool", action="store_true", help="unet.FUSED_POOL = True (A/B timing)")
 args = ap.parse_args()
 from paper_2512_08309_b200._native import check, lib  # noqa: E402
 check(lib().ig_conv_set_variant(args.variant))
+unet.FUSED_POOL = unet.FUSED_POOL or args.fused_pool
 cfg = unet.UNetConfig()
 if args.full:
     scfg = ig.SamplerConfig(steps=2, layout=WindowLayout(256, 128), seed=0,
