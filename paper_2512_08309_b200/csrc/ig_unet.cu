@@ -161,6 +161,29 @@ __device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t* r) {
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// D += A * B with A read from TMEM (M = 128 lanes, K-major, 2 f16 per column)
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 
 // K-major operand tile in SMEM written by TMA with SWIZZLE_128B: rows of 128 B
 // (64 bf16), 8-row (1024 B) swizzle atoms stacked along M/N.
@@ -2457,6 +2480,9 @@ constexpr int ATT_NG = 4;                            // softmax warp groups (32 
 #define ATT_PV_N 80                                  // PV MMA width: 64 dims + ones columns
 #endif
 
+// PT: P = 2^s goes back into the S buffer's TMEM columns (tcgen05.st) and the PV
+// MMA reads it as a TMEM A operand; else P is staged in SMEM (st.shared, SW128).
+template <bool PT>
 __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
     const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
     const __grid_constant__ CUtensorMap map_v, int n, int hw, int heads,
@@ -2495,7 +2521,7 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
     prefetch_map(&map_v);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sfull[s], 1);
-      mbar_init(&sempty[s], 128 * ATT_NG);
+      mbar_init(&sempty[s], PT ? 1 : 128 * ATT_NG);   // PT: released by the PV MMA
       mbar_init(&qfull[s], 1);
       mbar_init(&qempty[s], 1);
       mbar_init(&kfull[s], 1);
@@ -2585,7 +2611,21 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
       mbar_wait(&vfull[ps], ph);
       mbar_wait(&pfull[ps], ph);
       tc_fence_after();
-      if (elect_one()) {
+      if (PT && elect_one()) {
+        // P of keys [32g, 32g+32) sits in S columns [32g, 32g+16) (2 f16 per column)
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t vaddr = smem_u32(sm + AttnSmem::V0 + ps * 16384 + (kk * 16) * 128);
+          const uint32_t lbo = (uint32_t)(AttnSmem::ONES - (AttnSmem::V0 + ps * 16384));
+          const uint64_t vdesc = (smem_desc_sw128_mn(vaddr) & ~(0x3FFFull << 16)) |
+                                 ((uint64_t)((lbo >> 4) & 0x3FFF) << 16);
+          tc_mma_ts(tmem + 256 + ob * 128, tmem + ps * 128 + 32 * (kk >> 1) + 8 * (kk & 1),
+                    vdesc, idesc_o, (j | kk) ? 1u : 0u);
+        }
+        tc_commit(&sempty[ps]);
+        tc_commit(&vempty[ps]);
+        if (j == ktiles - 1) tc_commit(&ofull[ob]);
+      } else if (!PT && elect_one()) {
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
           const uint64_t pdesc =
@@ -2620,6 +2660,7 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
     // warp group g (4 warps, one per TMEM lane quarter) owns keys [32g, 32g+32)
     // of every tile and dims [16g, 16g+16) of the output
     constexpr int KG = 128 / ATT_NG, DG = 64 / ATT_NG;
+    static_assert(!PT || KG == 32, "TMEM P: one 32x32b.x16 store per group");
     const int quarter = warp & 3;
     const int grp = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;                      // query row == TMEM lane
@@ -2656,8 +2697,10 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
       uint32_t r[KG];
       tmem_ld32_nw(tmem + lanebase + s * 128 + grp * KG, r);
       tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&sempty[s]);
+      if (!PT) {
+        tc_fence_before();
+        mbar_arrive(&sempty[s]);
+      }
       const int kvalid = hw - j * 128 - grp * KG;             // keys of this group in range
       if (kvalid < KG) {                                      // partial last tile: mask
 #pragma unroll
@@ -2668,6 +2711,23 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
       // f32 (ex2.approx.f16x2 is two MUFU ops on sm_100 anyway and would round the
       // argument to f16), stored f16; the row sums come from the ones block of the
       // PV MMA.  r01: half of the exps as an FMA-pipe polynomial measured slower)
+      if (PT) {
+        // this group's own S columns: P of its 32 keys into the first 16 of them
+        uint32_t pw[KG / 2];
+#pragma unroll
+        for (int q2 = 0; q2 < KG / 2; ++q2) {
+          __half2 h = __floats2half2_rn(ex2_approx(__uint_as_float(r[2 * q2])),
+                                        ex2_approx(__uint_as_float(r[2 * q2 + 1])));
+          pw[q2] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        tmem_st16(tmem + lanebase + s * 128 + grp * KG, pw);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&pfull[s]);
+        if (j == 0 && it > 0) item_epilogue(it - 1);
+        if (++j == ktiles) { j = 0; ++it; }
+        continue;
+      }
       mbar_wait(&pempty[s], ph ^ 1);
       // keys [32g, 32g+32): 64-key chunk g/2, 16-byte columns 4*(g%2) .. +3
       uint8_t* pbase = sm + AttnSmem::P0 + s * 32768 + (grp * KG / 64) * 16384;
@@ -3227,7 +3287,7 @@ size_t ig_conv_workspace_bytes(void) { return 0; }
 // ring; 3: one-CTA halo kernel instead of CTA pairs; 4: CTA pairs with three
 // halo buffers; 5: two-row instead of four-row CTA-pair tiles for cout 64;
 // 6: separate skip-chunk ring; 15: two-row tiles for the single-chunk cout 64
-// layers (tests / A-B timing)
+// layers; 16: attention with P staged in SMEM (tests / A-B timing)
 int ig_conv_set_variant(int variant) {
   g_variant = variant;
   return IG_OK;
@@ -3512,12 +3572,15 @@ int ig_attention(const void* q, const void* k, const void* v, int32_t n, int32_t
   const int smem = AttnSmem::BYTES + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attention_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attention_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   const int64_t items = (int64_t)n * heads * ((hw + 127) / 128);
   const int ctas = (int)(items < kNumSMs ? items : kNumSMs);
-  { attention_kernel<<<(unsigned)ctas, 64 + 128 * ATT_NG, smem, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+  // variant 16: P staged through SMEM (the earlier path; A/B and cross-check)
+  auto kern = g_variant == 16 ? attention_kernel<false> : attention_kernel<true>;
+  { kern<<<(unsigned)ctas, 64 + 128 * ATT_NG, smem, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       mq, mk, mv, n, hw, heads, reinterpret_cast<__nv_bfloat16*>(y), c); note_launch(); }
   return cuda_check("ig_attention");
 }

@@ -712,3 +712,26 @@ def test_conv_qkv_fused_equals_three_launches(n, h, w):
     # wrong arguments fail loudly
     p.head_norm = 2
     assert lib().ig_conv_qkv(p, fused[1].data_ptr(), fused[2].data_ptr(), st) != 0
+
+
+@pytest.mark.parametrize("n,hw,c", [(2, 1024, 256), (1, 200, 128)])
+def test_attention_p_in_tmem_matches_smem_path(n, hw, c):
+    """The default attention kernel keeps P in TMEM (tcgen05.st, TS-MMA); variant
+    16 stages P through SMEM.  Same P values and MMAs: the outputs agree."""
+    g = torch.Generator(device=DEV).manual_seed(hw * 3 + c)
+    q, k, v = ((torch.randn(n, hw, c, device=DEV, generator=g) * s).bfloat16()
+               for s in (1.3, 0.7, 1.0))
+    st = torch.cuda.current_stream().cuda_stream
+    call("ig_attn_prep", q.data_ptr(), k.data_ptr(), v.data_ptr(), n, hw, c, None, st)
+    ys = []
+    try:
+        for variant in (0, 16):
+            check(lib().ig_conv_set_variant(variant))
+            y = torch.empty(n, hw, c, device=DEV, dtype=torch.bfloat16)
+            call("ig_attention", q.data_ptr(), k.data_ptr(), v.data_ptr(), n, hw, c,
+                 y.data_ptr(), st)
+            ys.append(y.float())
+    finally:
+        check(lib().ig_conv_set_variant(0))
+    torch.cuda.synchronize()
+    assert (ys[0] - ys[1]).abs().max().item() < 1e-2
