@@ -488,6 +488,12 @@ def run_cfg4(args):
     scfg = ig.SamplerConfig(steps=T, layout=WindowLayout(WINDOW, STRIDE), seed=0,
                             denoiser=ig.DenoiserSpec(kind="unet", unet=ucfg), name="stream",
                             cache_limit=args.cache_gb * (1 << 30))
+    from paper_2512_08309_b200 import _device as dev
+    # serving setting: grow the caching allocator to the cache budget plus the
+    # UNet's working set once, so the bounded cache fills from cached segments
+    # (a cudaMalloc mid-query stalled it by 20-45 ms, tools/cfg4_tail.py)
+    limit = args.cache_gb * (1 << 30)
+    dev.reserve(limit + min(limit, 16 << 30))
     state = ig.SamplerState(scfg, ig.TileStore())
     rng = random.Random(0 ^ 0xB1E55ED)
     n = args.queries

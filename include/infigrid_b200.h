@@ -15,7 +15,10 @@
  *   ig_blend               store.py:428-436 _accumulate (+ sampler.py:151-154 W*Phi
  *                          contribution) and store.py:549-554 divide_weighted
  *   ig_box_mean            transforms.py:29-51
- *   ig_block_mean_f64      transforms.py:61-67
+ *   ig_blur_block_mean_f64 transforms.py:54-67 (block_mean of blur3_iterated, float64)
+ *   ig_block_mean          transforms.py:61-67 block_mean (float32 / float64 accumulation)
+ *   ig_upsample_nn         transforms.py:70-72 upsample_nn
+ *   ig_convert             numpy astype at transforms.py:93,101 (dtype-preserving decode)
  *   ig_laplacian_residual  transforms.py:89-95 (high = x - up(low))
  *   ig_laplacian_merge     transforms.py:98-101 / :104-114 (up(low)+high [, signed_square])
  *   ig_signed_pow          transforms.py:17-26
@@ -24,6 +27,8 @@
  *   ig_procedural_map      pipeline.py:101-123 ProceduralMap.values
  *   ig_corrupt             pipeline.py:126-139 corrupt_user_map
  *   ig_raster_map          pipeline.py:72-84 RasterMap.values
+ *   ig_tiles_resolve       store.py:364-426 _gather_tiles + _commit_region of
+ *                          _read_indirect (INDIRECT tile cache in HBM)
  *   ig_unet_*              the Phi plugin (denoise.py:89 apply) for the new "unet" kind;
  *                          no reference implementation exists
  */
@@ -44,6 +49,9 @@ extern "C" {
 
 #define IG_DTYPE_F32 0
 #define IG_DTYPE_F64 1
+#define IG_DTYPE_F16 2   /* storage-only types of the dtype-generic transforms */
+#define IG_DTYPE_I32 3
+#define IG_DTYPE_I64 4
 
 #define IG_PHI_IDENTITY 0
 #define IG_PHI_SHRINK_SMOOTH 1
@@ -116,6 +124,18 @@ int ig_ipc_close(void* base);
 int ig_ipc_alloc(int64_t bytes, void** ptr_out);
 int ig_ipc_free(void* ptr);
 
+/* ---- INDIRECT tile cache (store.py:358-426) ---------------------------------
+ * table[2*(ty*ntx + tx)] = device pointer of tile (tx0+tx, ty0+ty)'s data
+ * (channels, tile_size, tile_size), table[... + 1] its finalized mask
+ * (tile_size^2 bytes, 0/1).  Every tile of the box that the region touches must
+ * exist.  Per pixel of the region (origin rx0, ry0; out is (channels, rh, rw)):
+ * finalized -> out = tile value; otherwise tile = out and the pixel becomes
+ * finalized (the reference's gather of finalized pixels followed by the commit
+ * of the whole region, in one pass).  elem_bytes 4 (float32) or 8 (float64). */
+int ig_tiles_resolve(const int64_t* table, int64_t tx0, int64_t ty0, int32_t ntx, int32_t nty,
+                     int32_t tile_size, int32_t channels, int32_t elem_bytes, int64_t rx0,
+                     int64_t ry0, int32_t rw, int32_t rh, void* out, void* cuda_stream);
+
 /* ---- K6 elevation transforms ---------------------------------------------- */
 int ig_box_mean(const void* in, int32_t planes, int32_t h, int32_t w, int32_t radius,
                 int32_t dtype, void* out, void* cuda_stream);
@@ -128,13 +148,29 @@ int ig_blur_block_mean_f64(const void* in, int32_t in_dtype, int32_t planes, int
 int ig_laplacian_residual(const void* x, int32_t x_dtype, const double* low, int32_t planes,
                           int32_t h, int32_t w, int32_t factor, double* high, void* cuda_stream);
 /* out = cast(up(low) + high) [then signed_square in out dtype when square_out] ;
- * out_dtype F64 keeps the provisional sum (stabilize) */
+ * out_dtype F64 keeps the provisional sum (stabilize); F16/I32/I64 outputs
+ * are laplacian_decode's astype(original dtype) (no square_out) */
 int ig_laplacian_merge(const double* low, const double* high, int32_t planes, int32_t h,
                        int32_t w, int32_t factor, int32_t out_dtype, int32_t square_out,
                        void* out, void* cuda_stream);
-/* op 0: signed_sqrt, 1: signed_square */
+/* op 0: signed_sqrt (F32/F64), 1: signed_square (F32/F64, or I32/I64 with
+ * two's-complement wraparound like numpy's integer multiply) */
 int ig_signed_pow(const void* in, int64_t n, int32_t op, int32_t dtype, void* out,
                   void* cuda_stream);
+/* block_mean (transforms.py:61-67) in the accumulation dtype numpy's .mean
+ * uses (F32 for float32/float16 input, F64 otherwise), numpy's order: for
+ * each of the f block rows the pairwise sum of its f values, added in row
+ * order, then one division by f*f */
+int ig_block_mean(const void* in, int32_t dtype, int32_t planes, int32_t h, int32_t w,
+                  int32_t factor, void* out, void* cuda_stream);
+/* elementwise astype between IG_DTYPE_* codes (exact widenings; RN narrowings;
+ * float -> int truncates) */
+int ig_convert(const void* in, int32_t in_dtype, int64_t n, void* out, int32_t out_dtype,
+               void* cuda_stream);
+/* upsample_nn (transforms.py:70-72): out[p][Y][X] = in[p][Y/f][X/f], any
+ * element size (1/2/4/8 bytes) */
+int ig_upsample_nn(const void* in, int32_t elem_bytes, int64_t planes, int32_t h, int32_t w,
+                   int32_t factor, void* out, void* cuda_stream);
 
 /* ---- K7/K8/K9 hierarchy helpers ----------------------------------------------
  * features over a batch of n elevation tiles [n][h][w] (channel 0 of each

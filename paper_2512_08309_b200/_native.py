@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libinfigrid_b200.so")
 
 IG_OK, IG_ERR_ARG, IG_ERR_CUDA, IG_ERR_UNSUPPORTED = 0, 1, 2, 3
-DTYPE_F32, DTYPE_F64 = 0, 1
+DTYPE_F32, DTYPE_F64, DTYPE_F16, DTYPE_I32, DTYPE_I64 = 0, 1, 2, 3, 4
 PHI_IDENTITY, PHI_SHRINK_SMOOTH, PHI_COND_AFFINE = 0, 1, 2
 
 V, I32, I64, U64, U32, F64, F32 = c_void_p, c_int32, c_int64, c_uint64, c_uint32, c_double, c_float
@@ -56,6 +56,10 @@ SIGNATURES = {
     "ig_laplacian_residual": [V, I32, V, I32, I32, I32, I32, V, V],
     "ig_laplacian_merge": [V, V, I32, I32, I32, I32, I32, I32, V, V],
     "ig_signed_pow": [V, I64, I32, I32, V, V],
+    "ig_block_mean": [V, I32, I32, I32, I32, I32, V, V],
+    "ig_convert": [V, I32, I64, V, I32, V],
+    "ig_upsample_nn": [V, I32, I64, I32, I32, I32, V, V],
+    "ig_tiles_resolve": [V, I64, I64, I32, I32, I32, I32, I32, I64, I64, I32, I32, V, V],
     "ig_patch_features": [V, I64, I32, I32, I32, I32, I32, I32, V, V],
     "ig_condition_window": [V, I64, I64, I32, I32, I32, I32, I32, U64, V, I32, I32, I32, V, V, V],
     "ig_procedural_map": [U64, U32, I32, I64, I64, I32, I32, I32, V, V],

@@ -10,6 +10,8 @@
 #include <cstring>
 
 #include <cuda.h>
+#include <cuda_fp16.h>
+#include <type_traits>
 
 #include "ig_common.cuh"
 #include "ig_noise.cuh"
@@ -599,8 +601,9 @@ __device__ T np_pairwise(const F& v, int s, int n) {
 // numpy order for .mean(axis=(-3,-1)) of the (h/f, f, w/f, f) view: for each
 // of the f block rows (outer, sequential, starting from 0) add the pairwise
 // sum of that row's f values; then divide by f*f.
-__global__ void block_mean_f64_kernel(const double* __restrict__ in, int planes, int h, int w,
-                                      int f, double* __restrict__ low) {
+template <typename T>
+__global__ void block_mean_kernel(const T* __restrict__ in, int planes, int h, int w, int f,
+                                  T* __restrict__ low) {
   const int lh = h / f, lw = w / f;
   const int64_t total = (int64_t)planes * lh * lw;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -608,13 +611,13 @@ __global__ void block_mean_f64_kernel(const double* __restrict__ in, int planes,
     const int64_t pl = idx / ((int64_t)lh * lw);
     const int rem = (int)(idx - pl * lh * lw);
     const int by = rem / lw, bx = rem - by * lw;
-    const double* P = in + pl * h * w + (int64_t)(by * f) * w + bx * f;
-    double s = 0.0;
+    const T* P = in + pl * h * w + (int64_t)(by * f) * w + bx * f;
+    T s = (T)0;
     for (int r = 0; r < f; ++r) {
-      const double* row = P + (int64_t)r * w;
-      s = radd(s, np_pairwise<double>([&](int i) { return row[i]; }, 0, f));
+      const T* row = P + (int64_t)r * w;
+      s = radd(s, np_pairwise<T>([&](int i) { return row[i]; }, 0, f));
     }
-    low[idx] = rdiv(s, (double)(f * f));
+    low[idx] = rdiv(s, (T)(f * f));
   }
 }
 
@@ -713,6 +716,28 @@ __global__ void __launch_bounds__(256) laplacian_residual_rows_kernel(
   }
 }
 
+// element conversions: exact widenings (f16/f32/ints -> f64, f16 -> f32) and the
+// round-to-nearest narrowings numpy's astype performs (f32 -> f16, f64 -> f32);
+// float -> int truncates toward zero like numpy's C cast
+template <typename TO, typename TI>
+__device__ __forceinline__ TO convert_elem(TI v) {
+  if constexpr (std::is_same<TI, __half>::value) {
+    return convert_elem<TO>(__half2float(v));
+  } else if constexpr (std::is_same<TO, __half>::value) {
+    if constexpr (std::is_same<TI, double>::value) return __double2half(v);
+    else return __float2half_rn((float)v);
+  } else {
+    return (TO)v;
+  }
+}
+
+template <typename TO, typename TI>
+__global__ void convert_kernel(const TI* __restrict__ in, int64_t n, TO* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = convert_elem<TO>(in[i]);
+}
+
 template <typename TO>
 __global__ void __launch_bounds__(256) laplacian_merge_rows_kernel(
     const double* __restrict__ low, const double* __restrict__ high, int planes, int h, int w,
@@ -733,13 +758,47 @@ __global__ void __launch_bounds__(256) laplacian_merge_rows_kernel(
     for (int e = 0; e < 4; ++e) {
       const int xx = blockIdx.x * 1024 + e * 256 + threadIdx.x;
       if (xx >= w) continue;
-      TO v = (TO)radd(lrow[sh >= 0 ? xx >> sh : xx / f], hv[e]);
-      if (square_out) {
-        const TO sg = v > (TO)0 ? (TO)1 : (v < (TO)0 ? (TO)-1 : (v == (TO)0 ? (TO)0 : v));
-        v = rmul(rmul(sg, v), v);
+      const double sum = radd(lrow[sh >= 0 ? xx >> sh : xx / f], hv[e]);
+      if constexpr (std::is_floating_point<TO>::value) {
+        TO v = (TO)sum;
+        if (square_out) {
+          const TO sg = v > (TO)0 ? (TO)1 : (v < (TO)0 ? (TO)-1 : (v == (TO)0 ? (TO)0 : v));
+          v = rmul(rmul(sg, v), v);
+        }
+        out[base + xx] = v;
+      } else {
+        out[base + xx] = convert_elem<TO>(sum);   // astype(original dtype)
       }
-      out[base + xx] = v;
     }
+  }
+}
+
+// nearest-neighbour replication on the last two axes (transforms.py:70-72),
+// element-size generic: one thread per output element of a row segment
+template <typename E>
+__global__ void upsample_nn_kernel(const E* __restrict__ in, int64_t planes, int h, int w, int f,
+                                   E* __restrict__ out) {
+  const int64_t W = (int64_t)w * f;
+  const int64_t total = planes * h * f * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / W;                 // plane * (h*f) + Y
+    const int64_t X = i - row * W;
+    const int64_t pl = row / ((int64_t)h * f);
+    const int64_t Y = row - pl * h * f;
+    out[i] = in[(pl * h + Y / f) * w + X / f];
+  }
+}
+
+template <typename T>
+__global__ void signed_square_int_kernel(const T* __restrict__ in, int64_t n, T* __restrict__ out) {
+  // np.sign(x) * x * x in the integer dtype (two's-complement wraparound)
+  using U = typename std::make_unsigned<T>::type;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T v = in[i];
+    const T sg = v > 0 ? (T)1 : (v < 0 ? (T)-1 : (T)0);
+    out[i] = (T)((U)((U)sg * (U)v) * (U)v);
   }
 }
 
@@ -879,6 +938,20 @@ __global__ void raster_map_kernel(const float* __restrict__ raster, int rc, int 
       Y = pymod(Y, rh);
     }
     out[idx] = raster[((int64_t)c * rh + Y) * rw + X];
+  }
+}
+
+// element-type dispatch for the dtype-generic transforms: calls f(T{}) with
+// the C++ type of an IG_DTYPE_* code; returns false for an unknown code
+template <typename F>
+static bool with_dtype(int32_t dtype, F&& f) {
+  switch (dtype) {
+    case IG_DTYPE_F32: f(float{}); return true;
+    case IG_DTYPE_F64: f(double{}); return true;
+    case IG_DTYPE_F16: f(__half{}); return true;
+    case IG_DTYPE_I32: f(int32_t{}); return true;
+    case IG_DTYPE_I64: f(int64_t{}); return true;
+    default: return false;
   }
 }
 
@@ -1089,7 +1162,7 @@ int ig_blur_block_mean_f64(const void* in, int32_t in_dtype, int32_t planes, int
     double* t = a; a = b; b = t;
   }
   const int64_t lt = total / ((int64_t)factor * factor);
-  { block_mean_f64_kernel<<<grid_for(lt, 256), 256, 0, st>>>(a, planes, h, w, factor, low); note_launch(); }
+  { block_mean_kernel<double><<<grid_for(lt, 256), 256, 0, st>>>(a, planes, h, w, factor, low); note_launch(); }
   return cuda_check("ig_blur_block_mean_f64");
 }
 
@@ -1112,31 +1185,90 @@ int ig_laplacian_residual(const void* x, int32_t x_dtype, const double* low, int
 int ig_laplacian_merge(const double* low, const double* high, int32_t planes, int32_t h,
                        int32_t w, int32_t factor, int32_t out_dtype, int32_t square_out,
                        void* out, void* cuda_stream) {
+  IG_REQUIRE(!square_out || out_dtype == IG_DTYPE_F32 || out_dtype == IG_DTYPE_F64,
+             "laplacian_merge: signed-square output needs a float32/float64 dtype");
   if ((int64_t)planes * h * w == 0) return IG_OK;
-  {
-    const dim3 grid((unsigned)((w + 1023) / 1024),
-                    (unsigned)((int64_t)planes * h < 65535 ? (int64_t)planes * h : 65535));
-    if (out_dtype == IG_DTYPE_F32)
-      { laplacian_merge_rows_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-          low, high, planes, h, w, factor, square_out, (float*)out); note_launch(); }
-    else
-      { laplacian_merge_rows_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
-          low, high, planes, h, w, factor, square_out, (double*)out); note_launch(); }
-    return cuda_check("ig_laplacian_merge");
-  }
+  const dim3 grid((unsigned)((w + 1023) / 1024),
+                  (unsigned)((int64_t)planes * h < 65535 ? (int64_t)planes * h : 65535));
+  const bool ok = with_dtype(out_dtype, [&](auto tag) {
+    using TO = decltype(tag);
+    laplacian_merge_rows_kernel<TO><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        low, high, planes, h, w, factor, square_out, (TO*)out);
+    note_launch();
+  });
+  IG_REQUIRE(ok, "laplacian_merge: unknown dtype %d", out_dtype);
+  return cuda_check("ig_laplacian_merge");
 }
 
 int ig_signed_pow(const void* in, int64_t n, int32_t op, int32_t dtype, void* out,
                   void* cuda_stream) {
+  IG_REQUIRE(op == 0 || op == 1, "signed_pow: op must be 0 (sqrt) or 1 (square)");
   if (n <= 0) return IG_OK;
   const int grid = grid_for(n, 256);
+  cudaStream_t st = as_stream(cuda_stream);
   if (dtype == IG_DTYPE_F32)
-    { signed_pow_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>((const float*)in, n, op,
-                                                                       (float*)out); note_launch(); }
+    { signed_pow_kernel<float><<<grid, 256, 0, st>>>((const float*)in, n, op, (float*)out); note_launch(); }
+  else if (dtype == IG_DTYPE_F64)
+    { signed_pow_kernel<double><<<grid, 256, 0, st>>>((const double*)in, n, op, (double*)out); note_launch(); }
+  else if (op == 1 && dtype == IG_DTYPE_I32)
+    { signed_square_int_kernel<int32_t><<<grid, 256, 0, st>>>((const int32_t*)in, n, (int32_t*)out); note_launch(); }
+  else if (op == 1 && dtype == IG_DTYPE_I64)
+    { signed_square_int_kernel<int64_t><<<grid, 256, 0, st>>>((const int64_t*)in, n, (int64_t*)out); note_launch(); }
   else
-    { signed_pow_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>((const double*)in, n, op,
-                                                                        (double*)out); note_launch(); }
+    IG_REQUIRE(false, "signed_pow: op %d undefined for dtype %d", op, dtype);
   return cuda_check("ig_signed_pow");
+}
+
+int ig_block_mean(const void* in, int32_t dtype, int32_t planes, int32_t h, int32_t w,
+                  int32_t factor, void* out, void* cuda_stream) {
+  IG_REQUIRE(factor >= 1 && h % factor == 0 && w % factor == 0,
+             "spatial dims %dx%d not divisible by factor %d", h, w, factor);
+  IG_REQUIRE(dtype == IG_DTYPE_F32 || dtype == IG_DTYPE_F64,
+             "block_mean: accumulation dtype must be float32 or float64");
+  const int64_t lt = (int64_t)planes * (h / factor) * (w / factor);
+  if (lt == 0) return IG_OK;
+  if (dtype == IG_DTYPE_F32)
+    { block_mean_kernel<float><<<grid_for(lt, 256), 256, 0, as_stream(cuda_stream)>>>(
+        (const float*)in, planes, h, w, factor, (float*)out); note_launch(); }
+  else
+    { block_mean_kernel<double><<<grid_for(lt, 256), 256, 0, as_stream(cuda_stream)>>>(
+        (const double*)in, planes, h, w, factor, (double*)out); note_launch(); }
+  return cuda_check("ig_block_mean");
+}
+
+int ig_convert(const void* in, int32_t in_dtype, int64_t n, void* out, int32_t out_dtype,
+               void* cuda_stream) {
+  if (n <= 0) return IG_OK;
+  const int grid = grid_for(n, 256);
+  bool ok_out = false;
+  const bool ok_in = with_dtype(in_dtype, [&](auto ti) {
+    using TI = decltype(ti);
+    ok_out = with_dtype(out_dtype, [&](auto to) {
+      using TO = decltype(to);
+      convert_kernel<TO, TI><<<grid, 256, 0, as_stream(cuda_stream)>>>((const TI*)in, n, (TO*)out);
+      note_launch();
+    });
+  });
+  IG_REQUIRE(ok_in && ok_out, "convert: unknown dtype pair %d -> %d", in_dtype, out_dtype);
+  return cuda_check("ig_convert");
+}
+
+int ig_upsample_nn(const void* in, int32_t elem_bytes, int64_t planes, int32_t h, int32_t w,
+                   int32_t factor, void* out, void* cuda_stream) {
+  IG_REQUIRE(factor >= 1, "upsample_nn: factor must be >= 1");
+  const int64_t total = planes * h * factor * (int64_t)w * factor;
+  if (total == 0) return IG_OK;
+  const int grid = grid_for(total, 256);
+  cudaStream_t st = as_stream(cuda_stream);
+  switch (elem_bytes) {
+    case 1: upsample_nn_kernel<uint8_t><<<grid, 256, 0, st>>>((const uint8_t*)in, planes, h, w, factor, (uint8_t*)out); break;
+    case 2: upsample_nn_kernel<uint16_t><<<grid, 256, 0, st>>>((const uint16_t*)in, planes, h, w, factor, (uint16_t*)out); break;
+    case 4: upsample_nn_kernel<uint32_t><<<grid, 256, 0, st>>>((const uint32_t*)in, planes, h, w, factor, (uint32_t*)out); break;
+    case 8: upsample_nn_kernel<uint64_t><<<grid, 256, 0, st>>>((const uint64_t*)in, planes, h, w, factor, (uint64_t*)out); break;
+    default: IG_REQUIRE(false, "upsample_nn: element size %d", elem_bytes);
+  }
+  note_launch();
+  return cuda_check("ig_upsample_nn");
 }
 
 int ig_patch_features(const void* in, int64_t tile_stride, int32_t n, int32_t h, int32_t w,

@@ -159,8 +159,16 @@ def apply_batch(spec: DenoiserSpec, src: torch.Tensor, src_region: Region | None
 # ---------------------------------------------------------------------------
 # reference-shaped single-window API
 
-def apply(spec: DenoiserSpec, x, y: Conditioning | None, t: int):
-    """Phi on one (C, H, W) window at outer step t (denoise.py:89-113)."""
+def apply(spec: DenoiserSpec, x, y: Conditioning | None, t: int, *,
+          origin: tuple[int, int] = (0, 0), seed: int = 0):
+    """Phi on one (C, H, W) window at outer step t (denoise.py:89-113).
+
+    The analytic kinds are pure functions of (x, y, t), as in the reference.
+    The ``"unet"`` kind (no reference counterpart) also depends on where the
+    window sits: its consistency renoise at steps t < T draws coordinate noise
+    (stream 301 + t) and conditioning holes are filled from stream 101, both
+    keyed on the window's lattice ``origin`` and the sampler ``seed`` -- pass
+    the window's origin and seed to reproduce the sampler's Phi exactly."""
     was_dev = isinstance(x, torch.Tensor)
     xa = x if was_dev else np.asarray(x)
     if xa.ndim != 3:
@@ -189,9 +197,42 @@ def apply(spec: DenoiserSpec, x, y: Conditioning | None, t: int):
         par = torch.cat([ch[:1].to(xt.dtype), mk.reshape(1, win, win).to(xt.dtype)], dim=0)
         cond = CondSource(par.contiguous(), Region(0, 0, win, win), 1, 1, 0, fill=False)
     if spec.kind == "unet":
-        raise ShapeError("single-window apply of the UNet kind: use the sampler (batched)")
-    out = apply_batch(spec, xt[None], None, wxy, win, t, cond)[0]
+        out = _apply_unet(spec, xt, y, t, origin, seed)
+    else:
+        out = apply_batch(spec, xt[None], None, wxy, win, t, cond)[0]
     return out if was_dev else dev.download(out)
+
+
+def _apply_unet(spec: DenoiserSpec, xt: torch.Tensor, y, t: int, origin, seed: int):
+    """One window through the batched UNet path (a batch of one; the kernels
+    are batch invariant, so this is bit-identical to the sampler's Phi)."""
+    from .unet import unet_phi_batch
+    cfg = spec.unet
+    steps = len(cfg.sigmas)
+    if not 1 <= t <= steps:
+        raise ValueError(f"outer step {t} outside [1, {steps}] for a {steps}-step UNet")
+    C, H, W = xt.shape
+    if C != cfg.data_channels:
+        raise ShapeError(f"window has {C} channels, the UNet expects {cfg.data_channels}")
+    x0, y0 = int(origin[0]), int(origin[1])
+    cond = None
+    if cfg.cond_channels:
+        if y is None:
+            raise ShapeError(f"the UNet takes {cfg.cond_channels} conditioning channels; "
+                             "y is None")
+        ch = y.channels if isinstance(y.channels, torch.Tensor) else dev.upload(
+            np.ascontiguousarray(np.asarray(y.channels, dtype=np.float32)))
+        mk = y.mask if isinstance(y.mask, torch.Tensor) else dev.upload(
+            np.ascontiguousarray(np.asarray(y.mask, dtype=np.float32)))
+        k = ch.shape[0]
+        # the materialised conditioning as a scale-1 parent slab at the window's
+        # own footprint, the mask as its last channel (holes are re-filled from
+        # the same stream-101 noise at the same coordinates: a no-op)
+        par = torch.cat([ch.float(), mk.reshape(1, H, W).float()], dim=0).contiguous()
+        cond = CondSource(par, Region(x0, y0, W, H), 1, k, seed)
+    wxy = dev.upload_i64([[x0, y0]])
+    return unet_phi_batch(cfg, xt.float()[None].contiguous(), None, wxy, W, t, cond, seed,
+                          steps)[0]
 
 
 def conditioning_for_window(parent, parent_region: Region, scale: int, layout: WindowLayout,

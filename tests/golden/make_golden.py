@@ -360,17 +360,123 @@ def gen_api():
     print("wrote api_surface.json")
 
 
+# cfg2 at the BASELINE size, and noise over the cfg5 outer cover: too large to
+# commit, so the fixture holds SHA-256 digests of the reference's output bytes
+# (plus a few sampled values for diagnostics)
+CFG5_COVER = (-256, -256, 16896, 16896)     # region_union_cover twice of 16384^2
+NOISE_STRIP = 512
+
+
+def gen_scale():
+    import hashlib
+    meta = {}
+    spec = DenoiserSpec(kind="shrink_smooth", radius=1, lambdas=(0.6, 0.4))
+    cfg = sampler.SamplerConfig(steps=2, layout=WindowLayout(256, 128), denoiser=spec, seed=0,
+                                name="cfg2")
+    st = sampler.SamplerState(cfg, store.TileStore())
+    r = Region(0, 0, 2048, 2048)
+    out0 = st.query(0, r)
+    cov = grid.region_union_cover(cfg.layout, r)
+    out1 = st.query(1, cov)
+    meta["cfg2"] = dict(region=[0, 0, 2048, 2048], cover=[cov.x0, cov.y0, cov.width, cov.height],
+                        spec=_spec_dict(spec), seed=0,
+                        sha_t0=hashlib.sha256(out0.tobytes()).hexdigest(),
+                        sha_t1=hashlib.sha256(out1.tobytes()).hexdigest(),
+                        calls=[st.denoiser_call_count(0), st.denoiser_call_count(1)],
+                        probe=[[y, x, int(out0[0, y, x].view(np.uint32))]
+                               for (y, x) in ((0, 0), (1023, 77), (2047, 2047), (129, 1900))])
+    x0, y0, w, h = CFG5_COVER
+    full = hashlib.sha256()
+    strips = []
+    for sy in range(0, h, NOISE_STRIP):
+        rows = min(NOISE_STRIP, h - sy)
+        z = noise.noise_region(noise.NoiseStream(0, 0), Region(x0, y0 + sy, w, rows), 1)
+        b = z.tobytes()
+        full.update(b)
+        strips.append(hashlib.sha256(b).hexdigest())
+    meta["noise_cfg5"] = dict(seed=0, stream=0, region=list(CFG5_COVER), strip_rows=NOISE_STRIP,
+                              samples=w * h, sha=full.hexdigest(), strips=strips)
+    with open(os.path.join(HERE, "scale.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+    print("wrote scale.json")
+
+
+def gen_persist():
+    """An ITNSTORE file flushed by the reference (the indirect store of the
+    acceptance test's shape, test_acceptance.py:157-183), plus what a reopened
+    store returns for the original and adjacent regions."""
+    import tempfile
+    meta = {}
+    arrays = {}
+    spec = DenoiserSpec(kind="shrink_smooth", radius=1, lambdas=(0.6, 0.4))
+
+    def state(st):
+        return sampler.SamplerState(sampler.SamplerConfig(
+            steps=2, layout=WindowLayout(16, 8), denoiser=spec, seed=47,
+            cache_method="indirect", name="acc6"), st)
+
+    rng = np.random.default_rng(6)
+    first = [Region(int(rng.integers(-100, 100)), int(rng.integers(-100, 100)),
+                    int(rng.integers(8, 32)), int(rng.integers(8, 32))) for _ in range(6)]
+    second = [r.translate(r.width, 0) for r in first[:3]] + [Region(-5, -7, 30, 19)]
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "acc.store")
+        st = store.TileStore(tile_size=32, path=path)
+        s0 = state(st)
+        for r in first:
+            s0.query(0, r)
+        st.flush()
+        blob = open(path, "rb").read()
+        arrays["store_file"] = np.frombuffer(blob, dtype=np.uint8)
+        meta["calls_before"] = [s0.denoiser_call_count(0), s0.denoiser_call_count(1)]
+        re = store.open_store(path)
+        s1 = state(re)
+        for k, r in enumerate(first + second):
+            arrays[f"q{k}"] = s1.query(0, r).view(np.uint32)
+        meta["calls_after"] = [s1.denoiser_call_count(0), s1.denoiser_call_count(1)]
+        meta["processed_after"] = {str(t): sorted([list(i) for i in re.processed_set(s1.handles[t])])
+                                   for t in (0, 1)}
+        re.path = os.path.join(tmp, "re.store")
+        re.flush()
+        arrays["store_file_after"] = np.frombuffer(open(re.path, "rb").read(), dtype=np.uint8)
+    meta["first"] = [[r.x0, r.y0, r.width, r.height] for r in first]
+    meta["second"] = [[r.x0, r.y0, r.width, r.height] for r in second]
+    _save("persist", meta, arrays)
+
+
+def gen_dtypes():
+    """Transforms on non-float64 inputs: the reference keeps numpy's result
+    dtypes (block_mean of float32 is a float32 mean, of ints a float64 mean;
+    laplacian_decode returns the input dtype)."""
+    rng = np.random.default_rng(99)
+    x32 = (rng.normal(size=(3, 64, 40)) * 700).astype(np.float32)
+    xi = rng.integers(-3000, 3000, size=(48, 32)).astype(np.int32)
+    x16 = (rng.normal(size=(32, 24)) * 100).astype(np.float16)
+    arrays = dict(x32=x32, xi=xi, x16=x16)
+    for f in (2, 4, 8):
+        arrays[f"bm32_f{f}"] = transforms.block_mean(x32, f)
+    arrays["bmi_f4"] = transforms.block_mean(xi, 4)
+    arrays["bm16_f4"] = transforms.block_mean(x16, 4)
+    arrays["up32_3"] = transforms.upsample_nn(x32, 3)
+    for name, x in (("x32", x32), ("xi", xi), ("x16", x16)):
+        pair = transforms.laplacian_encode(x, 8 if name == "x32" else 4, 1)
+        arrays[f"lap_{name}_low"] = pair.low
+        arrays[f"lap_{name}_dec"] = transforms.laplacian_decode(pair)
+        arrays[f"lap_{name}_stab"] = transforms.laplacian_decode(transforms.laplacian_stabilize(pair, 1))
+    arrays["ssq_i"] = transforms.signed_square(xi)
+    arrays["ssqrt_i"] = transforms.signed_sqrt(xi)
+    arrays["box_i"] = transforms.box_mean(xi.astype(np.float32), 1)
+    _save("dtypes", {}, arrays)
+
+
 if __name__ == "__main__":
     info = dict(python=sys.version.split()[0], numpy=np.__version__,
                 machine=platform.machine(), processor=platform.processor(),
                 infigrid=infigrid.__version__)
     with open(os.path.join(HERE, "PROVENANCE.json"), "w") as f:
         json.dump(info, f, indent=1)
-    gen_noise()
-    gen_sampler()
-    gen_transforms()
-    gen_denoise()
-    gen_pipeline()
-    gen_store()
-    gen_cli()
-    gen_api()
+    gens = dict(noise=gen_noise, sampler=gen_sampler, transforms=gen_transforms,
+                denoise=gen_denoise, pipeline=gen_pipeline, store=gen_store, cli=gen_cli,
+                api=gen_api, scale=gen_scale, persist=gen_persist, dtypes=gen_dtypes)
+    for name in (sys.argv[1:] or list(gens)):     # e.g. `make_golden.py scale persist`
+        gens[name]()

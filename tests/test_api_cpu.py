@@ -186,10 +186,24 @@ def test_api_surface_matches_reference():
     assert [n for n in surf["all"] if not hasattr(ours, n)] == []
     for m, names in surf["modules"].items():
         mod = importlib.import_module("paper_2512_08309_b200." + m)
-        assert [n for n in names if not hasattr(mod, n)] == [], m
+        # the reference's module-level imports (json, np, struct, ...) are not API
+        stdlib = {"json", "np", "os", "struct", "threading", "math", "random", "sys", "hashlib"}
+        assert [n for n in names if n not in stdlib and not hasattr(mod, n)] == [], m
     for c, members in surf["classes"].items():
         assert [k for k in members if not hasattr(getattr(ours, c), k)] == [], c
     for f, params in surf["params"].items():
         got = [(p.name, repr(p.default) if p.default is not p.empty else None)
                for p in inspect.signature(getattr(ours, f)).parameters.values()]
         assert got[:len(params)] == [tuple(p) for p in params], f
+
+
+@pytest.mark.parametrize("eps", [0.0, -1.0, 1.5])
+def test_bad_epsilon_fails_at_construction(eps):
+    """The reference raises ValueError when SamplerState builds its weight map
+    (sampler.py:133 via grid.py:148-170) -- before any window is generated."""
+    import paper_2512_08309_b200 as ig
+    from paper_2512_08309_b200.grid import WindowLayout
+    cfg = ig.SamplerConfig(steps=2, layout=WindowLayout(16, 8), denoiser=ig.DenoiserSpec(),
+                           epsilon=eps, seed=0)
+    with pytest.raises(ValueError):
+        ig.SamplerState(cfg, ig.TileStore())

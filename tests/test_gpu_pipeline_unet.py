@@ -14,7 +14,9 @@ from paper_2512_08309_b200 import transforms  # noqa: E402
 from paper_2512_08309_b200.grid import Region  # noqa: E402
 from paper_2512_08309_b200.unet import UNetConfig  # noqa: E402
 
-RMS_TOL, MAX_TOL = 0.03, 0.25
+# stated tolerance, ~2x the measured error (r02 B200: channels rel RMS 0.67-0.71 %,
+# rel max 2.9-3.6 %; decoded elevations RMS 0.0102 m / max-abs 0.065 m vs std 1.45 m)
+RMS_TOL, MAX_TOL = 0.015, 0.08
 
 COARSE = UNetConfig(base=64, mults=(1,), blocks=1, sigmas=(80.0,))
 BASE = UNetConfig(data_channels=2, cond_channels=3, base=64, mults=(1, 2), blocks=1,
@@ -55,6 +57,7 @@ def test_unet_hierarchy_vs_oracle():
         std = float(want[c].std())
         rms = float(np.sqrt(np.mean((got[c] - want[c]) ** 2))) / std
         mx = float(np.abs(got[c] - want[c]).max()) / std
+        print(f"\n[tol] hierarchy channel {c}: rel rms {rms:.4f}, rel max {mx:.4f}")
         assert rms < RMS_TOL and mx < MAX_TOL, (c, rms, mx)
     # Laplacian decode of the base stage's (low source, residual) channels
     low = transforms.block_mean(got[0].astype(np.float64), 8)
@@ -63,8 +66,8 @@ def test_unet_hierarchy_vs_oracle():
     elev = transforms.laplacian_decode_signed_square(transforms.laplacian_stabilize(pair, 1))
     assert elev.shape == (128, 128) and np.isfinite(elev).all()
     # final elevations (metres, the reference's signed-square convention) against the same
-    # decode of the fp32 oracle's channels: stated tolerance RMS <= 3% and max-abs <= 25%
-    # of the oracle elevation's standard deviation (bf16 activations, fp32 accumulation)
+    # decode of the fp32 oracle's channels: stated tolerance RMS <= 1.5% and max-abs <= 8%
+    # of the oracle elevation's standard deviation (now 1.5% / 8%) (bf16 activations, fp32 accumulation)
     low_r = transforms.block_mean(want[0].astype(np.float64), 8)
     pair_r = transforms.LaplacianPair(low=low_r, high=want[1].astype(np.float64), factor=8,
                                       dtype=np.dtype(np.float32))

@@ -9,6 +9,8 @@
 
 import math
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -25,8 +27,10 @@ DEV = "cuda"
 
 # Stated tolerance of the bf16 UNet path vs the fp32 oracle, relative to the
 # oracle output's standard deviation (elevation units of the sampler):
-UNET_RMS_TOL = 0.03     # RMS error / std
-UNET_MAX_TOL = 0.25     # max-abs error / std
+# stated tolerance, ~2x the error measured on a B200 (r02: rel RMS 0.53-0.89 %,
+# rel max-abs 2.4-4.2 % over the tests below)
+UNET_RMS_TOL = 0.02     # RMS error / std
+UNET_MAX_TOL = 0.09     # max-abs error / std
 
 
 def _conv_ref(a, b, w, cout, taps, scale, res, ra, rb, gain):
@@ -197,6 +201,8 @@ def test_unet_phi_vs_fp32_oracle(outer_step):
     std = float(want.std())
     rms = float(np.sqrt(np.mean((got - want) ** 2))) / std
     mx = float(np.abs(got - want).max()) / std
+    print(f"\n[tol] {os.environ.get('PYTEST_CURRENT_TEST', '').split(' ')[0]}: "
+          f"rel rms {rms:.4f}, rel max {mx:.4f}")
     assert rms < UNET_RMS_TOL and mx < UNET_MAX_TOL, (rms, mx)
 
 
@@ -221,6 +227,8 @@ def test_sampler_unet_two_step_vs_oracle():
     std = float(want.std())
     rms = float(np.sqrt(np.mean((got - want) ** 2))) / std
     mx = float(np.abs(got - want).max()) / std
+    print(f"\n[tol] {os.environ.get('PYTEST_CURRENT_TEST', '').split(' ')[0]}: "
+          f"rel rms {rms:.4f}, rel max {mx:.4f}")
     assert rms < UNET_RMS_TOL and mx < UNET_MAX_TOL, (rms, mx)
     # seed consistency: re-query of a sub-region from a fresh store is bit-identical
     sub = ig.SamplerState(scfg, ig.TileStore()).query(0, Region(32, 32, 64, 32))
@@ -677,6 +685,8 @@ def test_unet_with_attention_vs_fp32_oracle(win, nwin):
     std = float(want.std())
     rms = float(np.sqrt(np.mean((got - want) ** 2))) / std
     mx = float(np.abs(got - want).max()) / std
+    print(f"\n[tol] {os.environ.get('PYTEST_CURRENT_TEST', '').split(' ')[0]}: "
+          f"rel rms {rms:.4f}, rel max {mx:.4f}")
     assert rms < UNET_RMS_TOL and mx < UNET_MAX_TOL, (rms, mx)
 
 
