@@ -173,9 +173,13 @@ def build_program(cfg: UNetConfig) -> Program:
     return prog
 
 
-def conv_flops(cfg: UNetConfig, h: int, w: int, padded: bool = False) -> float:
+def conv_flops(cfg: UNetConfig, h: int, w: int, padded: bool = False,
+               stem_head: bool = True) -> float:
     """Algorithmic FLOPs of one window (real input/output channels unless
-    `padded`): sum over convs of 2 * H * W * Cin * Cout * taps."""
+    `padded`): sum over convs of 2 * H * W * Cin * Cout * taps, plus the
+    attention contractions.  ``stem_head=False`` leaves out the input stem and
+    the output head (the fused stem / head kernels, timed apart from the
+    tensor-core convolutions)."""
     prog = build_program(cfg)
     res = {}
     # resolution of each conv: walk the ops
@@ -185,6 +189,8 @@ def conv_flops(cfg: UNetConfig, h: int, w: int, padded: bool = False) -> float:
         lv_res.append((h >> lv, w >> lv))
     total = 0.0
     for name, cs in prog.convs.items():
+        if name in ("stem", "out") and not stem_head:
+            continue
         if name in ("stem", "out"):
             hh, ww = h, w
         else:

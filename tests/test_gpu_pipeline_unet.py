@@ -67,7 +67,7 @@ def test_unet_hierarchy_vs_oracle():
     assert elev.shape == (128, 128) and np.isfinite(elev).all()
     # final elevations (metres, the reference's signed-square convention) against the same
     # decode of the fp32 oracle's channels: stated tolerance RMS <= 1.5% and max-abs <= 8%
-    # of the oracle elevation's standard deviation (now 1.5% / 8%) (bf16 activations, fp32 accumulation)
+    # of the oracle elevation's standard deviation (bf16 activations, fp32 accumulation)
     low_r = transforms.block_mean(want[0].astype(np.float64), 8)
     pair_r = transforms.LaplacianPair(low=low_r, high=want[1].astype(np.float64), factor=8,
                                       dtype=np.dtype(np.float32))
