@@ -27,6 +27,9 @@
  *   ig_procedural_map      pipeline.py:101-123 ProceduralMap.values
  *   ig_corrupt             pipeline.py:126-139 corrupt_user_map
  *   ig_raster_map          pipeline.py:72-84 RasterMap.values
+ *   ig_pack_windows / ig_ipc_event_*   the halo exchange of the sharded query
+ *                          (no reference counterpart: the reference is
+ *                          single-process)
  *   ig_tiles_resolve       store.py:364-426 _gather_tiles + _commit_region of
  *                          _read_indirect (INDIRECT tile cache in HBM)
  *   ig_unet_*              the Phi plugin (denoise.py:89 apply) for the new "unet" kind;
@@ -123,6 +126,19 @@ int ig_ipc_close(void* base);
  * a peer maps only the exchanged windows) */
 int ig_ipc_alloc(int64_t bytes, void** ptr_out);
 int ig_ipc_free(void* ptr);
+/* one launch copies n windows (window_bytes each, a multiple of 16) from the
+ * device addresses src_ptrs[k] (a device table) into consecutive slots of dst:
+ * the producer's pack of its outgoing boundary windows */
+int ig_pack_windows(const int64_t* src_ptrs, int32_t n, int64_t window_bytes, void* dst,
+                    void* cuda_stream);
+/* cross-process device ordering of the exchange: the producer records an
+ * interprocess event after its pack, the consumer's stream waits on it before
+ * the blends that read the windows (64-byte cudaIpcEventHandle_t) */
+int ig_ipc_event_create(uint8_t* handle64, void** event_out);
+int ig_ipc_event_open(const uint8_t* handle64, void** event_out);
+int ig_event_record(void* event, void* cuda_stream);
+int ig_stream_wait_event(void* cuda_stream, void* event);
+int ig_event_destroy(void* event);
 
 /* ---- INDIRECT tile cache (store.py:358-426) ---------------------------------
  * table[2*(ty*ntx + tx)] = device pointer of tile (tx0+tx, ty0+ty)'s data

@@ -51,6 +51,12 @@ SIGNATURES = {
     "ig_ipc_close": [V],
     "ig_ipc_alloc": [I64, V],
     "ig_ipc_free": [V],
+    "ig_pack_windows": [V, I32, I64, V, V],
+    "ig_ipc_event_create": [V, V],
+    "ig_ipc_event_open": [V, V],
+    "ig_event_record": [V, V],
+    "ig_stream_wait_event": [V, V],
+    "ig_event_destroy": [V],
     "ig_box_mean": [V, I32, I32, I32, I32, I32, V, V],
     "ig_blur_block_mean_f64": [V, I32, I32, I32, I32, I32, I32, V, V, V],
     "ig_laplacian_residual": [V, I32, V, I32, I32, I32, I32, V, V],

@@ -3,13 +3,19 @@
 The world plane partitions naturally: every pixel of every step image is a
 pure function of (seed, coordinates), and its value is the canonical (j, i)
 ordered sum over the windows covering it.  A region R is split into
-horizontal output strips, one per rank.  Each step's window *rows* are then
-owned by exactly one rank (owner-computes: no window is evaluated twice), and
-before a step's blend every rank receives, from its neighbours, the Phi
-outputs of the boundary window rows it needs but does not own (the halo
-exchange, NCCL send/recv over NVLink).  Each rank then blends its strip with
-the full canonical window set, so the gathered result is bitwise equal to the
+horizontal output strips, one per rank.  Each step's windows -- exactly the
+ones a single-GPU query evaluates -- are split into equal-count runs in
+canonical order, one per rank (owner-computes: no window is evaluated twice,
+every step balanced to one window).  Before a step's blends every rank
+receives, from its neighbours, the Phi outputs of the boundary windows it
+needs but does not own (the halo exchange), then blends with the full
+canonical window set, so the gathered result is bitwise equal to the
 single-GPU query -- no all-reduce (partial sums would change the float order).
+
+Exchanges: ``IpcExchange`` (the default on one node: peer-memory reads fused
+into the consumer's blend, ordered by interprocess CUDA events, no device
+sync) and ``p2p_exchange`` (torch.distributed send/recv: NCCL over NVLink, or
+gloo in the CPU tests).
 
 The planner is pure host logic; execution goes through an executor with
 three operations (``generate``, ``inject``, ``query``) so the same plan runs
@@ -21,15 +27,20 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-from .grid import Region, WindowLayout, index_box, region_union_cover
+from .grid import Region, WindowIndex, WindowLayout, region_union_cover, window_region, \
+    windows_overlapping
 
 
 @dataclass
 class StepPlan:
-    rows_needed: dict[int, tuple[int, int]]      # rank -> inclusive window-row range
-    owner: dict[int, int]                          # window row j -> owning rank
-    cols: tuple[int, int]                          # inclusive window-column range (all ranks)
-    sends: dict[tuple[int, int], list[int]] = field(default_factory=dict)  # (src, dst) -> rows
+    windows: list[WindowIndex]                     # the step's windows, canonical (j, i) order
+    bounds: list[int]                              # rank k owns windows[bounds[k]:bounds[k+1]]
+    needed: dict[int, list[WindowIndex]]           # rank -> windows it must hold this step
+    sends: dict[tuple[int, int], list[WindowIndex]] = field(default_factory=dict)  # (src, dst)
+
+    def owner(self) -> dict[WindowIndex, int]:
+        return {w: k for k in range(len(self.bounds) - 1)
+                for w in self.windows[self.bounds[k]:self.bounds[k + 1]]}
 
 
 @dataclass
@@ -39,12 +50,21 @@ class ShardPlan:
     strips: list[Region]
     steps: list[StepPlan]                          # index t = sampler step (0 = final)
 
-    def owned(self, t: int, rank: int) -> list[int]:
-        return sorted(j for j, r in self.steps[t].owner.items() if r == rank)
+    def owned(self, t: int, rank: int) -> list[WindowIndex]:
+        sp = self.steps[t]
+        return sp.windows[sp.bounds[rank]:sp.bounds[rank + 1]]
 
-    def windows(self, t: int, rows) -> list[tuple[int, int]]:
-        i_lo, i_hi = self.steps[t].cols
-        return [(i, j) for j in sorted(rows) for i in range(i_lo, i_hi + 1)]
+    def load(self) -> dict:
+        """Phi-count balance: per rank the windows it evaluates; the critical
+        path is the sum over steps of the busiest rank (each step ends with an
+        exchange), relative to a perfect split."""
+        per_rank = [sum(len(self.owned(t, k)) for t in range(len(self.steps)))
+                    for k in range(self.world)]
+        crit = sum(max(len(self.owned(t, k)) for k in range(self.world))
+                   for t in range(len(self.steps)))
+        total = sum(per_rank)
+        return {"per_rank": per_rank, "max_over_mean": max(per_rank) * self.world / total,
+                "critical_path_over_ideal": crit * self.world / total}
 
 
 def split_rows(r: Region, world: int, align: int = 1) -> list[Region]:
@@ -60,51 +80,52 @@ def split_rows(r: Region, world: int, align: int = 1) -> list[Region]:
     return [Region(r.x0, cuts[k], r.width, cuts[k + 1] - cuts[k]) for k in range(world)]
 
 
+def _box(layout: WindowLayout, idxs) -> Region:
+    """Bounding box of the windows' footprints."""
+    regs = [window_region(layout, w) for w in idxs]
+    x0, y0 = min(g.x0 for g in regs), min(g.y0 for g in regs)
+    return Region(x0, y0, max(g.x1 for g in regs) - x0, max(g.y1 for g in regs) - y0)
+
+
 def plan(layouts: list[WindowLayout], r: Region, world: int) -> ShardPlan:
-    """Owner-computes plan for query(0, r) of a `len(layouts)`-step sampler."""
+    """Owner-computes plan for query(0, r) of a `len(layouts)`-step sampler
+    (SURVEY 8(e)).
+
+    Step t evaluates exactly the windows a single-GPU query does (those
+    overlapping the step's region: r, then its covers), each once.  They are
+    split into `world` runs of equal count in canonical (j, i) order --
+    contiguous window rows, a run may start or end mid-row -- so every step is
+    balanced to one window.  Rank k outputs strip k of r; it needs the step-0
+    windows overlapping its strip, and at step t >= 1 the windows overlapping
+    the bounding box of what it evaluates at step t - 1 (the parent region its
+    generator reads).  Needed windows owned elsewhere are sent by their owner."""
     T = len(layouts)
     strips = split_rows(r, world, align=layouts[0].stride)
+    regions = [r]
+    for t in range(T - 1):
+        regions.append(region_union_cover(layouts[t], regions[t]))
     steps: list[StepPlan] = []
-    need = {k: strips[k] for k in range(world)}   # region each rank needs at step t
-    full = r
     for t in range(T):
         lay = layouts[t]
-        fi_lo, fi_hi, _, _ = index_box(lay, full)
-        rows_needed = {}
+        wins = windows_overlapping(lay, regions[t])
+        n = len(wins)
+        bounds = [n * k // world for k in range(world + 1)]
+        needed = {}
         for k in range(world):
-            _, _, j_lo, j_hi = index_box(lay, need[k])
-            rows_needed[k] = (j_lo, j_hi)
-        # owner of a row: the lowest-numbered rank whose strip interior the
-        # row's first output line falls into; rows outside all strips go to
-        # the nearest rank.  Every needed row gets exactly one owner.
-        owner = {}
-        all_rows = sorted({j for k in range(world)
-                           for j in range(rows_needed[k][0], rows_needed[k][1] + 1)})
-        for j in all_rows:
-            y_mid = j * lay.stride + lay.offset[1] + lay.window // 2
-            cand = [k for k in range(world) if rows_needed[k][0] <= j <= rows_needed[k][1]]
-            best = min(cand, key=lambda k: (0 if strips[k].y0 <= y_mid < strips[k].y1 else 1,
-                                            abs(strips[k].y0 + strips[k].height // 2 - y_mid),
-                                            k))
-            owner[j] = best
-        sp = StepPlan(rows_needed=rows_needed, owner=owner, cols=(fi_lo, fi_hi))
+            if t == 0:
+                needed[k] = windows_overlapping(lay, strips[k])
+            else:
+                below = steps[t - 1]
+                mine = below.windows[below.bounds[k]:below.bounds[k + 1]]
+                needed[k] = windows_overlapping(lay, _box(layouts[t - 1], mine)) if mine else []
+        sp = StepPlan(windows=wins, bounds=bounds, needed=needed)
+        owner = sp.owner()
         for dst in range(world):
-            lo, hi = rows_needed[dst]
-            for j in range(lo, hi + 1):
-                src = owner[j]
+            for w in needed[dst]:
+                src = owner[w]
                 if src != dst:
-                    sp.sends.setdefault((src, dst), []).append(j)
+                    sp.sends.setdefault((src, dst), []).append(w)
         steps.append(sp)
-        # next step: each rank needs the union cover of its needed windows
-        nxt = {}
-        for k in range(world):
-            lo, hi = rows_needed[k]
-            box = Region(fi_lo * lay.stride + lay.offset[0], lo * lay.stride + lay.offset[1],
-                         (fi_hi - fi_lo) * lay.stride + lay.window,
-                         (hi - lo) * lay.stride + lay.window)
-            nxt[k] = box
-        need = nxt
-        full = region_union_cover(lay, full)
     return ShardPlan(region=r, world=world, strips=strips, steps=steps)
 
 
@@ -116,20 +137,21 @@ def run(plan_: ShardPlan, rank: int, executor, exchange):
     executor.query(region) -> step-0 image of the rank's strip
     exchange(t, {dst: [data, ...]}, {src: n}) -> {src: [data, ...]}
         moves packed window data; both sides derive the window order from the
-        plan, so only tensors travel.
+        plan, so only tensors travel.  An exchange with a ``finish()`` is told
+        when the rank's last read of received windows has been issued.
     Steps run deepest first (t = T-1 .. 0), as plan_rounds does.
     """
     T = len(plan_.steps)
     for t in reversed(range(T)):
         sp = plan_.steps[t]
         mine = plan_.owned(t, rank)
-        produced = executor.generate(t, plan_.windows(t, mine)) if mine else {}
+        produced = executor.generate(t, mine) if mine else {}
         outgoing, expect = {}, {}
-        for (src, dst), rows in sorted(sp.sends.items()):
+        for (src, dst), idxs in sorted(sp.sends.items()):
             if src == rank:
-                outgoing[dst] = [produced[idx] for idx in plan_.windows(t, rows)]
+                outgoing[dst] = [produced[idx] for idx in idxs]
             if dst == rank:
-                expect[src] = plan_.windows(t, rows)
+                expect[src] = idxs
         incoming = exchange(t, outgoing, {src: len(v) for src, v in expect.items()})
         got = {}
         for src, idxs in expect.items():
@@ -137,7 +159,10 @@ def run(plan_: ShardPlan, rank: int, executor, exchange):
                 got[idx] = data
         if got:
             executor.inject(t, got)
-    return executor.query(plan_.strips[rank])
+    out = executor.query(plan_.strips[rank])
+    if hasattr(exchange, "finish"):
+        exchange.finish()
+    return out
 
 
 class StoreExecutor:
@@ -211,90 +236,191 @@ class _DeviceBuffer:
                                          "data": (ptr, False), "version": 3, "strides": None}
 
 
-def ipc_exchange(dist, window_shape, dtype):
-    """Halo exchange over peer memory (NVLink on B200): no inter-GPU copy.
+class IpcExchange:
+    """Halo exchange over peer memory (NVLink on B200): no inter-GPU copy and no
+    host synchronisation of the device per step.
 
-    Per step every producer packs its outgoing windows (all destinations) into
-    ONE dedicated device allocation (ig_ipc_alloc, outside torch's caching
-    pool -- an IPC handle maps the whole allocation it points into) with an
-    on-device copy, exports its handle, and all ranks exchange the small
-    metadata in one all_gather_object.  Each consumer maps the allocation
-    (ig_ipc_open enables peer access from its own device) and installs the
-    windows as PeerWindow views: its blend kernel reads the boundary windows
-    in place, over NVLink, in the canonical (j, i) order -- the exchange is
-    fused into the blend's loads.
+    Per step t a producer packs its outgoing windows (all destinations) with
+    ONE kernel (``ig_pack_windows``) into its exchange buffer for t -- a
+    dedicated cudaMalloc (``ig_ipc_alloc``; an IPC handle maps the whole
+    allocation it points into) exported once -- and records an interprocess
+    CUDA event on its stream.  One small host collective per step (gloo) then
+    carries the window offsets (plus, the first time, the buffer and event
+    handles).  Each consumer maps the buffer once (``ig_ipc_open``), makes its
+    stream wait on the producer's event (``ig_stream_wait_event``: device-side
+    ordering, the host never waits for the GPU) and installs the windows as
+    ``PeerWindow`` slots, which its blend kernels read in place over NVLink in
+    the canonical (j, i) order -- the transfer is fused into the blend's loads.
 
-    Ordering: producers synchronise their device before publishing; consumers
-    launch their blends only after the gather.  Lifetime: every step's buffer
-    stays allocated (the windows of step t are parents of step t-1 and the
-    final query reads step 0's) until ``exchange.close()`` -- device sync +
-    barrier (all ranks done reading), then unmap and free."""
-    import ctypes
+    The host collective follows the producer's event record, so a consumer's
+    wait always sees this step's record.  Buffers are reused by the next query
+    (``run`` calls ``finish``): each rank records a release event after its
+    last read and every rank's stream waits on all release events before it
+    packs again.  ``close()`` unmaps and frees everything (after a device sync
+    and two barriers)."""
 
-    import numpy as np
-    import torch
+    def __init__(self, dist, window_shape, dtype):
+        import numpy as np
+        import torch
 
-    from . import _device as dev
-    from . import _native
+        from . import _native
+        self.dist = dist
+        self.L = _native.lib()
+        self._native = _native
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        # the per-step handshake is host-only: a gloo group beside an NCCL default
+        self.group = dist.new_group(backend="gloo") if dist.get_backend() != "gloo" else None
+        self.window_shape = tuple(window_shape)
+        self.dtype = dtype
+        self.wbytes = int(np.prod(window_shape)) * torch.empty((), dtype=dtype).element_size()
+        self.bufs: dict[int, tuple[int, int]] = {}       # step -> (ptr, capacity in windows)
+        self.retired: list[int] = []                     # outgrown buffers, freed at close
+        self.events: dict[int, int] = {}                 # step -> our pack event
+        self.release = None                              # our release event
+        self.peer_bufs: dict[tuple[int, int], int] = {}  # (src, step) -> window 0 address
+        self.peer_events: dict[tuple[int, int], int] = {}  # (src, step) -> opened event
+        self.mapped: list[int] = []                      # bases from ig_ipc_open
+        self.opened: dict[bytes, int] = {}               # event handle -> opened event
+        self.peer_release: list[int] = []
+        self.pending_release = False
 
-    L = _native.lib()
-    rank = dist.get_rank()
-    typestr = np.dtype(str(dtype).replace("torch.", "")).str
-    wbytes = int(np.prod(window_shape)) * torch.empty((), dtype=dtype).element_size()
-    owned: list[int] = []                 # our exchange buffers
-    mapped: dict[bytes, int] = {}         # peer handle -> mapped base
+    def _stream(self):
+        import torch
+        return torch.cuda.current_stream().cuda_stream
 
-    def exchange(t, outgoing, expect):
+    def _event(self):
+        import ctypes
+        h = (ctypes.c_uint8 * 64)()
+        ev = ctypes.c_void_p()
+        self._native.check(self.L.ig_ipc_event_create(h, ctypes.byref(ev)), "ig_ipc_event_create")
+        return ev.value, bytes(h)
+
+    def _open_event(self, hb: bytes) -> int:
+        import ctypes
+        ev = self.opened.get(hb)
+        if ev is None:
+            q = ctypes.c_void_p()
+            self._native.check(self.L.ig_ipc_event_open(
+                (ctypes.c_uint8 * 64).from_buffer_copy(hb), ctypes.byref(q)), "ig_ipc_event_open")
+            ev = self.opened[hb] = q.value
+        return ev
+
+    def _gather(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def __call__(self, t, outgoing, expect):
+        import ctypes
+
+        import numpy as np
+
+        from . import _device as dev
+        L, check, stream = self.L, self._native.check, self._stream()
+        if self.pending_release:
+            # the previous query's readers of our buffers are done before we pack
+            for ev in self.peer_release:
+                check(L.ig_stream_wait_event(stream, ev), "ig_stream_wait_event")
+            self.pending_release = False
         items = [(dst, x) for dst in sorted(outgoing) for x in outgoing[dst]]
-        mine = {}
+        meta = {"offsets": {}}
         if items:
-            p = ctypes.c_void_p()
-            _native.check(L.ig_ipc_alloc(len(items) * wbytes, ctypes.byref(p)), "ig_ipc_alloc")
-            owned.append(p.value)
-            buf = torch.as_tensor(_DeviceBuffer(p.value, (len(items),) + tuple(window_shape),
-                                                typestr), device=dev.device())
-            for k, (dst, x) in enumerate(items):
-                buf[k].copy_(x)
-            h = (ctypes.c_uint8 * 64)()
-            off = ctypes.c_int64()
-            _native.check(L.ig_ipc_export(ctypes.c_void_p(p.value), h, ctypes.byref(off)),
-                          "ig_ipc_export")
-            for k, (dst, _) in enumerate(items):
-                mine.setdefault(dst, []).append((bytes(h), off.value + k * wbytes))
-        torch.cuda.synchronize()          # published windows are complete
-        meta = [None] * dist.get_world_size()
-        dist.all_gather_object(meta, mine)
+            ptr, cap = self.bufs.get(t, (None, 0))
+            if cap < len(items):
+                if ptr is not None:
+                    self.retired.append(ptr)
+                p = ctypes.c_void_p()
+                check(L.ig_ipc_alloc(len(items) * self.wbytes, ctypes.byref(p)), "ig_ipc_alloc")
+                ptr, cap = p.value, len(items)
+                self.bufs[t] = (ptr, cap)
+                h = (ctypes.c_uint8 * 64)()
+                off = ctypes.c_int64()
+                check(L.ig_ipc_export(ctypes.c_void_p(ptr), h, ctypes.byref(off)),
+                      "ig_ipc_export")
+                meta["buf"] = (bytes(h), off.value)
+            table = dev.upload(np.asarray([x.data_ptr() for _, x in items], dtype=np.int64))
+            check(L.ig_pack_windows(ctypes.c_void_p(table.data_ptr()), len(items), self.wbytes,
+                                    ctypes.c_void_p(ptr), stream), "ig_pack_windows")
+            if t not in self.events:
+                self.events[t], meta["event"] = self._event()
+            check(L.ig_event_record(self.events[t], stream), "ig_event_record")
+            k = 0
+            for dst in sorted(outgoing):
+                meta["offsets"][dst] = k
+                k += len(outgoing[dst])
+        metas = self._gather(meta)
+        for src, m in enumerate(metas):
+            if src == self.rank:
+                continue
+            # every announced buffer / event is mapped by every peer, whether or
+            # not it reads from it this step (a later query may)
+            if "buf" in m:
+                hb, off = m["buf"]
+                q = ctypes.c_void_p()
+                check(L.ig_ipc_open((ctypes.c_uint8 * 64).from_buffer_copy(hb), ctypes.byref(q)),
+                      "ig_ipc_open")
+                self.mapped.append(q.value)
+                self.peer_bufs[(src, t)] = q.value + off
+            if "event" in m:
+                self.peer_events[(src, t)] = self._open_event(m["event"])
         got = {}
         for src, n in expect.items():
-            entries = meta[src].get(rank, []) if n else []
-            if len(entries) != n:
-                raise RuntimeError(f"ipc_exchange: rank {src} published {len(entries)} windows "
-                                   f"for rank {rank}, expected {n}")
-            views = []
-            for hb, off in entries:
-                base = mapped.get(hb)
-                if base is None:
-                    q = ctypes.c_void_p()
-                    _native.check(L.ig_ipc_open((ctypes.c_uint8 * 64).from_buffer_copy(hb),
-                                                ctypes.byref(q)), "ig_ipc_open")
-                    base = mapped[hb] = q.value
-                views.append(PeerWindow(base + off, window_shape, dtype))
-            got[src] = views
+            if not n:
+                continue
+            m = metas[src]
+            check(L.ig_stream_wait_event(stream, self.peer_events[(src, t)]),
+                  "ig_stream_wait_event")
+            base = self.peer_bufs[(src, t)] + m["offsets"][self.rank] * self.wbytes
+            got[src] = [PeerWindow(base + i * self.wbytes, self.window_shape, self.dtype)
+                        for i in range(n)]
         return got
 
-    def close():
-        torch.cuda.synchronize()
-        dist.barrier()                   # every consumer is done reading
-        for base in mapped.values():
-            _native.check(L.ig_ipc_close(ctypes.c_void_p(base)), "ig_ipc_close")
-        mapped.clear()
-        dist.barrier()                   # every peer has unmapped our buffers
-        for ptr in owned:
-            _native.check(L.ig_ipc_free(ctypes.c_void_p(ptr)), "ig_ipc_free")
-        owned.clear()
+    def finish(self):
+        """After the rank's final read of peer windows: publish a release event."""
+        if self.release is None:
+            self.release, hb = self._event()
+        else:
+            hb = None
+        self._native.check(self.L.ig_event_record(self.release, self._stream()), "ig_event_record")
+        handles = self._gather(hb)
+        if not self.peer_release:
+            self.peer_release = [self._open_event(h) for r, h in enumerate(handles)
+                                 if r != self.rank]
+        self.pending_release = True
 
-    exchange.close = close
-    return exchange
+    def close(self):
+        import ctypes
+
+        import torch
+        L = self.L
+        torch.cuda.synchronize()
+        self.dist.barrier(group=self.group)          # every consumer is done reading
+        for base in self.mapped:
+            self._native.check(L.ig_ipc_close(ctypes.c_void_p(base)), "ig_ipc_close")
+        self.mapped.clear()
+        self.peer_bufs.clear()
+        for ev in self.opened.values():
+            L.ig_event_destroy(ctypes.c_void_p(ev))
+        self.opened.clear()
+        self.peer_events.clear()
+        self.peer_release = []
+        self.dist.barrier(group=self.group)          # every peer has unmapped our buffers
+        for ptr, _ in self.bufs.values():
+            self._native.check(L.ig_ipc_free(ctypes.c_void_p(ptr)), "ig_ipc_free")
+        for ptr in self.retired:
+            self._native.check(L.ig_ipc_free(ctypes.c_void_p(ptr)), "ig_ipc_free")
+        self.bufs.clear()
+        self.retired.clear()
+        for ev in list(self.events.values()) + ([self.release] if self.release else []):
+            L.ig_event_destroy(ctypes.c_void_p(ev))
+        self.events.clear()
+        self.release = None
+
+
+def ipc_exchange(dist, window_shape, dtype):
+    """The peer-memory exchange for `shard.run` (see IpcExchange)."""
+    return IpcExchange(dist, window_shape, dtype)
 
 
 _IPC_OK: dict = {}
@@ -370,19 +496,15 @@ def run_emulated(plan_: ShardPlan, executors):
     """Run every rank of a plan inside one process: per step, all ranks
     generate their owned windows first, then exchange, then (after the last
     step) query.  Returns the per-rank strip images."""
-    mailbox = {}
     T = len(plan_.steps)
     world = plan_.world
     for t in reversed(range(T)):
         sp = plan_.steps[t]
-        produced = {k: (executors[k].generate(t, plan_.windows(t, plan_.owned(t, k)))
+        produced = {k: (executors[k].generate(t, plan_.owned(t, k))
                         if plan_.owned(t, k) else {}) for k in range(world)}
         for k in range(world):
-            got = {}
-            for (src, dst), rows in sp.sends.items():
-                if dst == k:
-                    for idx in plan_.windows(t, rows):
-                        got[idx] = produced[src][idx]
+            got = {idx: produced[src][idx] for (src, dst), idxs in sp.sends.items()
+                   if dst == k for idx in idxs}
             if got:
                 executors[k].inject(t, got)
     return [executors[k].query(plan_.strips[k]) for k in range(world)]

@@ -43,12 +43,15 @@ def test_sharded_equals_single(kind, steps, H, s, world, region):
 
 
 # ---------------------------------------------------------------------------
-# Peer-memory halo exchange (shard.ipc_exchange): real processes, each with its
-# own CUDA context; on the round-end box they share one GPU (CUDA IPC works
-# between processes on the same device exactly as across NVLink peers; no
-# kernel waits on another rank -- publication is host-ordered after a device
-# sync).  The gathered strips must be bitwise equal to a one-process query and
-# the boundary windows must have been read in place (PeerWindow slots).
+# Peer-memory halo exchange (shard.IpcExchange): real processes, each with its
+# own CUDA context; on the round-end box they share one GPU (CUDA IPC memory
+# and interprocess events work between processes on the same device exactly as
+# across NVLink peers).  A consumer's stream waits on the producer's pack event
+# (device-side ordering; the producers never wait on their consumers within a
+# query, so time-sliced contexts always make progress).  Two queries run
+# through the same exchange (buffer reuse behind the release events).  The
+# gathered strips must be bitwise equal to one-process queries and the
+# boundary windows must have been read in place (PeerWindow slots).
 
 def _ipc_worker(rank, world, port_, kind, steps, H, s, region, q):
     import os
@@ -61,16 +64,20 @@ def _ipc_worker(rank, world, port_, kind, steps, H, s, region, q):
     try:
         torch.cuda.set_device(0)
         cfg = _cfg(kind, steps, H, s)
-        st = ig.SamplerState(cfg, ig.TileStore())
-        p = shard.plan([WindowLayout(H, s)] * steps, Region(*region), world)
         assert shard.ipc_supported(dist)
         xch = shard.ipc_exchange(dist, (1, H, H), torch.float32)
-        strip = shard.run(p, rank, shard.StoreExecutor(st), xch).cpu().numpy()
-        peers = sum(1 for t in range(steps)
-                    for slot in st.store._tensor(st.handles[t]).lru.values()
-                    if getattr(slot.data, "is_peer", False))
+        out = []
+        for shift in (0, 8 * s):
+            st = ig.SamplerState(cfg, ig.TileStore())
+            r = Region(region[0] + shift, region[1], region[2], region[3])
+            p = shard.plan([WindowLayout(H, s)] * steps, r, world)
+            strip = shard.run(p, rank, shard.StoreExecutor(st), xch).cpu().numpy()
+            peers = sum(1 for t in range(steps)
+                        for slot in st.store._tensor(st.handles[t]).lru.values()
+                        if getattr(slot.data, "is_peer", False))
+            out.append((strip, st.total_denoiser_calls(), peers))
         xch.close()
-        q.put((rank, strip, st.total_denoiser_calls(), peers))
+        q.put((rank, out))
     finally:
         dist.destroy_process_group()
 
@@ -98,9 +105,10 @@ def test_ipc_exchange_bitwise(kind, steps, H, s, world, region):
         pr.join(timeout=60)
         assert pr.exitcode == 0
     cfg = _cfg(kind, steps, H, s)
-    single = ig.SamplerState(cfg, ig.TileStore())
-    want = single.query(0, Region(*region))
-    got = np.concatenate([r_[1] for r_ in res], axis=1)
-    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
-    assert sum(r_[2] for r_ in res) == single.total_denoiser_calls()   # no Phi twice
-    assert sum(r_[3] for r_ in res) > 0          # boundary windows were read in place
+    for k, shift in enumerate((0, 8 * s)):
+        single = ig.SamplerState(cfg, ig.TileStore())
+        want = single.query(0, Region(region[0] + shift, region[1], region[2], region[3]))
+        got = np.concatenate([r_[1][k][0] for r_ in res], axis=1)
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+        assert sum(r_[1][k][1] for r_ in res) == single.total_denoiser_calls()  # no Phi twice
+        assert sum(r_[1][k][2] for r_ in res) > 0    # boundary windows were read in place

@@ -40,11 +40,26 @@ def test_plan_partitions_windows(steps, world):
     need = r
     for t in range(steps):
         full = set(windows_overlapping(lay, need))
-        owned = [set(p.windows(t, p.owned(t, k))) for k in range(world)]
+        owned = [set(p.owned(t, k)) for k in range(world)]
         union = set().union(*owned)
         assert union == full                               # same windows as 1 GPU
         assert sum(len(o) for o in owned) == len(full)     # each exactly once
         need = region_union_cover(lay, need)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_plan_balance_cfg5(world):
+    """cfg5 (16384^2, T=2, 256/128): every step split to within one window, so
+    the Phi critical path is within 2% of a perfect split."""
+    lay = WindowLayout(256, 128)
+    p = shard.plan([lay] * 2, Region(0, 0, 16384, 16384), world)
+    ld = p.load()
+    assert sum(ld["per_rank"]) == 16641 + 17161
+    assert ld["critical_path_over_ideal"] <= 1.02 and ld["max_over_mean"] <= 1.02, ld
+    # boundary traffic: a rank receives about one window row per neighbour and step
+    for t in range(2):
+        for (src, dst), ws in p.steps[t].sends.items():
+            assert abs(src - dst) == 1 and len(ws) <= 3 * 131, (t, src, dst, len(ws))
 
 
 @pytest.mark.parametrize("steps,world", [(2, 2), (2, 4), (3, 3)])
