@@ -20,6 +20,8 @@
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "ig_common.cuh"
 #include "ig_noise.cuh"
 
@@ -252,6 +254,7 @@ struct ConvArgs {
   float res_a, res_b, act_gain;
   __nv_bfloat16* out0;
   __nv_bfloat16* out1;
+  int res_v8;             // residual read as 32-byte (full-sector) loads
 };
 
 template <int N>
@@ -340,6 +343,14 @@ __device__ __forceinline__ void stg_v8(void* p, uint4 a, uint4 b) {
                : "memory");
 }
 
+// 32-byte streaming load (sm_100: LDG.E.256): one lane reads a whole sector
+__device__ __forceinline__ void ldg_nc_v8(const void* p, uint4& a, uint4& b) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z),
+                 "=r"(b.w)
+               : "l"(p));
+}
+
 __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -419,8 +430,13 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
   const int64_t ob0 = out_base(a, p) + c0;
   uint4 res[NC / 8];
   if (resp) {
+    if (a.res_v8 && NC % 16 == 0) {
 #pragma unroll
-    for (int i = 0; i < NC / 8; ++i) res[i] = ldg_nc_v4(resp + off + 8 * i);
+      for (int i = 0; i < NC / 16; ++i) ldg_nc_v8(resp + off + 16 * i, res[2 * i], res[2 * i + 1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < NC / 8; ++i) res[i] = ldg_nc_v4(resp + off + 8 * i);
+    }
   }
 #pragma unroll
   for (int b = 0; b < NC; b += BC) {
@@ -2461,6 +2477,27 @@ __device__ __forceinline__ float ex2_approx(float x) {   // MUFU.EX2, ex2(-inf) 
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA / integer pipes (no MUFU): x = j + f with j = rint(x) (the
+// 1.5 * 2^23 add puts j in the low mantissa bits, no F2I / FRND, which would
+// go through the XU pipe like MUFU), 2^f on [-0.5, 0.5] by a degree-3 minimax
+// polynomial (max rel. error 7.5e-5, below P's f16 rounding of 4.9e-4), and
+// 2^j added to the exponent field.  x is clamped at -126 (2^-126 rounds to 0
+// in the f16 P), so -inf masks still give 0.
+__device__ __forceinline__ float ex2_fma(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = __fadd_rn(x, 12582912.f);
+  const float f = __fsub_rn(x, __fsub_rn(t, 12582912.f));
+  const float p = fmaf(fmaf(fmaf(0.0551715f, f, 0.24261096f), f, 0.69326099f), f, 0.99992808f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+// Q of the tile's 16 key pairs per thread go to ex2_fma, spread evenly
+// (Bresenham), the rest to MUFU.EX2: the softmax warps are bound by the XU
+// pipe (MUFU: 16 exps / clk / SM, ncu XU 67%) while the FMA pipe idles.
+template <int Q>
+__device__ __forceinline__ constexpr bool att_poly_pair(int q2) {
+  return (q2 * Q) / 16 != ((q2 + 1) * Q) / 16;
+}
+
 struct AttnSmem {
   static constexpr int Q0 = 0;                       // 2 x 16 KB [128 q][64 d]
   static constexpr int K0 = 2 * 16384;               // 2 x 16 KB [128 keys][64 d]
@@ -2476,13 +2513,16 @@ struct AttnSmem {
 // sequence, Q and the O accumulator are double-buffered per item, so the next
 // item's loads and MMAs overlap the previous item's epilogue.
 constexpr int ATT_NG = 4;                            // softmax warp groups (32 keys each)
+#ifndef ATT_POLY_DEFAULT
+#define ATT_POLY_DEFAULT 4
+#endif
 #ifndef ATT_PV_N
 #define ATT_PV_N 80                                  // PV MMA width: 64 dims + ones columns
 #endif
 
 // PT: P = 2^s goes back into the S buffer's TMEM columns (tcgen05.st) and the PV
 // MMA reads it as a TMEM A operand; else P is staged in SMEM (st.shared, SW128).
-template <bool PT>
+template <bool PT, int POLY>
 __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
     const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
     const __grid_constant__ CUtensorMap map_v, int n, int hw, int heads,
@@ -2716,8 +2756,9 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
         uint32_t pw[KG / 2];
 #pragma unroll
         for (int q2 = 0; q2 < KG / 2; ++q2) {
-          __half2 h = __floats2half2_rn(ex2_approx(__uint_as_float(r[2 * q2])),
-                                        ex2_approx(__uint_as_float(r[2 * q2 + 1])));
+          const float a = __uint_as_float(r[2 * q2]), b = __uint_as_float(r[2 * q2 + 1]);
+          __half2 h = att_poly_pair<POLY>(q2) ? __floats2half2_rn(ex2_fma(a), ex2_fma(b))
+                                              : __floats2half2_rn(ex2_approx(a), ex2_approx(b));
           pw[q2] = *reinterpret_cast<uint32_t*>(&h);
         }
         tmem_st16(tmem + lanebase + s * 128 + grp * KG, pw);
@@ -3083,6 +3124,10 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
   return cuda_check("ig_conv_tc(halo)");
 }
 
+static int g_res_v8 = [] {
+  const char* e = getenv("IG_RES_V8");
+  return e ? atoi(e) : 1;
+}();
 static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
                             // 4 CTA pairs with three halo buffers, 5 no 4-row tiles,
                             // 6 separate ring for the skip chunks, 7 2-row/3-buffer out head,
@@ -3230,6 +3275,7 @@ static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   a->res_a = p->res_a; a->res_b = p->res_b; a->act_gain = p->act_gain;
   a->out0 = reinterpret_cast<__nv_bfloat16*>(p->out0);
   a->out1 = reinterpret_cast<__nv_bfloat16*>(p->out1);
+  a->res_v8 = g_res_v8;
   IG_REQUIRE(p->csa % 64 == 0 && p->csb % 64 == 0 && p->csa >= 0 && p->csb >= 0,
              "conv: skip channels must be multiples of 64");
   IG_REQUIRE(p->csa > 0 || p->csb == 0, "conv: skip_b without skip_a");
@@ -3572,14 +3618,27 @@ int ig_attention(const void* q, const void* k, const void* v, int32_t n, int32_t
   const int smem = AttnSmem::BYTES + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attention_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attention_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attention_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attention_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attention_kernel<true, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attention_kernel<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attention_kernel<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   const int64_t items = (int64_t)n * heads * ((hw + 127) / 128);
   const int ctas = (int)(items < kNumSMs ? items : kNumSMs);
-  // variant 16: P staged through SMEM (the earlier path; A/B and cross-check)
-  auto kern = g_variant == 16 ? attention_kernel<false> : attention_kernel<true>;
+  // exp2 split between MUFU and the FMA pipe: IG_ATT_POLY = key pairs (of 16
+  // per thread and tile) on ex2_fma; variant 16: P staged through SMEM
+  static int poly = -1;
+  if (poly < 0) {
+    const char* e = getenv("IG_ATT_POLY");
+    poly = e ? atoi(e) : ATT_POLY_DEFAULT;
+  }
+  auto kern = g_variant == 16 ? attention_kernel<false, 0>
+              : poly >= 8     ? attention_kernel<true, 8>
+              : poly >= 6     ? attention_kernel<true, 6>
+              : poly >= 4     ? attention_kernel<true, 4>
+                              : attention_kernel<true, 0>;
   { kern<<<(unsigned)ctas, 64 + 128 * ATT_NG, smem, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
       mq, mk, mv, n, hw, heads, reinterpret_cast<__nv_bfloat16*>(y), c); note_launch(); }
   return cuda_check("ig_attention");
