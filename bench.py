@@ -769,6 +769,11 @@ def run_cfg4(args):
     }
     m = min(args.cpu_queries, n)
     if m > 0:
+        # the UNet store's cache goes back to the allocator pool first, so the
+        # analytic store fills from reserved segments instead of growing them
+        del state, q_unet
+        import gc
+        gc.collect()
         sub = origins[:args.warmup + m]
         spec = ig.DenoiserSpec(kind="shrink_smooth", radius=1, lambdas=(0.6, 0.4))
         gst = gpu_state(spec, "analytic")

@@ -229,7 +229,7 @@ def _merge(pair: LaplacianPair, out_dtype, square: bool):
     low = _convert(low, torch.float64)
     high = _convert(high, torch.float64)
     p, h, w = _planes(high)
-    want = np.dtype(out_dtype)
+    want = _NP_OF[out_dtype] if isinstance(out_dtype, torch.dtype) else np.dtype(out_dtype)
     tdt = _TORCH_OF.get(want, torch.int64 if want.kind in "iub" else None)
     if tdt is None:
         raise ShapeError(f"unsupported decode dtype {want}")

@@ -73,3 +73,17 @@ def test_integer_signed_ops_and_box():
             acc += xp[tuple(sl)]
         want = acc / 3
     _same(transforms.box_mean(xi, 1), want)
+
+
+def test_device_tensor_pair_with_torch_dtype():
+    """A LaplacianPair built on the device may carry a torch dtype (the hierarchy
+    bench and user code do); decode keeps it."""
+    import torch
+    x = torch.from_numpy(G["x32"]).cuda()
+    pair = transforms.laplacian_encode(x, 8, 1)
+    p2 = transforms.LaplacianPair(low=pair.low, high=pair.high, factor=8, dtype=torch.float32)
+    dec = transforms.laplacian_decode(p2)
+    assert isinstance(dec, torch.Tensor) and dec.dtype == torch.float32
+    assert torch.equal(dec.cpu(), x.cpu())
+    el = transforms.laplacian_decode_signed_square(transforms.laplacian_stabilize(p2, 1))
+    assert el.dtype == torch.float32 and bool(torch.isfinite(el).all())
