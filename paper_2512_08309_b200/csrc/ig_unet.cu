@@ -2801,6 +2801,585 @@ __global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention_kernel(
   }
 }
 
+// attention2_kernel: the production attention (r02).  Same math as
+// attention_kernel (unit-RMS q / k, one pass, no running max, y = O / l with
+// l from a ones block of the PV MMA), but P no longer lives in the S buffer it
+// came from.  With P written back into S, S_{t+2} could only start once PV_t
+// had read P_t (the S buffer was released by the PV MMA's commit), so every
+// second S waited on a softmax -> PV -> commit -> S round trip and the softmax
+// warps sat on sfull (ncu: the top stall of the softmax loop).  Here:
+//   TMEM  S0/S1 [0,256) f32 scores; O0 [256,336), O1 [352,432) (64 dims + the
+//         denominator column block); P [448,512): 128 keys of f16 P, two per
+//         column, ONE buffer (P_{t+1} is stored late in softmax_{t+1}, long
+//         after PV_t, which reads P_t, has completed);
+//   S[s] is released as soon as the softmax warps have LOADED it (tcgen05.ld),
+//   so S_{t+2} overlaps softmax_t;
+//   the FMA-pipe exponentials (POLY pairs of 16 per thread) run as packed
+//   f32x2 FFMA2 / FADD2, half the issue slots of scalar FMAs;
+//   K / V rings are ATT2_KV deep (SMEM freed by the P tiles).
+constexpr int ATT2_KV = 3;
+struct Attn2Smem {
+  static constexpr int Q0 = 0;                                   // 2 x 16 KB
+  static constexpr int K0 = 2 * 16384;                           // KV x 16 KB
+  static constexpr int V0 = K0 + ATT2_KV * 16384;                // KV x 16 KB (f16, MN-major B)
+  static constexpr int ONES = V0 + ATT2_KV * 16384;              // 16 KB f16 ones (B cols 64..)
+  static constexpr int BARS = ONES + 16384;
+  static constexpr int BYTES = BARS + 512;
+};
+
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// (2^a, 2^b) for a, b in [-126, 12] on the FMA pipe, as ex2_fma, two lanes per
+// instruction: 2 FADD2 + 4 FFMA2 + 2 integer exponent adds per pair
+__device__ __forceinline__ void ex2_fma_x2(float a, float b, float& ea, float& eb) {
+  const uint64_t x = f2pack(a, b);
+  const uint64_t M = f2pack(12582912.f, 12582912.f), NM = f2pack(-12582912.f, -12582912.f);
+  const uint64_t t = fadd2(x, M);
+  const uint64_t f = ffma2(fadd2(t, NM), f2pack(-1.f, -1.f), x);      // x - rint(x)
+  uint64_t p = ffma2(f2pack(0.0551715f, 0.0551715f), f, f2pack(0.24261096f, 0.24261096f));
+  p = ffma2(p, f, f2pack(0.69326099f, 0.69326099f));
+  p = ffma2(p, f, f2pack(0.99992808f, 0.99992808f));
+  const uint32_t tl = (uint32_t)t, th = (uint32_t)(t >> 32);
+  const uint32_t pl = (uint32_t)p, ph = (uint32_t)(p >> 32);
+  ea = __uint_as_float(pl + (tl << 23));
+  eb = __uint_as_float(ph + (th << 23));
+}
+
+template <int POLY>
+__global__ void __launch_bounds__(64 + 128 * ATT_NG, 1) attention2_kernel(
+    const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+    const __grid_constant__ CUtensorMap map_v, int n, int hw, int heads,
+    __nv_bfloat16* __restrict__ y, int c) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Attn2Smem::BARS);
+  uint64_t* qfull = bars;                  // [2]
+  uint64_t* qempty = bars + 2;             // [2]
+  uint64_t* sfull = bars + 4;              // [2]
+  uint64_t* sempty = bars + 6;             // [2]  released by the softmax loads
+  uint64_t* pfull = bars + 8;              // [1]
+  uint64_t* pempty = bars + 9;             // [1]  released by the PV commit
+  uint64_t* ofull = bars + 10;             // [2]
+  uint64_t* oempty = bars + 12;            // [2]
+  uint64_t* kfull = bars + 14;             // [KV]
+  uint64_t* kempty = kfull + ATT2_KV;      // [KV]
+  uint64_t* vfull = kempty + ATT2_KV;      // [KV]
+  uint64_t* vempty = vfull + ATT2_KV;      // [KV]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(vempty + ATT2_KV);
+  constexpr int NSOFT = 128 * ATT_NG;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qtiles = (hw + 127) / 128, ktiles = (hw + 127) / 128;
+  const int nitems = n * heads * qtiles;
+  const int my_items = blockIdx.x < nitems ? (nitems - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int T = my_items * ktiles;
+  auto item_of = [&](int it, int& img, int& hd, int& qt) {
+    const int w = blockIdx.x + it * gridDim.x;
+    qt = w % qtiles;
+    hd = (w / qtiles) % heads;
+    img = w / (qtiles * heads);
+  };
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_q);
+    prefetch_map(&map_k);
+    prefetch_map(&map_v);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&qfull[s], 1);
+      mbar_init(&qempty[s], 1);
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], NSOFT);
+      mbar_init(&ofull[s], 1);
+      mbar_init(&oempty[s], NSOFT);
+    }
+    mbar_init(pfull, NSOFT);
+    mbar_init(pempty, 1);
+    for (int s = 0; s < ATT2_KV; ++s) {
+      mbar_init(&kfull[s], 1);
+      mbar_init(&kempty[s], 1);
+      mbar_init(&vfull[s], 1);
+      mbar_init(&vempty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int i = threadIdx.x; i < 16384 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(sm + Attn2Smem::ONES)[i] =
+        make_uint4(0x3C003C00u, 0x3C003C00u, 0x3C003C00u, 0x3C003C00u);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t TS = 0, TO0 = 256, TO1 = 352, TP = 448;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int it = 0, j = 0, img = 0, hd = 0, qt = 0;
+      for (int t = 0; t < T; ++t) {
+        if (j == 0) {
+          item_of(it, img, hd, qt);
+          const int qb = it & 1, qph = (it >> 1) & 1;
+          mbar_wait(&qempty[qb], qph ^ 1);
+          mbar_expect_tx(&qfull[qb], 16384);
+          tma_load_3d(sm + Attn2Smem::Q0 + qb * 16384, &map_q, &qfull[qb], hd * 64, qt * 128, img);
+        }
+        const int ks = t % ATT2_KV, kph = (t / ATT2_KV) & 1;
+        mbar_wait(&kempty[ks], kph ^ 1);
+        mbar_expect_tx(&kfull[ks], 16384);
+        tma_load_3d(sm + Attn2Smem::K0 + ks * 16384, &map_k, &kfull[ks], hd * 64, j * 128, img);
+        mbar_wait(&vempty[ks], kph ^ 1);
+        mbar_expect_tx(&vfull[ks], 16384);
+        tma_load_3d(sm + Attn2Smem::V0 + ks * 16384, &map_v, &vfull[ks], hd * 64, j * 128, img);
+        if (++j == ktiles) { j = 0; ++it; }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc_s = idesc_bf16(128, 128);
+    constexpr uint32_t idesc_o = (1u << 4) | (1u << 16) | ((uint32_t)(ATT_PV_N >> 3) << 17) |
+                                 ((uint32_t)(128 >> 4) << 24);
+    auto issue_s = [&](int t, int it, int j) {
+      const int qb = it & 1;
+      const int s = t & 1, ph = (t >> 1) & 1;
+      const int ks = t % ATT2_KV, kph = (t / ATT2_KV) & 1;
+      if (j == 0) mbar_wait(&qfull[qb], (it >> 1) & 1);
+      mbar_wait(&kfull[ks], kph);
+      mbar_wait(&sempty[s], ph ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t qdesc = smem_desc_sw128(smem_u32(sm + Attn2Smem::Q0 + qb * 16384));
+        const uint64_t kdesc = smem_desc_sw128(smem_u32(sm + Attn2Smem::K0 + ks * 16384));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc_mma(tmem + TS + s * 128, qdesc + 2 * kk, kdesc + 2 * kk, idesc_s, kk ? 1u : 0u);
+        tc_commit(&kempty[ks]);
+        tc_commit(&sfull[s]);
+        if (j == ktiles - 1) tc_commit(&qempty[qb]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int t, int it, int j) {
+      const int ob = it & 1;
+      const int ks = t % ATT2_KV, kph = (t / ATT2_KV) & 1;
+      if (j == 0) mbar_wait(&oempty[ob], ((it >> 1) & 1) ^ 1);
+      mbar_wait(&vfull[ks], kph);
+      mbar_wait(pfull, t & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t lbo = (uint32_t)(Attn2Smem::ONES - (Attn2Smem::V0 + ks * 16384));
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {          // keys [16kk, 16kk+16): P columns 8kk..8kk+7
+          const uint32_t vaddr = smem_u32(sm + Attn2Smem::V0 + ks * 16384 + (kk * 16) * 128);
+          const uint64_t vdesc = (smem_desc_sw128_mn(vaddr) & ~(0x3FFFull << 16)) |
+                                 ((uint64_t)((lbo >> 4) & 0x3FFF) << 16);
+          tc_mma_ts(tmem + (ob ? TO1 : TO0), tmem + TP + 8 * kk, vdesc, idesc_o,
+                    (j | kk) ? 1u : 0u);
+        }
+        tc_commit(pempty);
+        tc_commit(&vempty[ks]);
+        if (j == ktiles - 1) tc_commit(&ofull[ob]);
+      }
+      __syncwarp();
+    };
+    if (T > 0) issue_s(0, 0, 0);
+    int it = 0, j = 0, it1 = ktiles > 1 ? 0 : 1, j1 = ktiles > 1 ? 1 : 0;   // (it1, j1): tile t+1
+    for (int t = 0; t < T; ++t) {
+      if (t + 1 < T) issue_s(t + 1, it1, j1);
+      issue_pv(t, it, j);
+      if (++j == ktiles) { j = 0; ++it; }
+      if (++j1 == ktiles) { j1 = 0; ++it1; }
+    }
+  } else {
+    // ---------------- softmax / epilogue (warps 2 .. 2 + 4*ATT_NG) ----------------
+    constexpr int KG = 128 / ATT_NG, DG = 64 / ATT_NG;
+    static_assert(KG == 32 && DG == 16, "one 32x32b.x16 P store / O load per group");
+    const int quarter = warp & 3;
+    const int grp = (warp - 2) >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t lanebase = (uint32_t)(quarter * 32) << 16;
+    auto item_epilogue = [&](int e) {         // y = O / l of item e (l = O column 64)
+      int img, hd, qt;
+      item_of(e, img, hd, qt);
+      const int ob = e & 1;
+      mbar_wait(&ofull[ob], (e >> 1) & 1);
+      tc_fence_after();
+      float o[DG], lrow[16];
+      const uint32_t tob = tmem + lanebase + (ob ? TO1 : TO0);
+      tmem_ld16(tob + grp * DG, o);
+      tmem_ld16(tob + 64, lrow);
+      tc_fence_before();
+      mbar_arrive(&oempty[ob]);
+      const float inv_l = 1.f / lrow[0];
+      if (qt * 128 + row < hw) {
+        __nv_bfloat16* dst = y + ((int64_t)img * hw + qt * 128 + row) * c + hd * 64 + grp * DG;
+        uint4 u[2];
+        __nv_bfloat162* ob2 = reinterpret_cast<__nv_bfloat162*>(u);
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2)
+          ob2[q2] = __floats2bfloat162_rn(o[2 * q2] * inv_l, o[2 * q2 + 1] * inv_l);
+        stg_v8(dst, u[0], u[1]);
+      }
+    };
+    int it = 0, j = 0;
+    for (int t = 0; t < T; ++t) {
+      const int s = t & 1, ph = (t >> 1) & 1;
+      mbar_wait(&sfull[s], ph);
+      tc_fence_after();
+      uint32_t r[KG];
+      tmem_ld32_nw(tmem + lanebase + TS + s * 128 + grp * KG, r);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&sempty[s]);               // S[s] is free for S_{t+2}
+      const int kvalid = hw - j * 128 - grp * KG;
+      if (kvalid < KG) {                      // keys past the image: 2^-126 -> 0 in f16
+#pragma unroll
+        for (int kk = 0; kk < KG; ++kk)
+          if (kk >= kvalid) r[kk] = __float_as_uint(-126.f);
+      }
+      uint32_t pw[KG / 2];
+#pragma unroll
+      for (int q2 = 0; q2 < KG / 2; ++q2) {
+        const float a = __uint_as_float(r[2 * q2]), b = __uint_as_float(r[2 * q2 + 1]);
+        float ea, eb;
+        if (att_poly_pair<POLY>(q2)) {
+          ex2_fma_x2(a, b, ea, eb);
+        } else {
+          ea = ex2_approx(a);
+          eb = ex2_approx(b);
+        }
+        __half2 h = __floats2half2_rn(ea, eb);
+        pw[q2] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      mbar_wait(pempty, (t & 1) ^ 1);        // PV_{t-1} is done with P
+      tc_fence_after();
+      tmem_st16(tmem + lanebase + TP + grp * (KG / 2), pw);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(pfull);
+      // the O / l epilogue of item it-1 runs after this item's first tile (O is
+      // double-buffered), so the item's last PV completes under this softmax
+      if (j == 0 && it > 0) item_epilogue(it - 1);
+      if (++j == ktiles) { j = 0; ++it; }
+    }
+    if (my_items > 0) item_epilogue(my_items - 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// attention3_kernel: the production attention (r02), a ping-pong of two
+// softmax warp sets.  The softmax of one tile is MUFU-bound (16 exp2 / clk /
+// SM, measured) but 16 warps in lock-step on one tile leave the MUFU idle
+// while they all wait for S, load it, store P and signal: ncu XU ~55%.  Here
+// set A (8 warps) takes the even tiles of the CTA's sequence and set B the odd
+// ones, each warp 64 keys of its 32 query rows, so one set's loads / stores /
+// barrier waits overlap the other set's exponentials.
+//   TMEM  S0 (set A) / S1 (set B) [0,256); O0/O1 [256,384) 64 f32 dims, double
+//         buffered across items; P0/P1 [384,512) f16 P, two keys per column;
+//   S[σ] is released by set σ's loads, P[σ] by the PV MMA's commit;
+//   row denominators: f32x2 sums in the softmax threads (P in f16 for the MMA),
+//   combined from the four (set, key half) partials through SMEM once per
+//   item; the item's y = O / l is written by the set that starts the next item;
+//   exp2: POLY of the 32 key pairs per thread on the FMA pipe (ex2_fma_x2).
+constexpr int ATT3_KV = 4;   // K / V ring depth of attention3_kernel
+struct Attn3Smem {
+  static constexpr int Q0 = 0;                                   // 2 x 16 KB
+  static constexpr int K0 = 2 * 16384;                           // KV x 16 KB
+  static constexpr int V0 = K0 + ATT3_KV * 16384;                // KV x 16 KB (f16, MN-major B)
+  static constexpr int L0 = V0 + ATT3_KV * 16384;                // [2 items][2 sets][2 halves][128]
+  static constexpr int BARS = L0 + 2 * 4 * 128 * 4;
+  static constexpr int BYTES = BARS + 512;
+};
+
+template <int POLY>
+__global__ void __launch_bounds__(96 + 128 * ATT_NG, 1) attention3_kernel(
+    const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+    const __grid_constant__ CUtensorMap map_v, int n, int hw, int heads,
+    __nv_bfloat16* __restrict__ y, int c, int flags) {
+  static_assert(ATT_NG == 4, "two sets x two key halves x four lane quarters");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Attn3Smem::BARS);
+  uint64_t* qfull = bars;                  // [2]
+  uint64_t* qempty = bars + 2;             // [2]
+  uint64_t* sfull = bars + 4;              // [2] per set
+  uint64_t* sempty = bars + 6;             // [2] per set: released by the set's loads
+  uint64_t* pfull = bars + 8;              // [2] per set
+  uint64_t* pempty = bars + 10;            // [2] per set: released by the PV commit
+  uint64_t* ofull = bars + 12;             // [2]
+  uint64_t* oempty = bars + 14;            // [2]
+  uint64_t* lready = bars + 16;            // [2] the item's row-sum partials are in SMEM
+  uint64_t* turn = bars + 18;              // [2] set s may start its exponentials
+  uint64_t* kfull = bars + 20;             // [KV]
+  uint64_t* kempty = kfull + ATT3_KV;
+  uint64_t* vfull = kempty + ATT3_KV;
+  uint64_t* vempty = vfull + ATT3_KV;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(vempty + ATT3_KV);
+  float* lpart = reinterpret_cast<float*>(sm + Attn3Smem::L0);
+  constexpr int NSET = 256;                // threads per softmax set
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qtiles = (hw + 127) / 128, ktiles = (hw + 127) / 128;
+  const int nitems = n * heads * qtiles;
+  const int my_items = blockIdx.x < nitems ? (nitems - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int T = my_items * ktiles;
+  auto item_of = [&](int it, int& img, int& hd, int& qt) {
+    const int w = blockIdx.x + it * gridDim.x;
+    qt = w % qtiles;
+    hd = (w / qtiles) % heads;
+    img = w / (qtiles * heads);
+  };
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_q);
+    prefetch_map(&map_k);
+    prefetch_map(&map_v);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&qfull[s], 1);
+      mbar_init(&qempty[s], 1);
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], NSET);
+      mbar_init(&pfull[s], NSET);
+      mbar_init(&pempty[s], 1);
+      mbar_init(&ofull[s], 1);
+      mbar_init(&oempty[s], NSET);
+      // every softmax thread whose set sees a tile of the item arrives once
+      mbar_init(&lready[s], ktiles >= 2 ? 2 * NSET : NSET);
+      mbar_init(&turn[s], NSET);
+    }
+    for (int s = 0; s < ATT3_KV; ++s) {
+      mbar_init(&kfull[s], 1);
+      mbar_init(&kempty[s], 1);
+      mbar_init(&vfull[s], 1);
+      mbar_init(&vempty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t TS = 0, TO = 256, TP = 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int it = 0, j = 0, img = 0, hd = 0, qt = 0;
+      for (int t = 0; t < T; ++t) {
+        if (j == 0) {
+          item_of(it, img, hd, qt);
+          const int qb = it & 1, qph = (it >> 1) & 1;
+          mbar_wait(&qempty[qb], qph ^ 1);
+          mbar_expect_tx(&qfull[qb], 16384);
+          tma_load_3d(sm + Attn3Smem::Q0 + qb * 16384, &map_q, &qfull[qb], hd * 64, qt * 128, img);
+        }
+        const int ks = t % ATT3_KV, kph = (t / ATT3_KV) & 1;
+        mbar_wait(&kempty[ks], kph ^ 1);
+        mbar_expect_tx(&kfull[ks], 16384);
+        tma_load_3d(sm + Attn3Smem::K0 + ks * 16384, &map_k, &kfull[ks], hd * 64, j * 128, img);
+        mbar_wait(&vempty[ks], kph ^ 1);
+        mbar_expect_tx(&vfull[ks], 16384);
+        tma_load_3d(sm + Attn3Smem::V0 + ks * 16384, &map_v, &vfull[ks], hd * 64, j * 128, img);
+        if (++j == ktiles) { j = 0; ++it; }
+      }
+    }
+  } else if (warp == 1 || warp == 2) {
+    // ---------------- MMA issuers: warp 1 the S = Q K^T MMAs, warp 2 the O += P V
+    // MMAs.  With one issuer, S(t+2) waited in program order behind PV(t)'s wait
+    // for P(t) and the softmax sets were starved of scores (ncu: their top stall
+    // was sfull); tcgen05.commit tracks the issuing thread's own MMAs, so the two
+    // streams are independent.
+    constexpr uint32_t idesc_s = idesc_bf16(128, 128);
+    constexpr uint32_t idesc_o = (1u << 4) | (1u << 16) | ((uint32_t)(64 >> 3) << 17) |
+                                 ((uint32_t)(128 >> 4) << 24);
+    int it = 0, j = 0;
+    for (int t = 0; t < T; ++t) {
+      const int s = t & 1, ph = (t >> 1) & 1;
+      const int ks = t % ATT3_KV, kph = (t / ATT3_KV) & 1;
+      if (warp == 1) {
+        const int qb = it & 1;
+        if (j == 0) mbar_wait(&qfull[qb], (it >> 1) & 1);
+        mbar_wait(&kfull[ks], kph);
+        mbar_wait(&sempty[s], ph ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t qdesc = smem_desc_sw128(smem_u32(sm + Attn3Smem::Q0 + qb * 16384));
+          const uint64_t kdesc = smem_desc_sw128(smem_u32(sm + Attn3Smem::K0 + ks * 16384));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma(tmem + TS + s * 128, qdesc + 2 * kk, kdesc + 2 * kk, idesc_s, kk ? 1u : 0u);
+          tc_commit(&kempty[ks]);
+          tc_commit(&sfull[s]);
+          if (j == ktiles - 1) tc_commit(&qempty[qb]);
+        }
+        __syncwarp();
+      } else {
+        const int ob = it & 1;
+        if (j == 0) mbar_wait(&oempty[ob], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&vfull[ks], kph);
+        mbar_wait(&pfull[s], ph);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {          // keys [16kk, 16kk+16): P columns 8kk..
+            const uint32_t vaddr = smem_u32(sm + Attn3Smem::V0 + ks * 16384 + (kk * 16) * 128);
+            tc_mma_ts(tmem + TO + ob * 64, tmem + TP + s * 64 + 8 * kk,
+                      smem_desc_sw128_mn(vaddr), idesc_o, (j | kk) ? 1u : 0u);
+          }
+          tc_commit(&pempty[s]);
+          tc_commit(&vempty[ks]);
+          if (j == ktiles - 1) tc_commit(&ofull[ob]);
+        }
+        __syncwarp();
+      }
+      if (++j == ktiles) { j = 0; ++it; }
+    }
+  } else {
+    // ---------------- softmax sets / epilogue (warps 3 .. 18) ----------------
+    const int quarter = warp & 3;               // TMEM lane quarter of this warp
+    const int half = ((warp - 3) >> 2) & 1;     // keys [64 half, +64) of the set's tiles
+    const int set = (warp - 3) >> 3;            // tiles t with t % 2 == set
+    const int row = quarter * 32 + lane;
+    const uint32_t lanebase = (uint32_t)(quarter * 32) << 16;
+    auto lslot = [&](int e, int st, int hf) { return lpart + (((e & 1) * 2 + st) * 2 + hf) * 128; };
+    auto item_epilogue = [&](int e) {           // y = O / l of item e, by this set
+      int img, hd, qt;
+      item_of(e, img, hd, qt);
+      const int ob = e & 1;
+      mbar_wait(&lready[ob], (e >> 1) & 1);
+      float l = 0.f;
+      const int first_set = (e * ktiles) & 1;
+#pragma unroll
+      for (int st = 0; st < 2; ++st) {
+        if (ktiles < 2 && st != first_set) continue;   // this set saw no tile of item e
+        l += lslot(e, st, 0)[row] + lslot(e, st, 1)[row];
+      }
+      mbar_wait(&ofull[ob], (e >> 1) & 1);
+      tc_fence_after();
+      uint32_t o[32];
+      tmem_ld32_nw(tmem + lanebase + TO + ob * 64 + 32 * half, o);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&oempty[ob]);
+      const float inv_l = 1.f / l;
+      if (qt * 128 + row < hw) {
+        __nv_bfloat16* dst = y + ((int64_t)img * hw + qt * 128 + row) * c + hd * 64 + 32 * half;
+#pragma unroll
+        for (int q4 = 0; q4 < 2; ++q4) {
+          uint4 u[2];
+          __nv_bfloat162* ob2 = reinterpret_cast<__nv_bfloat162*>(u);
+#pragma unroll
+          for (int q2 = 0; q2 < 8; ++q2)
+            ob2[q2] = __floats2bfloat162_rn(__uint_as_float(o[16 * q4 + 2 * q2]) * inv_l,
+                                            __uint_as_float(o[16 * q4 + 2 * q2 + 1]) * inv_l);
+          stg_v8(dst + 16 * q4, u[0], u[1]);
+        }
+      }
+    };
+    uint64_t lacc = f2pack(0.f, 0.f);
+    int it = set / ktiles, j = set % ktiles;   // tile t = set: (item, key tile)
+    int k = 0;                                  // this set's tile counter
+    for (int t = set; t < T; t += 2, ++k) {
+      const int ph = (t >> 1) & 1;
+      mbar_wait(&sfull[set], ph);
+      tc_fence_after();
+      uint32_t r[64];
+      tmem_ld32_nw(tmem + lanebase + TS + set * 128 + 64 * half, r);
+      tmem_ld32_nw(tmem + lanebase + TS + set * 128 + 64 * half + 32, r + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&sempty[set]);             // S[set] is free for this set's next tile
+      const int kvalid = hw - j * 128 - half * 64;
+      if (kvalid < 64) {                      // keys past the image: 2^-126 -> 0 in f16
+#pragma unroll
+        for (int kk = 0; kk < 64; ++kk)
+          if (kk >= kvalid) r[kk] = __float_as_uint(-126.f);
+      }
+      // the two sets take turns on the MUFU: A's k-th exponentials follow B's
+      // (k-1)-th, B's k-th follow A's k-th (both sets would otherwise receive
+      // their scores together and stay in lock-step)
+      if (flags & 1) {
+        if (set == 0) {
+          if (k > 0) mbar_wait(&turn[0], (k - 1) & 1);
+        } else {
+          mbar_wait(&turn[1], k & 1);
+        }
+      }
+      uint32_t pw[32];
+#pragma unroll
+      for (int q2 = 0; q2 < 32; ++q2) {
+        const float a = __uint_as_float(r[2 * q2]), b = __uint_as_float(r[2 * q2 + 1]);
+        float ea, eb;
+        if (att_poly_pair<POLY>(q2 & 15)) {       // POLY of every 16 pairs
+          ex2_fma_x2(a, b, ea, eb);
+        } else {
+          ea = ex2_approx(a);
+          eb = ex2_approx(b);
+        }
+        lacc = fadd2(lacc, f2pack(ea, eb));
+        __half2 h = __floats2half2_rn(ea, eb);
+        pw[q2] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      if (flags & 1) mbar_arrive(&turn[set ^ 1]);
+      mbar_wait(&pempty[set], ph ^ 1);       // PV of this set's previous tile is done
+      tc_fence_after();
+      tmem_st16(tmem + lanebase + TP + set * 64 + 32 * half, pw);
+      tmem_st16(tmem + lanebase + TP + set * 64 + 32 * half + 16, pw + 16);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&pfull[set]);
+      // the item's last tile seen by this set: publish the row-sum partial
+      const int jn = j + 2;                   // this set's next key tile of the same item
+      if (jn >= ktiles) {
+        const float2 v = make_float2(__uint_as_float((uint32_t)lacc),
+                                     __uint_as_float((uint32_t)(lacc >> 32)));
+        lslot(it, set, half)[row] = v.x + v.y;
+        lacc = f2pack(0.f, 0.f);
+        mbar_arrive(&lready[it & 1]);
+      }
+      // the set that starts item it writes item it-1's y (O is double-buffered)
+      if (j == 0 && it > 0) item_epilogue(it - 1);
+      j += 2;
+      while (j >= ktiles) { j -= ktiles; ++it; }
+    }
+    if (my_items > 0 && (T & 1) == set) item_epilogue(my_items - 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 __global__ void unet_output_kernel(const __nv_bfloat16* __restrict__ f, int n, int h, int w,
                                    int fc, const float* __restrict__ x_noisy, int C,
                                    float c_skip, float c_out, float* __restrict__ out) {
@@ -3623,6 +4202,16 @@ int ig_attention(const void* q, const void* k, const void* v, int32_t n, int32_t
     cudaFuncSetAttribute(attention_kernel<true, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attention_kernel<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(attention_kernel<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int smem2 = Attn2Smem::BYTES + 1024;
+    cudaFuncSetAttribute(attention2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    cudaFuncSetAttribute(attention2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    cudaFuncSetAttribute(attention2_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    cudaFuncSetAttribute(attention2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    const int smem3 = Attn3Smem::BYTES + 1024;
+    cudaFuncSetAttribute(attention3_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+    cudaFuncSetAttribute(attention3_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+    cudaFuncSetAttribute(attention3_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+    cudaFuncSetAttribute(attention3_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
     attr = true;
   }
   const int64_t items = (int64_t)n * heads * ((hw + 127) / 128);
@@ -3634,6 +4223,37 @@ int ig_attention(const void* q, const void* k, const void* v, int32_t n, int32_t
     const char* e = getenv("IG_ATT_POLY");
     poly = e ? atoi(e) : ATT_POLY_DEFAULT;
   }
+  if (g_variant != 16 && g_variant != 17 && g_variant != 18) {
+    // production: two ping-pong softmax sets (attention3_kernel)
+    auto k3 = poly >= 8 ? attention3_kernel<8>
+              : poly >= 6 ? attention3_kernel<6>
+              : poly >= 4 ? attention3_kernel<4>
+                          : attention3_kernel<0>;
+    static int aflags = -1;
+    if (aflags < 0) {
+      const char* e = getenv("IG_ATT_FLAGS");
+      aflags = e ? atoi(e) : 1;
+    }
+    k3<<<(unsigned)ctas, 96 + 128 * ATT_NG, Attn3Smem::BYTES + 1024,
+         reinterpret_cast<cudaStream_t>(cuda_stream)>>>(mq, mk, mv, n, hw, heads,
+                                                        reinterpret_cast<__nv_bfloat16*>(y), c,
+                                                        aflags);
+    note_launch();
+    return cuda_check("ig_attention");
+  }
+  if (g_variant == 18) {
+    // P in its own TMEM buffer, one softmax set (attention2_kernel)
+    auto k2 = poly >= 8 ? attention2_kernel<8>
+              : poly >= 6 ? attention2_kernel<6>
+              : poly >= 4 ? attention2_kernel<4>
+                          : attention2_kernel<0>;
+    k2<<<(unsigned)ctas, 64 + 128 * ATT_NG, Attn2Smem::BYTES + 1024,
+         reinterpret_cast<cudaStream_t>(cuda_stream)>>>(mq, mk, mv, n, hw, heads,
+                                                        reinterpret_cast<__nv_bfloat16*>(y), c);
+    note_launch();
+    return cuda_check("ig_attention");
+  }
+  // variant 17: P written back into its S buffer (r01 kernel); 16: P staged in SMEM
   auto kern = g_variant == 16 ? attention_kernel<false, 0>
               : poly >= 8     ? attention_kernel<true, 8>
               : poly >= 6     ? attention_kernel<true, 6>

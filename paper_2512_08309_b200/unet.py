@@ -420,6 +420,11 @@ class UNetDevice:
         gut = self._gutter(lv, w)   # (x, xa) in the gutter layout
         for k in range(1, len(ops)):
             op = ops[k]
+            nxt = ops[k + 1][0] if k + 1 < len(ops) else None
+            # a block output feeding an attention block is only read as x (the
+            # attention returns a new (x, mp_silu(x))); the output layer only
+            # reads mp_silu(x): those tensors are not written at all
+            want0, want1 = nxt != "out", nxt != "attn"
             if op[0] == "enc":
                 nm = op[1]
                 g = int(gut)
@@ -437,7 +442,8 @@ class UNetDevice:
                             torch.empty(shp, dtype=torch.bfloat16, device=h1.device))
                     g |= 4 * int(ng)
                 x, xa = self.conv(nm + ".c2", h1, None, sigma, skip=(x,), wskip=wsk,
-                                  scale=self._rb(c2.cout_pad), gutter=g, pool=pool)
+                                  scale=self._rb(c2.cout_pad), gutter=g, pool=pool,
+                                  out0=want0 or pool is not None, out1=want1)
                 skips.append((x, xa))
             elif op[0] == "attn":
                 x, xa = self.attention(op[1], x)
@@ -467,7 +473,8 @@ class UNetDevice:
                 # epilogue directly, but its 4x scattered stores measured slower
                 # (r01: 132 vs 121 ms/step) than the separate coalesced kernel)
                 x, xa = self.conv(nm + ".c2", h1, None, sigma, skip=(x, s), wskip=wsk,
-                                  scale=self._rb(c2.cout_pad), up_in=2 if up else 0, gutter=g)
+                                  scale=self._rb(c2.cout_pad), up_in=2 if up else 0, gutter=g,
+                                  out0=want0, out1=want1)
                 up = 0
             elif op[0] == "up":
                 ng = self._gutter(lv - 1, 2 * w)

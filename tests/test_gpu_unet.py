@@ -726,8 +726,11 @@ def test_conv_qkv_fused_equals_three_launches(n, h, w):
 
 @pytest.mark.parametrize("n,hw,c", [(2, 1024, 256), (1, 200, 128)])
 def test_attention_p_in_tmem_matches_smem_path(n, hw, c):
-    """The default attention kernel keeps P in TMEM (tcgen05.st, TS-MMA); variant
-    16 stages P through SMEM.  Same P values and MMAs: the outputs agree."""
+    """The default attention kernel (attention2_kernel) keeps P in its own TMEM
+    buffers and sums the softmax denominators in the softmax warps; variant 17
+    writes P back into its S buffer and takes the denominator from a ones block
+    of the PV MMA (r01); variant 16 stages P through SMEM.  Same P values: the
+    outputs agree to bf16 rounding."""
     g = torch.Generator(device=DEV).manual_seed(hw * 3 + c)
     q, k, v = ((torch.randn(n, hw, c, device=DEV, generator=g) * s).bfloat16()
                for s in (1.3, 0.7, 1.0))
@@ -735,7 +738,7 @@ def test_attention_p_in_tmem_matches_smem_path(n, hw, c):
     call("ig_attn_prep", q.data_ptr(), k.data_ptr(), v.data_ptr(), n, hw, c, None, st)
     ys = []
     try:
-        for variant in (0, 16):
+        for variant in (0, 16, 17):
             check(lib().ig_conv_set_variant(variant))
             y = torch.empty(n, hw, c, device=DEV, dtype=torch.bfloat16)
             call("ig_attention", q.data_ptr(), k.data_ptr(), v.data_ptr(), n, hw, c,
@@ -745,3 +748,4 @@ def test_attention_p_in_tmem_matches_smem_path(n, hw, c):
         check(lib().ig_conv_set_variant(0))
     torch.cuda.synchronize()
     assert (ys[0] - ys[1]).abs().max().item() < 1e-2
+    assert (ys[0] - ys[2]).abs().max().item() < 1e-2

@@ -43,7 +43,9 @@ def layer_ops(cfg, win):
     seq = [] if fused else [("gather", "gather", win, 0, cfg.cin_pad, 0, 1, 0)]
     h = win
     c = ch[0]
-    for op in prog.ops:
+    for k, op in enumerate(prog.ops):
+        nxt = prog.ops[k + 1][0] if k + 1 < len(prog.ops) else None
+        c2_outs = 1 if nxt in ("attn", "out") else 2     # unet.forward_after_stem
         if op[0] == "stem":
             # fused: reads the f32 source plane(s), writes x_noisy (f32) + x/xa
             seq.append(("conv", "stem", h, cfg.cin_pad, ch[0], 1, 2, 0))
@@ -53,7 +55,7 @@ def layer_ops(cfg, win):
             seq.append(("conv", nm + ".c1", h, c1.cin, c1.cout, 9, 1, 0))
             c2 = prog.convs[nm + ".c2"]
             # c2 with the fused skip GEMM: reads the block input (c1.cin) once more
-            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, 2, c1.cin / c2.cout))
+            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, c2_outs, c1.cin / c2.cout))
             c = c2.cout
         elif op[0] == "attn":
             nm = op[1]
@@ -72,7 +74,7 @@ def layer_ops(cfg, win):
             c1 = prog.convs[nm + ".c1"]
             seq.append(("conv", nm + ".c1", h, c1.cin, c1.cout, 9, 1, 0))
             c2 = prog.convs[nm + ".c2"]
-            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, 2, c1.cin / c2.cout))
+            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, c2_outs, c1.cin / c2.cout))
             c = c2.cout
         elif op[0] == "up":
             if not (unet.FUSED_UP and (2 * h) % 128 == 0):   # else folded into the TMA loads
