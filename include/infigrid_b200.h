@@ -18,6 +18,7 @@
  *   ig_blur_block_mean_f64 transforms.py:54-67 (block_mean of blur3_iterated, float64)
  *   ig_block_mean          transforms.py:61-67 block_mean (float32 / float64 accumulation)
  *   ig_upsample_nn         transforms.py:70-72 upsample_nn
+ *   ig_normalize_u8        transforms.py:117-135 normalize_heightmap_u8 (render path)
  *   ig_convert             numpy astype at transforms.py:93,101 (dtype-preserving decode)
  *   ig_laplacian_residual  transforms.py:89-95 (high = x - up(low))
  *   ig_laplacian_merge     transforms.py:98-101 / :104-114 (up(low)+high [, signed_square])
@@ -183,6 +184,10 @@ int ig_block_mean(const void* in, int32_t dtype, int32_t planes, int32_t h, int3
  * float -> int truncates) */
 int ig_convert(const void* in, int32_t in_dtype, int64_t n, void* out, int32_t out_dtype,
                void* cuda_stream);
+/* normalize_heightmap_u8 (transforms.py:117-135): in (images, hw) float32 or
+ * float64, out (images, 3, hw) uint8; minmax: device scratch of 2*images u64 */
+int ig_normalize_u8(const void* in, int32_t dtype, int32_t images, int64_t hw, void* minmax,
+                    uint8_t* out, void* cuda_stream);
 /* upsample_nn (transforms.py:70-72): out[p][Y][X] = in[p][Y/f][X/f], any
  * element size (1/2/4/8 bytes) */
 int ig_upsample_nn(const void* in, int32_t elem_bytes, int64_t planes, int32_t h, int32_t w,

@@ -955,6 +955,66 @@ static bool with_dtype(int32_t dtype, F&& f) {
   }
 }
 
+
+// ---------------------------------------------------------------------
+// render normalisation (transforms.py:117-135 normalize_heightmap_u8): per
+// image min / max (exact in any order; doubles mapped to order-preserving
+// 64-bit keys for the atomics), then ((x - mid) / range + 0.5) * 255 clipped,
+// rounded half-to-even (rint) and replicated to 3 channels -- every step an
+// IEEE f64 operation, so the bytes equal numpy's
+__device__ __forceinline__ unsigned long long f64_key(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double f64_unkey(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k));
+}
+__global__ void minmax_init_kernel(unsigned long long* mm, int b) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < b) { mm[2 * i] = ~0ull; mm[2 * i + 1] = 0ull; }
+}
+template <typename T>
+__global__ void __launch_bounds__(256) minmax_kernel(const T* __restrict__ in, int64_t hw,
+                                                     unsigned long long* __restrict__ mm) {
+  const int img = blockIdx.y;
+  const T* p = in + (int64_t)img * hw;
+  double lo = INFINITY, hi = -INFINITY;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hw;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = (double)p[i];
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mm[2 * img], f64_key(lo));
+    atomicMax(&mm[2 * img + 1], f64_key(hi));
+  }
+}
+template <typename T>
+__global__ void __launch_bounds__(256) normalize_u8_kernel(const T* __restrict__ in, int64_t hw,
+                                                           const unsigned long long* __restrict__ mm,
+                                                           uint8_t* __restrict__ out) {
+  const int img = blockIdx.y;
+  const double mn = f64_unkey(mm[2 * img]), mx = f64_unkey(mm[2 * img + 1]);
+  const double rng = fmax(rsub(mx, mn), 255.0);
+  const double mid = rdiv(radd(mn, mx), 2.0);
+  const T* p = in + (int64_t)img * hw;
+  uint8_t* o = out + (int64_t)img * 3 * hw;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hw;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = rmul(radd(rdiv(rsub((double)p[i], mid), rng), 0.5), 255.0);
+    v = fmin(fmax(v, 0.0), 255.0);
+    const uint8_t u = (uint8_t)rint(v);
+    o[i] = u;
+    o[hw + i] = u;
+    o[2 * hw + i] = u;
+  }
+}
 }  // namespace ig
 
 // =====================================================================
@@ -1251,6 +1311,26 @@ int ig_convert(const void* in, int32_t in_dtype, int64_t n, void* out, int32_t o
   });
   IG_REQUIRE(ok_in && ok_out, "convert: unknown dtype pair %d -> %d", in_dtype, out_dtype);
   return cuda_check("ig_convert");
+}
+
+int ig_normalize_u8(const void* in, int32_t dtype, int32_t images, int64_t hw, void* minmax,
+                    uint8_t* out, void* cuda_stream) {
+  IG_REQUIRE(dtype == IG_DTYPE_F32 || dtype == IG_DTYPE_F64, "normalize_u8: float input");
+  if (images <= 0 || hw <= 0) return IG_OK;
+  IG_REQUIRE(images <= 65535, "normalize_u8: at most 65535 images per call");
+  cudaStream_t st = as_stream(cuda_stream);
+  unsigned long long* mm = (unsigned long long*)minmax;
+  { minmax_init_kernel<<<(images + 255) / 256, 256, 0, st>>>(mm, images); note_launch(); }
+  const int bx = grid_for(hw, 256, 4 > images ? 4 : 1);
+  const dim3 grid((unsigned)bx, (unsigned)images);
+  if (dtype == IG_DTYPE_F32) {
+    minmax_kernel<float><<<grid, 256, 0, st>>>((const float*)in, hw, mm); note_launch();
+    normalize_u8_kernel<float><<<grid, 256, 0, st>>>((const float*)in, hw, mm, out); note_launch();
+  } else {
+    minmax_kernel<double><<<grid, 256, 0, st>>>((const double*)in, hw, mm); note_launch();
+    normalize_u8_kernel<double><<<grid, 256, 0, st>>>((const double*)in, hw, mm, out); note_launch();
+  }
+  return cuda_check("ig_normalize_u8");
 }
 
 int ig_upsample_nn(const void* in, int32_t elem_bytes, int64_t planes, int32_t h, int32_t w,

@@ -260,20 +260,29 @@ def laplacian_stabilize(pair: LaplacianPair, blur_radius: int = 1) -> LaplacianP
     return LaplacianPair(low_hat, pair.high, pair.factor, pair.dtype)
 
 
-def normalize_heightmap_u8(batch) -> np.ndarray:
-    """Algorithm 2 render normalisation (transforms.py:117-135).
-
-    Out of the throughput path; evaluated on the host.
-    """
-    b = np.asarray(batch.detach().cpu().numpy() if isinstance(batch, torch.Tensor) else batch,
-                   dtype=np.float64)
-    if b.ndim == 3:
-        b = b[:, None]
-    if b.ndim != 4 or b.shape[1] != 1:
-        raise ShapeError(f"expected (B, 1, H, W) or (B, H, W), got {b.shape}")
-    lo = b.min(axis=(-2, -1), keepdims=True)
-    hi = b.max(axis=(-2, -1), keepdims=True)
-    span = np.maximum(hi - lo, 255.0)
-    centre = (lo + hi) / 2.0
-    scaled = np.clip(((b - centre) / span + 0.5) * 255.0, 0.0, 255.0)
-    return np.repeat(np.rint(scaled).astype(np.uint8), 3, axis=1)
+def normalize_heightmap_u8(batch):
+    """Algorithm 2 render normalisation (transforms.py:117-135) on the device:
+    per image, centre on (min + max) / 2, scale by max(range, 255), shift to
+    [0, 255], round half to even, clamp, replicate to 3 channels (uint8).
+    Every step is an IEEE float64 operation, so the bytes equal numpy's.
+    numpy in -> numpy out; a CUDA tensor stays on the device."""
+    was_dev = isinstance(batch, torch.Tensor)
+    if was_dev:
+        t = batch.contiguous()
+        if t.dtype not in (torch.float32, torch.float64):
+            t = _convert(t, torch.float64)
+    else:
+        arr = np.asarray(batch)
+        if arr.dtype not in (np.float32, np.float64):
+            arr = arr.astype(np.float64)         # numpy's float64 view of the input
+        t = dev.upload(np.ascontiguousarray(arr))
+    if t.dim() == 3:
+        t = t[:, None]
+    if t.dim() != 4 or t.shape[1] != 1:
+        raise ShapeError(f"expected (B, 1, H, W) or (B, H, W), got {tuple(t.shape)}")
+    b, _, h, w = t.shape
+    out = torch.empty((b, 3, h, w), dtype=torch.uint8, device=t.device)
+    mm = torch.empty(2 * max(b, 1), dtype=torch.int64, device=t.device)
+    call("ig_normalize_u8", t.data_ptr(), _dt(t), b, h * w, mm.data_ptr(), out.data_ptr(),
+         dev.stream_ptr())
+    return out if was_dev else dev.download(out)

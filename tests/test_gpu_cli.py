@@ -60,7 +60,7 @@ def test_render_signed_square_golden(cli_golden, tmp_path):
     _, z, _ = cli_golden
     raster = str(tmp_path / "r.bin")
     save_raster(raster, z["render_in"])
-    for tag, extra in (("ssq", ["--signed-square"]),
+    for tag, extra in (("plain", []), ("ssq", ["--signed-square"]),
                        ("ssq_hill", ["--signed-square", "--hillshade"])):
         out = str(tmp_path / f"{tag}.pgm")
         assert cli.main(["render", raster, out] + extra) == 0
@@ -114,3 +114,41 @@ def test_dense_helpers():
     from paper_2512_08309_b200.grid import windows_overlapping
     assert dense.brute_force_windows(lay, r, 6) == set(windows_overlapping(lay, r))
     assert dense.count_denoiser_calls_naive(2, lay, Region(0, 0, 16, 16)) == 9 + 9 * 9
+
+
+def test_render_constant_is_128(tmp_path):
+    raster = str(tmp_path / "r.bin")
+    out = str(tmp_path / "r.pgm")
+    save_raster(raster, np.full((1, 8, 8), 100.0, dtype=np.float32))
+    assert cli.main(["render", raster, out]) == 0
+    data = open(out, "rb").read()
+    assert data.startswith(b"P5\n8 8\n255\n") and set(data.split(b"\n", 3)[3]) == {128}
+
+
+def test_normalize_heightmap_u8_device_matches_numpy():
+    """ig_normalize_u8 against the reference's float64 expression
+    (transforms.py:117-135), for f64 and f32 batches, wide and narrow ranges,
+    half-way ties and a constant image."""
+    from paper_2512_08309_b200 import transforms
+
+    def ref(b):
+        b = np.asarray(b, dtype=np.float64)
+        if b.ndim == 3:
+            b = b[:, None]
+        mins = b.min(axis=(-2, -1), keepdims=True)
+        maxs = b.max(axis=(-2, -1), keepdims=True)
+        rng = np.maximum(maxs - mins, 255.0)
+        mid = (mins + maxs) / 2.0
+        norm = np.clip(((b - mid) / rng + 0.5) * 255.0, 0.0, 255.0)
+        return np.repeat(np.rint(norm).astype(np.uint8), 3, axis=1)
+
+    rng_ = np.random.default_rng(5)
+    cases = [rng_.normal(size=(3, 37, 53)) * 3000.0,
+             (rng_.normal(size=(2, 1, 64, 40)) * 40.0).astype(np.float32),
+             np.full((1, 9, 7), -12.5),
+             np.arange(2 * 16 * 16, dtype=np.float64).reshape(2, 16, 16) * 0.5]   # ties
+    for b in cases:
+        got = transforms.normalize_heightmap_u8(b)
+        want = ref(b)
+        assert got.dtype == np.uint8 and got.shape == want.shape
+        np.testing.assert_array_equal(got, want)

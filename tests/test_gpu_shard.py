@@ -14,7 +14,12 @@ from paper_2512_08309_b200.grid import Region, WindowLayout  # noqa: E402
 
 
 def _cfg(kind, steps, H, s):
-    if kind == "unet":
+    if kind == "unet_prod":
+        # the bench's network: default UNetConfig (attention at 32^2, CTA-pair
+        # four-row kernels at 256^2, gutter layout at 64^2)
+        from paper_2512_08309_b200.unet import UNetConfig
+        spec = ig.DenoiserSpec(kind="unet", unet=UNetConfig())
+    elif kind == "unet":
         from paper_2512_08309_b200.unet import UNetConfig
         spec = ig.DenoiserSpec(kind="unet", unet=UNetConfig(base=64, mults=(1, 2), blocks=1))
     else:
@@ -28,6 +33,7 @@ def _cfg(kind, steps, H, s):
     ("shrink", 3, 16, 8, 4, (0, 0, 64, 96)),
     ("shrink", 2, 256, 128, 2, (0, 0, 512, 768)),
     ("unet", 2, 64, 32, 2, (0, 0, 128, 192)),
+    ("unet_prod", 2, 256, 128, 3, (-256, 128, 512, 768)),
 ])
 def test_sharded_equals_single(kind, steps, H, s, world, region):
     cfg = _cfg(kind, steps, H, s)
@@ -86,6 +92,7 @@ def _ipc_worker(rank, world, port_, kind, steps, H, s, region, q):
     ("shrink", 2, 16, 8, 2, (-37, 11, 70, 90)),
     ("shrink", 3, 16, 8, 3, (0, 0, 64, 96)),
     ("unet", 2, 64, 32, 2, (0, 0, 128, 192)),
+    ("unet_prod", 2, 256, 128, 2, (0, 0, 512, 512)),
 ])
 def test_ipc_exchange_bitwise(kind, steps, H, s, world, region):
     import multiprocessing as mp
