@@ -840,6 +840,7 @@ struct HaloArgs {
   int sbufs;         // CTA-pair kernel: separate ring for the 1x1 skip chunks (0: they
                      // ride in the halo ring)
   int l2pf;          // CTA-pair kernel: L2-prefetch the next tile's halo boxes
+  int l2pf_skip;     // CTA-pair kernel: L2-prefetch the next tile's 1x1 skip-GEMM boxes
 };
 
 template <int N, int ROWS>
@@ -1128,6 +1129,19 @@ __device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int c0, 
                "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_5d(const CUtensorMap* map, int c0, int c1, int c2,
+                                                int c3, int c4) {
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 __device__ __forceinline__ void tma2_load_5d(void* dst, const CUtensorMap* map, uint32_t bar,
                                              int c0, int c1, int c2, int c3, int c4) {
   asm volatile(
@@ -1288,6 +1302,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         const int r = tile - img * tiles_per_img;
         const int ty = r / ha.tiles_x;
         const int x0 = (r - ty * ha.tiles_x) * 128, y0 = ty * ROWS;
+        if (ha.l2pf_skip && kskip) {
+          // warm L2 with the next tile's 1x1 skip-GEMM boxes: each skip chunk is
+          // only ~8 MMAs, consumed far faster than an HBM round trip, so with
+          // them riding in the two-slot halo ring every skip chunk of a tile
+          // stalled the MMAs on its load (ncu dec1.0.c2: tensor pipe 66%)
+          const int prn = pr + pstride;
+          if (prn < npairs) {
+            const int tn = 2 * prn + (int)rank;
+            const int imgn = tn / tiles_per_img;
+            const int rn = tn - imgn * tiles_per_img;
+            if (imgn < args.n) {
+              for (int ks = 0; ks < kskip; ++ks) {
+                const bool sa = ks < args.kskip_a;
+                const CUtensorMap* m = sa ? &map_sa : &map_sb;
+                const int c = (sa ? ks : ks - args.kskip_a) * 64;
+                if constexpr (GUT) {
+                  tma_prefetch_3d(m, c, rn * ROWS * 128, imgn);
+                } else {
+                  const int tyn = rn / ha.tiles_x;
+                  const int x0n = (rn - tyn * ha.tiles_x) * 128, y0n = tyn * ROWS;
+                  if (sa && args.up_sa)
+                    tma_prefetch_5d(m, c, 0, x0n / 2, y0n >> 1, imgn);
+                  else
+                    tma_prefetch_4d(m, c, x0n, y0n, imgn);
+                }
+              }
+            }
+          }
+        }
         if constexpr (!GUT) {
           // warm L2 with the next tile's halo boxes: with two halo buffers a box is
           // loaded only one tile ahead, too little to hide an HBM round trip
@@ -3707,6 +3750,13 @@ static int g_res_v8 = [] {
   const char* e = getenv("IG_RES_V8");
   return e ? atoi(e) : 1;
 }();
+// L2 prefetch of the next tile's skip-GEMM boxes: measured slower on every c2
+// layer (r02 A/B, tools/ab_layers.sh: dec1.0.c2 979 -> 901 TFLOP/s, forward
+// 7.05 -> 7.24 ms per 64 windows); off unless IG_L2PF_SKIP=1
+static int g_l2pf_skip = [] {
+  const char* e = getenv("IG_L2PF_SKIP");
+  return e ? atoi(e) : 0;
+}();
 static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
                             // 4 CTA pairs with three halo buffers, 5 no 4-row tiles,
                             // 6 separate ring for the skip chunks, 7 2-row/3-buffer out head,
@@ -3771,6 +3821,7 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   // r01 A/B: enc0.0.c2 452 -> 420 us; multi-chunk and N = 128 layers measured
   // slower with it); variant 12: off
   ha.l2pf = g_variant != 12 && N == 64 && a.kchunks_a + a.kchunks_b == 1;
+  ha.l2pf_skip = g_l2pf_skip;
   if (GUT) {
     ha.tiles_x = 1;
     ha.tiles_y = (a.gP + ROWS * 128 - 1) / (ROWS * 128);
