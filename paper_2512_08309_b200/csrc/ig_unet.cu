@@ -1198,7 +1198,20 @@ constexpr int GBOX = 136;                    // positions per gutter TMA box (8-
 // boxes per gutter halo: ROWS*128 + 2(w+3) positions, w <= 64
 __host__ __device__ constexpr int gboxes(int rows) { return rows == 1 ? 2 : 3; }
 
-template <int N, int ROWS, bool GUT>
+// DYN (cout 64, two-row tiles, 3x3 without skip chunks): the three dy taps go
+// in N.  Halo row h feeds output rows h+1, h, h-1 through W[0], W[1], W[2]
+// (dx fixed); with the two accumulator rows laid out in DECREASING row order,
+// one MMA of N = 128 (or 64 at the box edges) against [W[a]; W[a+1]] covers
+// both output rows the halo row feeds.  Per K16 step an SM's tensor core then
+// reads 16 KB of A for 192 MMA cycles instead of 24 KB for 192 (the per-tap
+// schedule re-read each halo row once per output row): the N = 64 layers were
+// SMEM-read bound (A 4 KB + B 1 KB per 32-cycle MMA, 160 B/clk against 128).
+// Per (chunk, dx) each CTA stages four weight views at the same offsets in both
+// CTAs of the pair (cta_group::2 reads rows [0, N/2) of B from the even CTA and
+// [N/2, N) from the odd one): V128a = [W0; W1], V128b = [W1; W2], V64a = W0,
+// V64b = W2 -- CTA r holds its half of each (24 KB per (chunk, dx)).
+constexpr int DYN_BLK = 6 * 4096;
+template <int N, int ROWS, bool GUT, bool DYN = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     conv_halo2_kernel(const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b,
@@ -1219,12 +1232,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   const int kskip = args.kskip_a + args.kskip_b;
   const int nchunks = kchunks + kskip;
   constexpr uint32_t SKIP_TX = ROWS * 128 * 128;
-  const int nb = ha.resident ? 9 * kchunks + kskip : ha.b_stages;
+  static_assert(!DYN || (N == 64 && ROWS == 2 && !GUT), "DYN: cout 64, two-row 2-D tiles");
+  constexpr int WBLK = DYN ? DYN_BLK : BH_BYTES;   // one staged weight unit
+  const int nb = ha.resident ? (DYN ? 3 * kchunks : 9 * kchunks + kskip) : ha.b_stages;
   constexpr int SBYTES = ROWS * 128 * 128;   // one skip chunk: the tile's pixels, no halo
   uint8_t* sH = smem;
   uint8_t* sS = smem + ha.hbufs * HBYTES;      // skip ring (ha.sbufs slots)
   uint8_t* sB = sS + ha.sbufs * SBYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + nb * BH_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + nb * WBLK);
   const int HB = ha.hbufs, SB = ha.sbufs;
   uint64_t* hfull = bars;          // [HB] (leader's used)
   uint64_t* hempty = bars + 4;     // [HB] (each CTA's own)
@@ -1284,7 +1299,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       // ---------------- TMA producer (both CTAs) ----------------
       const uint32_t l_wfull = mapa_u32(wfull, 0);
       const int brow = (int)rank * BH;
-      if (ha.resident) {
+      // DYN: the four views of weight unit (chunk kc, dx) for this CTA (see above)
+      auto load_dyn = [&](uint8_t* dst, int kc, int dx, uint32_t bar) {
+        const int k0 = kc * 64;
+        const int kin = args.ca + args.cb;
+        const int r = (int)rank;
+        // V128a: W[r] rows 0..63; V128b: W[1+r]; V64a: W0 rows 32r..; V64b: W2 rows 32r..
+        const int dys[6] = {r, r, 1 + r, 1 + r, 0, 2};
+        const int rows[6] = {0, 32, 0, 32, 32 * r, 32 * r};
+#pragma unroll
+        for (int q = 0; q < 6; ++q)
+          tma2_load_2d(dst + q * 4096, &map_w, bar, (dys[q] * 3 + dx) * kin + k0, rows[q]);
+      };
+      if (DYN && ha.resident) {
+        if (leader) mbar_expect_tx(wfull, (uint32_t)(2 * 3 * kchunks * DYN_BLK));
+        for (int kc = 0; kc < kchunks; ++kc)
+          for (int dx = 0; dx < 3; ++dx) load_dyn(sB + (kc * 3 + dx) * DYN_BLK, kc, dx, l_wfull);
+      } else if (ha.resident) {
         if (leader) mbar_expect_tx(wfull, (uint32_t)(2 * (9 * kchunks + kskip) * BH_BYTES));
         for (int t = 0; t < 9 * kchunks; ++t) {
           const int tap = t / kchunks, kc = t - tap * kchunks;
@@ -1410,7 +1441,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             hs = 0;
             hph ^= 1;
           }
-          if (!ha.resident) {
+          if (DYN && !ha.resident) {
+            for (int dx = 0; dx < 3; ++dx) {
+              mbar_wait(&bempty[bs], bph ^ 1);
+              if (leader) mbar_expect_tx(&bfull[bs], 2 * DYN_BLK);
+              load_dyn(sB + bs * DYN_BLK, kc, dx, mapa_u32(&bfull[bs], 0));
+              if (++bs == ha.b_stages) { bs = 0; bph ^= 1; }
+            }
+          } else if (!ha.resident) {
             const int ntaps = kc < kchunks ? 9 : 1;
             for (int tap = 0; tap < ntaps; ++tap) {
               mbar_wait(&bempty[bs], bph ^ 1);
@@ -1451,7 +1489,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           const uint32_t hbase = smem_u32(sring ? sS + ss * SBYTES : sH + hs * HBYTES);
           const bool upc = skipc ? (kc - kchunks < args.kskip_a && args.up_sa)
                                  : (kc < args.kchunks_a && args.up_a);
-          const int ntaps = skipc ? 1 : 9;
+          if constexpr (DYN) {
+            // halo rows in the order 1, 0, 2, 3: the first MMA of a tile (chunk 0,
+            // dx 0, halo row 1: N = 128 over both accumulator rows) initialises them
+            constexpr uint32_t id128 = idesc_bf16(256, 128), id64 = idesc_bf16(256, 64);
+            for (int dx = 0; dx < 3; ++dx) {
+              uint32_t wbase;
+              if (ha.resident) {
+                wbase = smem_u32(sB + (kc * 3 + dx) * DYN_BLK);
+              } else {
+                mbar_wait(&bfull[bs], bph);
+                tc_fence_after();
+                wbase = smem_u32(sB + bs * DYN_BLK);
+              }
+              if (elect_one()) {
+#pragma unroll
+                for (int o = 0; o < 4; ++o) {
+                  const int hr = o == 0 ? 1 : (o == 1 ? 0 : o);
+                  const int prow = upc ? (((y0 + hr - 1) >> 1) - ylo0) * 132 + dx + 1
+                                       : hr * 130 + dx;
+                  const uint64_t adesc = smem_desc_sw128(hbase + prow * 128);
+                  // V128a at 0, V128b at 8 KB, V64a at 16 KB, V64b at 20 KB
+                  const uint32_t voff = hr == 0 ? 16384u : hr == 1 ? 0u : hr == 2 ? 8192u : 20480u;
+                  const uint64_t bdesc = smem_desc_sw128(wbase + voff);
+                  const uint32_t dcol = hr == 0 ? (uint32_t)N : 0u;   // row y0 sits at column N
+                  const uint32_t id = (hr == 1 || hr == 2) ? id128 : id64;
+#pragma unroll
+                  for (int kq = 0; kq < 4; ++kq)
+                    tc_mma2(d0 + dcol, adesc + 2 * kq, bdesc + 2 * kq, id,
+                            (kc | dx | o | kq) ? 1u : 0u);
+                }
+                if (!ha.resident) tc_commit2_mc(&bempty[bs]);
+              }
+              __syncwarp();
+              if (!ha.resident) {
+                if (++bs == ha.b_stages) { bs = 0; bph ^= 1; }
+              }
+            }
+          }
+          const int ntaps = DYN ? 0 : (skipc ? 1 : 9);
           for (int tap = 0; tap < ntaps; ++tap) {
             const int dy = tap / 3, dx = tap % 3;
             uint32_t baddr;
@@ -1550,8 +1626,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
 #pragma unroll
           for (int row = grp; row < ROWS; row += 2) {
             const int64_t p = ((int64_t)img * args.h + y0 + row) * args.w + x0 + m;
-            const uint32_t taddr =
-                tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N + row * N;
+            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N +
+                                   (DYN ? (ROWS - 1 - row) : row) * N;
             epi_span<N>(args, args.scale ? s_scale : nullptr, p, 0, taddr);
           }
         }
@@ -3773,7 +3849,7 @@ static int make_w_map_rows(CUtensorMap* m, const void* base, int ktot, int cout,
   return r == CUDA_SUCCESS ? IG_OK : IG_ERR_CUDA;
 }
 
-template <int N, int ROWS, bool GUT>
+template <int N, int ROWS, bool GUT, bool DYN = false>
 static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaStream_t st) {
   using Cfg = HaloCfg<N, ROWS>;
   constexpr int BH_BYTES = N / 2 * 128;
@@ -3831,7 +3907,8 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   }
   ha.c.num_tiles = p->n * ha.tiles_x * ha.tiles_y;
   const int kchunks = a.kchunks_a + a.kchunks_b;
-  const int wbytes = (9 * kchunks + a.kskip_a + a.kskip_b) * BH_BYTES;
+  const int wbytes = DYN ? 3 * kchunks * DYN_BLK : (9 * kchunks + a.kskip_a + a.kskip_b) * BH_BYTES;
+  const int wunit = DYN ? DYN_BLK : BH_BYTES;
   // two halo buffers with resident weights where they fit (variant 4: try
   // three buffers, the next tile's box streaming in during the whole tile)
   constexpr int kBudget = 226 * 1024;
@@ -3856,13 +3933,13 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
       ha.b_stages = 1;
       smem = fixed + wbytes;
     } else {
-      int stages = (kBudget - fixed) / BH_BYTES;
+      int stages = (kBudget - fixed) / wunit;
       if (stages > 16) stages = 16;
       if (stages >= (hb == 3 ? 4 : 2)) {
         ha.hbufs = hb;
         ha.resident = 0;
         ha.b_stages = stages;
-        smem = fixed + stages * BH_BYTES;
+        smem = fixed + stages * wunit;
       }
     }
   }
@@ -3872,13 +3949,13 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(conv_halo2_kernel<N, ROWS, GUT>,
+    cudaFuncSetAttribute(conv_halo2_kernel<N, ROWS, GUT, DYN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   const int ctas = 2 * ((ha.c.num_tiles + 1) / 2);
   const int grid = ctas < kNumSMs ? ctas : kNumSMs;
-  { conv_halo2_kernel<N, ROWS, GUT><<<grid, Cfg::THREADS, smem, st>>>(ma, mb, mw, msa, msb, mws, ha); note_launch(); }
+  { conv_halo2_kernel<N, ROWS, GUT, DYN><<<grid, Cfg::THREADS, smem, st>>>(ma, mb, mw, msa, msb, mws, ha); note_launch(); }
   return cuda_check("ig_conv_tc(halo2)");
 }
 
@@ -4011,6 +4088,10 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
     // (enc0.0.c1 347 -> 324, enc0.0.c2 418 -> 389, dec0.1.c2 548 -> 493 us per
     // 64 windows).  Variant 15: the earlier rule, four rows only for the
     // multi-chunk layers.
+    // cout-64 3x3 convs without a skip GEMM (the c1 layers of the 256^2 level):
+    // the dy taps in N (DYN); any A/B variant (e.g. 19): the per-tap schedule
+    if (p->cout == 64 && a.kskip_a + a.kskip_b == 0 && !p->pool0 && g_variant == 0)
+      return launch_conv_halo2<64, 2, false, true>(p, a, st);
     const bool deep = g_variant != 15 || a.kchunks_a + a.kchunks_b >= 2 ||
                       a.kskip_a + a.kskip_b >= 3;
     if (p->cout == 64 && deep && p->h % 4 == 0 && g_variant != 5 &&
