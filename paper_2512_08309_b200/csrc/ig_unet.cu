@@ -3833,6 +3833,10 @@ static int g_l2pf_skip = [] {
   const char* e = getenv("IG_L2PF_SKIP");
   return e ? atoi(e) : 0;
 }();
+static int g_halo3 = [] {
+  const char* e = getenv("IG_HALO3");
+  return e ? atoi(e) : 0;
+}();
 static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
                             // 4 CTA pairs with three halo buffers, 5 no 4-row tiles,
                             // 6 separate ring for the skip chunks, 7 2-row/3-buffer out head,
@@ -3924,8 +3928,15 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
     for (int sb = (kskip >= 2 ? 2 : 1); sb >= 1 && !ha.sbufs; --sb)
       if (1024 + 2 * HBYTES + sb * SBYTES + 512 + 1024 + wbytes <= kBudget) ha.sbufs = sb;
   }
-  // (r01: three buffers measured slower -- the weights then stream per tile)
-  for (int hb = (g_variant == 4 ? 3 : 2); hb >= 2 && !ha.hbufs; --hb) {
+  // (r01: three buffers measured slower for the layers whose weights are
+  // resident with two -- they then stream per tile).  Layers that stream their
+  // weights anyway (multi-chunk cout 128) may take a third halo slot, so a short
+  // skip chunk's load is two chunks ahead (IG_HALO3=1 / variant 4 to force it).
+  // Measured slower (r02, tools/ab_layers.sh: dec1.0.c1 1608 -> 1439, dec1.1.c2
+  // 1039 -> 976 TFLOP/s; the weight ring drops to 3 stages), so off by default.
+  const bool streams2 = 1024 + 2 * HBYTES + 512 + 1024 + wbytes > kBudget;
+  const bool try3 = g_variant == 4 || (g_halo3 && streams2 && !DYN && !GUT && N == 128);
+  for (int hb = try3 ? 3 : 2; hb >= 2 && !ha.hbufs; --hb) {
     const int fixed = 1024 + hb * HBYTES + ha.sbufs * SBYTES + 512 + 1024;
     if (fixed + wbytes <= kBudget) {
       ha.hbufs = hb;
@@ -3935,7 +3946,7 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
     } else {
       int stages = (kBudget - fixed) / wunit;
       if (stages > 16) stages = 16;
-      if (stages >= (hb == 3 ? 4 : 2)) {
+      if (stages >= (hb == 3 ? 3 : 2)) {
         ha.hbufs = hb;
         ha.resident = 0;
         ha.b_stages = stages;
