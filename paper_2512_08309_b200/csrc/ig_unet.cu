@@ -4352,7 +4352,9 @@ int ig_attention(const void* q, const void* k, const void* v, int32_t n, int32_t
     cudaFuncSetAttribute(attention2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
     const int smem3 = Attn3Smem::BYTES + 1024;
     cudaFuncSetAttribute(attention3_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+    cudaFuncSetAttribute(attention3_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
     cudaFuncSetAttribute(attention3_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+    cudaFuncSetAttribute(attention3_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
     cudaFuncSetAttribute(attention3_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
     cudaFuncSetAttribute(attention3_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
     attr = true;
@@ -4370,7 +4372,9 @@ int ig_attention(const void* q, const void* k, const void* v, int32_t n, int32_t
     // production: two ping-pong softmax sets (attention3_kernel)
     auto k3 = poly >= 8 ? attention3_kernel<8>
               : poly >= 6 ? attention3_kernel<6>
-              : poly >= 4 ? attention3_kernel<4>
+              : poly == 5 ? attention3_kernel<5>
+              : poly == 4 ? attention3_kernel<4>
+              : poly == 3 ? attention3_kernel<3>
                           : attention3_kernel<0>;
     static int aflags = -1;
     if (aflags < 0) {
