@@ -1234,12 +1234,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   constexpr uint32_t SKIP_TX = ROWS * 128 * 128;
   static_assert(!DYN || (N == 64 && ROWS == 2 && !GUT), "DYN: cout 64, two-row 2-D tiles");
   constexpr int WBLK = DYN ? DYN_BLK : BH_BYTES;   // one staged weight unit
-  const int nb = ha.resident ? (DYN ? 3 * kchunks : 9 * kchunks + kskip) : ha.b_stages;
   constexpr int SBYTES = ROWS * 128 * 128;   // one skip chunk: the tile's pixels, no halo
   uint8_t* sH = smem;
   uint8_t* sS = smem + ha.hbufs * HBYTES;      // skip ring (ha.sbufs slots)
   uint8_t* sB = sS + ha.sbufs * SBYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + nb * WBLK);
+  // resident DYN weights: 3 * kchunks units of DYN_BLK, then kskip 1x1 units
+  const int wres = DYN ? 3 * kchunks * DYN_BLK + kskip * BH_BYTES
+                       : (9 * kchunks + kskip) * BH_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (ha.resident ? wres : ha.b_stages * WBLK));
   const int HB = ha.hbufs, SB = ha.sbufs;
   uint64_t* hfull = bars;          // [HB] (leader's used)
   uint64_t* hempty = bars + 4;     // [HB] (each CTA's own)
@@ -1312,9 +1314,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           tma2_load_2d(dst + q * 4096, &map_w, bar, (dys[q] * 3 + dx) * kin + k0, rows[q]);
       };
       if (DYN && ha.resident) {
-        if (leader) mbar_expect_tx(wfull, (uint32_t)(2 * 3 * kchunks * DYN_BLK));
+        if (leader) mbar_expect_tx(wfull, (uint32_t)(2 * wres));
         for (int kc = 0; kc < kchunks; ++kc)
           for (int dx = 0; dx < 3; ++dx) load_dyn(sB + (kc * 3 + dx) * DYN_BLK, kc, dx, l_wfull);
+        for (int ks = 0; ks < kskip; ++ks)
+          tma2_load_2d(sB + 3 * kchunks * DYN_BLK + ks * BH_BYTES, &map_ws, l_wfull, ks * 64, brow);
       } else if (ha.resident) {
         if (leader) mbar_expect_tx(wfull, (uint32_t)(2 * (9 * kchunks + kskip) * BH_BYTES));
         for (int t = 0; t < 9 * kchunks; ++t) {
@@ -1442,10 +1446,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             hph ^= 1;
           }
           if (DYN && !ha.resident) {
-            for (int dx = 0; dx < 3; ++dx) {
+            for (int dx = 0; dx < (kc < kchunks ? 3 : 1); ++dx) {
               mbar_wait(&bempty[bs], bph ^ 1);
-              if (leader) mbar_expect_tx(&bfull[bs], 2 * DYN_BLK);
-              load_dyn(sB + bs * DYN_BLK, kc, dx, mapa_u32(&bfull[bs], 0));
+              const uint32_t bb = mapa_u32(&bfull[bs], 0);
+              if (kc < kchunks) {
+                if (leader) mbar_expect_tx(&bfull[bs], 2 * DYN_BLK);
+                load_dyn(sB + bs * DYN_BLK, kc, dx, bb);
+              } else {                          // a 1x1 skip unit in a ring slot
+                if (leader) mbar_expect_tx(&bfull[bs], 2 * BH_BYTES);
+                tma2_load_2d(sB + bs * DYN_BLK, &map_ws, bb, (kc - kchunks) * 64, brow);
+              }
               if (++bs == ha.b_stages) { bs = 0; bph ^= 1; }
             }
           } else if (!ha.resident) {
@@ -1490,10 +1500,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           const bool upc = skipc ? (kc - kchunks < args.kskip_a && args.up_sa)
                                  : (kc < args.kchunks_a && args.up_a);
           if constexpr (DYN) {
+            constexpr uint32_t id128 = idesc_bf16(256, 128), id64 = idesc_bf16(256, 64);
+            if (skipc) {
+              // 1x1 skip chunk: one N = 64 MMA per accumulator row (row rr at
+              // column (ROWS - 1 - rr) * N)
+              uint32_t wbase;
+              if (ha.resident) {
+                wbase = smem_u32(sB + 3 * kchunks * DYN_BLK + (kc - kchunks) * BH_BYTES);
+              } else {
+                mbar_wait(&bfull[bs], bph);
+                tc_fence_after();
+                wbase = smem_u32(sB + bs * DYN_BLK);
+              }
+              if (elect_one()) {
+                const uint64_t bdesc = smem_desc_sw128(wbase);
+#pragma unroll
+                for (int rr = 0; rr < ROWS; ++rr) {
+                  const int prow = upc ? (rr >> 1) * 128 : rr * 128;
+                  const uint64_t adesc = smem_desc_sw128(hbase + prow * 128);
+#pragma unroll
+                  for (int kq = 0; kq < 4; ++kq)
+                    tc_mma2(d0 + (ROWS - 1 - rr) * N, adesc + 2 * kq, bdesc + 2 * kq, id64, 1u);
+                }
+                if (!ha.resident) tc_commit2_mc(&bempty[bs]);
+              }
+              __syncwarp();
+              if (!ha.resident) {
+                if (++bs == ha.b_stages) { bs = 0; bph ^= 1; }
+              }
+            }
             // halo rows in the order 1, 0, 2, 3: the first MMA of a tile (chunk 0,
             // dx 0, halo row 1: N = 128 over both accumulator rows) initialises them
-            constexpr uint32_t id128 = idesc_bf16(256, 128), id64 = idesc_bf16(256, 64);
-            for (int dx = 0; dx < 3; ++dx) {
+            for (int dx = 0; dx < (skipc ? 0 : 3); ++dx) {
               uint32_t wbase;
               if (ha.resident) {
                 wbase = smem_u32(sB + (kc * 3 + dx) * DYN_BLK);
@@ -3837,6 +3875,14 @@ static int g_halo3 = [] {
   const char* e = getenv("IG_HALO3");
   return e ? atoi(e) : 0;
 }();
+// DYN also for the cout-64 convs with skip chunks (the c2 layers, two-row
+// tiles instead of four): measured neutral-to-slower (r02, tools/ab_layers.sh:
+// dec0.0.c2 625 -> 594, dec0.1.c2 695 -> 669 TFLOP/s; these layers are HBM
+// bound and the two-row halo reads more), so off unless IG_DYN_SKIP=1
+static int g_dyn_skip = [] {
+  const char* e = getenv("IG_DYN_SKIP");
+  return e ? atoi(e) : 0;
+}();
 static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
                             // 4 CTA pairs with three halo buffers, 5 no 4-row tiles,
                             // 6 separate ring for the skip chunks, 7 2-row/3-buffer out head,
@@ -3911,7 +3957,8 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   }
   ha.c.num_tiles = p->n * ha.tiles_x * ha.tiles_y;
   const int kchunks = a.kchunks_a + a.kchunks_b;
-  const int wbytes = DYN ? 3 * kchunks * DYN_BLK : (9 * kchunks + a.kskip_a + a.kskip_b) * BH_BYTES;
+  const int wbytes = DYN ? 3 * kchunks * DYN_BLK + (a.kskip_a + a.kskip_b) * BH_BYTES
+                        : (9 * kchunks + a.kskip_a + a.kskip_b) * BH_BYTES;
   const int wunit = DYN ? DYN_BLK : BH_BYTES;
   // two halo buffers with resident weights where they fit (variant 4: try
   // three buffers, the next tile's box streaming in during the whole tile)
@@ -4101,7 +4148,7 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
     // multi-chunk layers.
     // cout-64 3x3 convs without a skip GEMM (the c1 layers of the 256^2 level):
     // the dy taps in N (DYN); any A/B variant (e.g. 19): the per-tap schedule
-    if (p->cout == 64 && a.kskip_a + a.kskip_b == 0 && !p->pool0 && g_variant == 0)
+    if (p->cout == 64 && !p->pool0 && g_variant == 0 && g_dyn_skip >= (a.kskip_a + a.kskip_b ? 1 : 0))
       return launch_conv_halo2<64, 2, false, true>(p, a, st);
     const bool deep = g_variant != 15 || a.kchunks_a + a.kchunks_b >= 2 ||
                       a.kskip_a + a.kskip_b >= 3;
