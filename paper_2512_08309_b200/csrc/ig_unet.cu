@@ -841,6 +841,7 @@ struct HaloArgs {
                      // ride in the halo ring)
   int l2pf;          // CTA-pair kernel: L2-prefetch the next tile's halo boxes
   int l2pf_skip;     // CTA-pair kernel: L2-prefetch the next tile's 1x1 skip-GEMM boxes
+  int pair_skip;     // CTA-pair kernel: two 1x1 skip chunks per halo slot
 };
 
 template <int N, int ROWS>
@@ -1231,6 +1232,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   const int kchunks = args.kchunks_a + args.kchunks_b;
   const int kskip = args.kskip_a + args.kskip_b;
   const int nchunks = kchunks + kskip;
+  // two 1x1 skip chunks ride in one halo slot when both fit: a lone skip chunk
+  // is only a few MMAs, consumed long before the next slot's load returns
+  const bool pair_skip = ha.pair_skip && ha.sbufs == 0 && kskip >= 2 &&
+                         2 * ROWS * 128 * 128 <= (GUT ? gboxes(ROWS) * GBOX * 128
+                                                      : HaloCfg<N, ROWS>::HALO_BYTES);
   constexpr uint32_t SKIP_TX = ROWS * 128 * 128;
   static_assert(!DYN || (N == 64 && ROWS == 2 && !GUT), "DYN: cout 64, two-row 2-D tiles");
   constexpr int WBLK = DYN ? DYN_BLK : BH_BYTES;   // one staged weight unit
@@ -1388,32 +1394,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             }
           }
         }
+        // one skip chunk's box: returns its bytes (per CTA)
+        auto load_skip = [&](int ks, uint8_t* dst, uint32_t hb) -> uint32_t {
+          if constexpr (GUT) {
+            const int q0 = r * ROWS * 128;
+            if (ks < args.kskip_a)
+              tma2_load_3d(dst, &map_sa, hb, ks * 64, q0, img);
+            else
+              tma2_load_3d(dst, &map_sb, hb, (ks - args.kskip_a) * 64, q0, img);
+            return ROWS * 128 * 128;
+          } else {
+            if (ks < args.kskip_a && args.up_sa) {
+              // the tile's ROWS upsampled rows (y0 even when ROWS >= 2) are
+              // max(1, ROWS/2) low-res rows
+              tma2_load_5d(dst, &map_sa, hb, ks * 64, 0, x0 / 2, y0 >> 1, img);
+              return (ROWS >= 2 ? ROWS / 2 : 1) * 128 * 128;
+            }
+            if (ks < args.kskip_a)
+              tma2_load_4d(dst, &map_sa, hb, ks * 64, x0, y0, img);
+            else
+              tma2_load_4d(dst, &map_sb, hb, (ks - args.kskip_a) * 64, x0, y0, img);
+            return SKIP_TX;
+          }
+        };
         for (int kc = 0; kc < nchunks; ++kc) {
           const bool sring = SB && kc >= kchunks;    // skip chunk in its own ring
+          const int ks = kc - kchunks;
+          // paired skip chunks share one halo slot: the even one loads both
+          const bool opening = !(pair_skip && ks >= 0) || (ks & 1) == 0;
+          const bool closing = !(pair_skip && ks >= 0) || (ks & 1) == 1 || kc == nchunks - 1;
+          if (opening) {
           uint64_t* fb = sring ? &sfull[ss] : &hfull[hs];
           mbar_wait(sring ? &sempty[ss] : &hempty[hs], (sring ? sph : hph) ^ 1);
           uint8_t* dst = sring ? sS + ss * SBYTES : sH + hs * HBYTES;
           const uint32_t hb = mapa_u32(fb, 0);
-          if constexpr (GUT) {
-            // (a dummy tile has img == n: out of range, zero filled, bytes still counted)
+          if (kc >= kchunks) {
+            // (a dummy GUT tile has img == n: out of range, zero filled, bytes counted)
+            uint32_t tx = load_skip(ks, dst, hb);
+            if (pair_skip && ks + 1 < kskip) tx += load_skip(ks + 1, dst + SBYTES, hb);
+            if (leader) mbar_expect_tx(fb, 2 * tx);
+          } else if constexpr (GUT) {
             const int q0 = r * ROWS * 128;
-            if (kc < kchunks) {
-              if (leader) mbar_expect_tx(fb, 2 * HBYTES);
-              const CUtensorMap* m = kc < args.kchunks_a ? &map_a : &map_b;
-              const int c = (kc < args.kchunks_a ? kc : kc - args.kchunks_a) * 64;
-              const int start = q0 - (args.w + 3);
+            if (leader) mbar_expect_tx(fb, 2 * HBYTES);
+            const CUtensorMap* m = kc < args.kchunks_a ? &map_a : &map_b;
+            const int c = (kc < args.kchunks_a ? kc : kc - args.kchunks_a) * 64;
+            const int start = q0 - (args.w + 3);
 #pragma unroll
-              for (int bx = 0; bx < gboxes(ROWS); ++bx)
-                tma2_load_3d(dst + bx * GBOX * 128, m, hb, c, start + bx * GBOX, img);
-            } else {
-              const int ks = kc - kchunks;
-              if (leader) mbar_expect_tx(fb, 2 * ROWS * 128 * 128);
-              if (ks < args.kskip_a)
-                tma2_load_3d(dst, &map_sa, hb, ks * 64, q0, img);
-              else
-                tma2_load_3d(dst, &map_sb, hb, (ks - args.kskip_a) * 64, q0, img);
-            }
-          } else if (kc < kchunks) {
+            for (int bx = 0; bx < gboxes(ROWS); ++bx)
+              tma2_load_3d(dst + bx * GBOX * 128, m, hb, c, start + bx * GBOX, img);
+          } else {
             if (kc < args.kchunks_a && args.up_a) {
               if (leader) mbar_expect_tx(fb, 2 * Cfg::UP_TX);
               tma2_load_5d(dst, &map_a, hb, kc * 64, 0, x0 / 2 - 1, (y0 - 1) >> 1, img);
@@ -1424,26 +1453,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
               else
                 tma2_load_4d(dst, &map_b, hb, (kc - args.kchunks_a) * 64, x0 - 1, y0 - 1, img);
             }
-          } else {
-            const int ks = kc - kchunks;
-            if (ks < args.kskip_a && args.up_sa) {
-              // the tile's ROWS upsampled rows (y0 even when ROWS >= 2) are
-              // max(1, ROWS/2) low-res rows
-              if (leader) mbar_expect_tx(fb, 2 * (ROWS >= 2 ? ROWS / 2 : 1) * 128 * 128);
-              tma2_load_5d(dst, &map_sa, hb, ks * 64, 0, x0 / 2, y0 >> 1, img);
-            } else {
-              if (leader) mbar_expect_tx(fb, 2 * SKIP_TX);
-              if (ks < args.kskip_a)
-                tma2_load_4d(dst, &map_sa, hb, ks * 64, x0, y0, img);
-              else
-                tma2_load_4d(dst, &map_sb, hb, (ks - args.kskip_a) * 64, x0, y0, img);
-            }
           }
-          if (sring) {
-            if (++ss == SB) { ss = 0; sph ^= 1; }
-          } else if (++hs == HB) {
-            hs = 0;
-            hph ^= 1;
+          }
+          if (closing) {
+            if (sring) {
+              if (++ss == SB) { ss = 0; sph ^= 1; }
+            } else if (++hs == HB) {
+              hs = 0;
+              hph ^= 1;
+            }
           }
           if (DYN && !ha.resident) {
             for (int dx = 0; dx < (kc < kchunks ? 3 : 1); ++dx) {
@@ -1494,9 +1512,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         for (int kc = 0; kc < nchunks; ++kc) {
           const bool skipc = kc >= kchunks;
           const bool sring = SB && skipc;
-          mbar_wait(sring ? &sfull[ss] : &hfull[hs], sring ? sph : hph);
-          tc_fence_after();
-          const uint32_t hbase = smem_u32(sring ? sS + ss * SBYTES : sH + hs * HBYTES);
+          const int ksx = kc - kchunks;
+          const bool second = pair_skip && ksx >= 0 && (ksx & 1) == 1;   // 2nd of a pair
+          const bool closing = !(pair_skip && ksx >= 0) || second || kc == nchunks - 1;
+          if (!second) {
+            mbar_wait(sring ? &sfull[ss] : &hfull[hs], sring ? sph : hph);
+            tc_fence_after();
+          }
+          const uint32_t hbase = smem_u32(sring ? sS + ss * SBYTES : sH + hs * HBYTES) +
+                                 (second ? (uint32_t)SBYTES : 0u);
           const bool upc = skipc ? (kc - kchunks < args.kskip_a && args.up_sa)
                                  : (kc < args.kchunks_a && args.up_a);
           if constexpr (DYN) {
@@ -1599,13 +1623,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
               if (++bs == ha.b_stages) { bs = 0; bph ^= 1; }
             }
           }
-          if (elect_one()) tc_commit2_mc(sring ? &sempty[ss] : &hempty[hs]);
-          __syncwarp();
-          if (sring) {
-            if (++ss == SB) { ss = 0; sph ^= 1; }
-          } else if (++hs == HB) {
-            hs = 0;
-            hph ^= 1;
+          if (closing) {
+            if (elect_one()) tc_commit2_mc(sring ? &sempty[ss] : &hempty[hs]);
+            __syncwarp();
+            if (sring) {
+              if (++ss == SB) { ss = 0; sph ^= 1; }
+            } else if (++hs == HB) {
+              hs = 0;
+              hph ^= 1;
+            }
           }
         }
         if (elect_one()) tc_commit2_mc(&tfull[acc]);
@@ -3883,6 +3909,10 @@ static int g_dyn_skip = [] {
   const char* e = getenv("IG_DYN_SKIP");
   return e ? atoi(e) : 0;
 }();
+static int g_pair_skip = [] {
+  const char* e = getenv("IG_PAIR_SKIP");
+  return e ? atoi(e) : 1;
+}();
 static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
                             // 4 CTA pairs with three halo buffers, 5 no 4-row tiles,
                             // 6 separate ring for the skip chunks, 7 2-row/3-buffer out head,
@@ -3948,6 +3978,7 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   // slower with it); variant 12: off
   ha.l2pf = g_variant != 12 && N == 64 && a.kchunks_a + a.kchunks_b == 1;
   ha.l2pf_skip = g_l2pf_skip;
+  ha.pair_skip = g_pair_skip;
   if (GUT) {
     ha.tiles_x = 1;
     ha.tiles_y = (a.gP + ROWS * 128 - 1) / (ROWS * 128);
