@@ -1198,6 +1198,16 @@ __device__ __forceinline__ void tc_commit2_mc(uint64_t* bar) {
 constexpr int GBOX = 136;                    // positions per gutter TMA box (8-row aligned)
 // boxes per gutter halo: ROWS*128 + 2(w+3) positions, w <= 64
 __host__ __device__ constexpr int gboxes(int rows) { return rows == 1 ? 2 : 3; }
+template <int N, int ROWS>
+struct HaloCfg;
+// halo slot bytes of the CTA-pair kernel; a gutter slot is widened so that two
+// 1x1 skip chunks (2 x ROWS x 128 positions) can share it (pair_skip)
+template <int N, int ROWS, bool GUT>
+__host__ __device__ constexpr int gut_slot_bytes() {
+  return GUT ? (gboxes(ROWS) * GBOX * 128 > 2 * ROWS * 128 * 128 ? gboxes(ROWS) * GBOX * 128
+                                                                  : 2 * ROWS * 128 * 128)
+             : HaloCfg<N, ROWS>::HALO_BYTES;
+}
 
 // DYN (cout 64, two-row tiles, 3x3 without skip chunks): the three dy taps go
 // in N.  Halo row h feeds output rows h+1, h, h-1 through W[0], W[1], W[2]
@@ -1221,7 +1231,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                       const __grid_constant__ CUtensorMap map_sb,
                       const __grid_constant__ CUtensorMap map_ws, const HaloArgs ha) {
   using Cfg = HaloCfg<N, ROWS>;
-  constexpr int HBYTES = GUT ? gboxes(ROWS) * GBOX * 128 : Cfg::HALO_BYTES;
+  constexpr int HBYTES = gut_slot_bytes<N, ROWS, GUT>();
   constexpr int BH = N / 2;                    // weight rows staged by this CTA
   constexpr int BH_BYTES = BH * 128;
   const ConvArgs args = ha.c;
@@ -1235,8 +1245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   // two 1x1 skip chunks ride in one halo slot when both fit: a lone skip chunk
   // is only a few MMAs, consumed long before the next slot's load returns
   const bool pair_skip = ha.pair_skip && ha.sbufs == 0 && kskip >= 2 &&
-                         2 * ROWS * 128 * 128 <= (GUT ? gboxes(ROWS) * GBOX * 128
-                                                      : HaloCfg<N, ROWS>::HALO_BYTES);
+                         2 * ROWS * 128 * 128 <= HBYTES;
   constexpr uint32_t SKIP_TX = ROWS * 128 * 128;
   static_assert(!DYN || (N == 64 && ROWS == 2 && !GUT), "DYN: cout 64, two-row 2-D tiles");
   constexpr int WBLK = DYN ? DYN_BLK : BH_BYTES;   // one staged weight unit
@@ -1435,7 +1444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             if (leader) mbar_expect_tx(fb, 2 * tx);
           } else if constexpr (GUT) {
             const int q0 = r * ROWS * 128;
-            if (leader) mbar_expect_tx(fb, 2 * HBYTES);
+            if (leader) mbar_expect_tx(fb, 2 * gboxes(ROWS) * GBOX * 128);
             const CUtensorMap* m = kc < args.kchunks_a ? &map_a : &map_b;
             const int c = (kc < args.kchunks_a ? kc : kc - args.kchunks_a) * 64;
             const int start = q0 - (args.w + 3);
@@ -3933,7 +3942,7 @@ template <int N, int ROWS, bool GUT, bool DYN = false>
 static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaStream_t st) {
   using Cfg = HaloCfg<N, ROWS>;
   constexpr int BH_BYTES = N / 2 * 128;
-  constexpr int HBYTES = GUT ? gboxes(ROWS) * GBOX * 128 : Cfg::HALO_BYTES;
+  constexpr int HBYTES = gut_slot_bytes<N, ROWS, GUT>();
   CUtensorMap ma, mb, mw;
   const int hl = p->h / 2, wl = p->w / 2;
   int rc_a;
