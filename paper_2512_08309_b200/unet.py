@@ -39,6 +39,10 @@ RES_T = 1.0 / 3.0            # mp_sum blend of the residual branch (EDM2 uses 0.
 #                              1/3 makes ra/rb = 2 exactly, see UNetDevice.forward)
 RES_RA = (1 - RES_T) / math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
 RES_RB = RES_T / math.sqrt((1 - RES_T) ** 2 + RES_T ** 2)
+# identity-skip blocks: IG_IDENT_RES=1 adds the residual in the c2 epilogue instead
+# of as a K chunk of 2 * I in the same accumulator; measured slower (r02,
+# tools/ab_layers.sh: enc0.0.c2 779 -> 707 TFLOP/s), so the K chunk stays
+IDENT_RES = os.environ.get("IG_IDENT_RES", "0") == "1"
 RES_Q = 2.0                  # ra / rb
 ATTN_T = 0.3                 # EDM2 attn_balance: x = mp_sum(x, attn(x), t=0.3)
 Q_SCALE = 0.125 * math.log2(math.e)   # softmax 1/sqrt(64) in log2 units, carried by q
@@ -317,7 +321,7 @@ class UNetDevice:
 
     # -- primitive launches -------------------------------------------------
     def conv(self, name, a, b, sigma, out0=True, out1=True, skip=None, wskip=None,
-             scale=None, up2=False, up_in=0, gutter=0, pool=None):
+             scale=None, up2=False, up_in=0, gutter=0, pool=None, res=None):
         """gutter bit 0: activations in the gutter layout (n, h, w+2, c); bit 1:
         the up_in low-res sources are."""
         cs = self.prog.convs[name]
@@ -337,9 +341,11 @@ class UNetDevice:
             if out1 else None
         sa = skip[0] if skip else None
         sb = skip[1] if skip and len(skip) > 1 else None
+        # res: (tensor, ra, rb) -> the epilogue's mp_sum ra * res + rb * acc
+        rp, ra_, rb_ = (None, 0.0, 1.0) if res is None else res
         p = ConvParams(n, h, w, ca, cb, cs.cout_pad, cs.taps, a.data_ptr(), dev.ptr(b),
-                       self.w[name].data_ptr(), dev.ptr(scale), None, None, 0.0, 1.0,
-                       MP_SILU_GAIN, dev.ptr(o0), dev.ptr(o1),
+                       self.w[name].data_ptr(), dev.ptr(scale), None, dev.ptr(rp), float(ra_),
+                       float(rb_), MP_SILU_GAIN, dev.ptr(o0), dev.ptr(o1),
                        0 if sa is None else sa.shape[3], 0 if sb is None else sb.shape[3],
                        dev.ptr(sa), dev.ptr(sb), dev.ptr(wskip), int(up2), int(up_in),
                        int(gutter), dev.ptr(pool[0] if pool else None),
@@ -441,9 +447,16 @@ class UNetDevice:
                     pool = (torch.empty(shp, dtype=torch.bfloat16, device=h1.device),
                             torch.empty(shp, dtype=torch.bfloat16, device=h1.device))
                     g |= 4 * int(ng)
-                x, xa = self.conv(nm + ".c2", h1, None, sigma, skip=(x,), wskip=wsk,
-                                  scale=self._rb(c2.cout_pad), gutter=g, pool=pool,
-                                  out0=want0 or pool is not None, out1=want1)
+                if IDENT_RES and pool is None and nm + ".skip" not in self.prog.convs:
+                    # identity skip: the residual read in the epilogue, ra * x + rb * c2(h),
+                    # instead of a K chunk of 2 * I -- a lone skip chunk per tile held a
+                    # halo slot for only 16 MMAs (the next tile's box then arrived late)
+                    x, xa = self.conv(nm + ".c2", h1, None, sigma, gutter=g,
+                                      res=(x, RES_RA, RES_RB), out0=want0, out1=want1)
+                else:
+                    x, xa = self.conv(nm + ".c2", h1, None, sigma, skip=(x,), wskip=wsk,
+                                      scale=self._rb(c2.cout_pad), gutter=g, pool=pool,
+                                      out0=want0 or pool is not None, out1=want1)
                 skips.append((x, xa))
             elif op[0] == "attn":
                 x, xa = self.attention(op[1], x)
