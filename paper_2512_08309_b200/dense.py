@@ -19,8 +19,6 @@ which the package never imports).
 
 from __future__ import annotations
 
-from dataclasses import dataclass
-
 import numpy as np
 import torch
 
@@ -32,19 +30,43 @@ from .grid import (Region, WindowIndex, WindowLayout, index_box, region_union_co
 from .noise import NoiseStream, noise_region_device
 
 
-@dataclass
+class CropError(AssertionError, ValueError):
+    """A crop outside the canvas (the reference asserts, oracle.py:30)."""
+
+
 class DenseCanvas:
     """A finite multi-channel tensor with explicit lattice bounds (oracle.py:23-32).
-    ``data`` is float64 (C, H, W) on the device."""
 
-    region: Region
-    data: torch.Tensor
+    ``data`` is the float64 (C, H, W) numpy array, as in the reference; the
+    device copy the dense steps compute on is ``device()``.  Either side is
+    materialised on first use, once."""
+
+    def __init__(self, region: Region, data):
+        self.region = region
+        if isinstance(data, torch.Tensor):
+            self._dev, self._host = data, None
+        else:
+            self._dev, self._host = None, np.asarray(data, dtype=np.float64)
+
+    @property
+    def data(self) -> np.ndarray:
+        if self._host is None:
+            self._host = dev.download(self._dev)
+        return self._host
+
+    def device(self) -> torch.Tensor:
+        if self._dev is None:
+            self._dev = dev.upload(np.ascontiguousarray(self._host))
+        return self._dev
 
     def crop(self, r: Region) -> np.ndarray:
         if not self.region.contains(r):
-            raise ValueError(f"{r} outside canvas {self.region}")
-        return dev.download(self.data[:, r.y0 - self.region.y0:r.y1 - self.region.y0,
-                                      r.x0 - self.region.x0:r.x1 - self.region.x0])
+            raise CropError(f"{r} outside canvas {self.region}")
+        ys = slice(r.y0 - self.region.y0, r.y1 - self.region.y0)
+        xs = slice(r.x0 - self.region.x0, r.x1 - self.region.x0)
+        if self._host is not None:
+            return self._host[:, ys, xs].copy()
+        return dev.download(self._dev[:, ys, xs])
 
 
 def dense_fusion_step(canvas: DenseCanvas, target: Region, layout: WindowLayout,
@@ -53,12 +75,12 @@ def dense_fusion_step(canvas: DenseCanvas, target: Region, layout: WindowLayout,
     """One fusion step over ``target`` from its defining weighted sum
     (oracle.py:35-68): Phi of every window overlapping target on the canvas,
     weighted average in canonical window order, float64."""
-    c = int(canvas.data.shape[0])
+    c = int(canvas.device().shape[0])
     win = layout.window
     idxs = windows_overlapping(layout, target)
     i_lo, i_hi, j_lo, j_hi = index_box(layout, target)
     ni, nj = i_hi - i_lo + 1, j_hi - j_lo + 1
-    src = canvas.data.to(torch.float64).contiguous()
+    src = canvas.device().to(torch.float64).contiguous()
     if conditioning is None and spec.kind != "unet":
         ij = np.asarray(idxs, dtype=np.int64).reshape(-1, 2)
         wxy = dev.upload(ij * layout.stride + np.asarray(layout.offset, dtype=np.int64))

@@ -301,3 +301,56 @@ def test_pipeline_properties():
         hh = ig.build_pipeline(s, _two_stage(), seed=seed, user_map=ig.ProceduralMap(seed))
         outs.append(s.read_values(hh, Region(0, 0, 32, 32)))
     assert not np.array_equal(outs[0], outs[1])
+
+
+# ----------------------------------------------------------------- dense definition
+# (the reference's infigrid.oracle module = paper_2512_08309_b200.dense, float64 on the
+# device; reference pkg/tests/test_oracle.py)
+
+def test_dense_definition_properties():
+    from paper_2512_08309_b200 import dense
+    from paper_2512_08309_b200.grid import linear_weight_window
+    canvas = dense.DenseCanvas(Region(0, 0, 8, 8), np.random.default_rng(0).normal(size=(1, 8, 8)))
+    sp = ig.DenoiserSpec(kind="shrink_smooth", radius=1, lambdas=(0.7,))
+    out = dense.dense_fusion_step(canvas, canvas.region, WindowLayout(8, 8), np.ones((8, 8)), sp, 1)
+    np.testing.assert_allclose(out.data, denoise.apply(sp, canvas.data, None, 1))
+    big = dense.DenseCanvas(Region(-8, -8, 32, 32), np.random.default_rng(1).normal(size=(1, 32, 32)))
+    tgt = Region(0, 0, 16, 16)
+    out = dense.dense_fusion_step(big, tgt, WindowLayout(16, 8), linear_weight_window(16, 0.1),
+                                  ig.DenoiserSpec(kind="identity"), 1)
+    np.testing.assert_allclose(out.data, big.crop(tgt))
+    # f32 store within 1e-5 of the definition at every step
+    lay = WindowLayout(16, 8)
+    sp2 = ig.DenoiserSpec(kind="shrink_smooth", radius=1, lambdas=(0.6, 0.4))
+    cfg = ig.SamplerConfig(steps=2, layout=lay, denoiser=sp2, seed=31)
+    st = ig.SamplerState(cfg, ig.TileStore())
+    target = Region(0, 0, 64, 64)
+    ref = dense.dense_trajectory(31, 2, lay, cfg.weight_for(0).astype(np.float64), sp2, target)
+    for t in range(3):
+        want = ref[t].crop(target)
+        dev_ = float(np.abs(st.query(t, target).astype(np.float64) - want).max())
+        assert dev_ / max(float(np.abs(want).max()), 1e-12) <= 1e-5
+    rng = np.random.default_rng(2)
+    for _ in range(100):
+        w = int(rng.integers(1, 12))
+        layout = WindowLayout(w, int(rng.integers(1, w + 1)))
+        r = Region(int(rng.integers(-15, 15)), int(rng.integers(-15, 15)),
+                   int(rng.integers(1, 10)), int(rng.integers(1, 10)))
+        assert dense.brute_force_windows(layout, r, 40) == set(ig.windows_overlapping(layout, r))
+    assert dense.brute_force_windows(WindowLayout(4, 4), Region(5, 5, 1, 1), 10) == {(1, 1)}
+    win = Region(0, 0, 16, 16)
+    assert dense.count_denoiser_calls_naive(1, lay, win) == 9
+    assert dense.count_denoiser_calls_naive(2, lay, win) == 90
+    assert dense.count_denoiser_calls_naive(3, lay, win) > 90
+    cached = ig.SamplerState(ig.SamplerConfig(steps=2, layout=lay, seed=0,
+                                              denoiser=ig.DenoiserSpec(lambdas=(0.5,))),
+                             ig.TileStore())
+    cached.query(0, win)
+    assert cached.total_denoiser_calls() < 90
+    out = dense.dense_trajectory(5, 1, WindowLayout(8, 4), np.ones((8, 8)),
+                                 ig.DenoiserSpec(kind="identity"), Region(0, 0, 8, 8))
+    np.testing.assert_array_equal(
+        out[1].data, ig.noise_region(ig.NoiseStream(5), out[1].region).astype(np.float64))
+    np.testing.assert_allclose(out[0].data, out[1].crop(Region(0, 0, 8, 8)))
+    with pytest.raises(AssertionError):
+        dense.DenseCanvas(Region(0, 0, 4, 4), np.zeros((1, 4, 4))).crop(Region(2, 2, 4, 4))
