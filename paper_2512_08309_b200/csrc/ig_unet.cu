@@ -842,6 +842,7 @@ struct HaloArgs {
   int l2pf;          // CTA-pair kernel: L2-prefetch the next tile's halo boxes
   int l2pf_skip;     // CTA-pair kernel: L2-prefetch the next tile's 1x1 skip-GEMM boxes
   int pair_skip;     // CTA-pair kernel: two 1x1 skip chunks per halo slot
+  int skip_first;    // CTA-pair kernel: a tile's skip chunks before its halo chunks
 };
 
 template <int N, int ROWS>
@@ -1246,6 +1247,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   // is only a few MMAs, consumed long before the next slot's load returns
   const bool pair_skip = ha.pair_skip && ha.sbufs == 0 && kskip >= 2 &&
                          2 * ROWS * 128 * 128 <= HBYTES;
+  const bool skip_first = ha.skip_first && kskip > 0;
   constexpr uint32_t SKIP_TX = ROWS * 128 * 128;
   static_assert(!DYN || (N == 64 && ROWS == 2 && !GUT), "DYN: cout 64, two-row 2-D tiles");
   constexpr int WBLK = DYN ? DYN_BLK : BH_BYTES;   // one staged weight unit
@@ -1426,12 +1428,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             return SKIP_TX;
           }
         };
-        for (int kc = 0; kc < nchunks; ++kc) {
+        for (int pos = 0; pos < nchunks; ++pos) {
+          // skip_first: the 1x1 skip chunks of a tile go before its halo chunks
+          const int kc = skip_first ? (pos < kskip ? kchunks + pos : pos - kskip) : pos;
           const bool sring = SB && kc >= kchunks;    // skip chunk in its own ring
           const int ks = kc - kchunks;
           // paired skip chunks share one halo slot: the even one loads both
           const bool opening = !(pair_skip && ks >= 0) || (ks & 1) == 0;
-          const bool closing = !(pair_skip && ks >= 0) || (ks & 1) == 1 || kc == nchunks - 1;
+          const bool closing = !(pair_skip && ks >= 0) || (ks & 1) == 1 || ks == kskip - 1;
           if (opening) {
           uint64_t* fb = sring ? &sfull[ss] : &hfull[hs];
           mbar_wait(sring ? &sempty[ss] : &hempty[hs], (sring ? sph : hph) ^ 1);
@@ -1518,12 +1522,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         const int tile = 2 * pr;               // both tiles of the pair share y0 parity
         const int y0 = ((tile % tiles_per_img) / ha.tiles_x) * ROWS;
         const int ylo0 = (y0 - 1) >> 1;
-        for (int kc = 0; kc < nchunks; ++kc) {
+        for (int pos = 0; pos < nchunks; ++pos) {
+          // skip_first: the 1x1 skip chunks of a tile go before its halo chunks
+          const int kc = skip_first ? (pos < kskip ? kchunks + pos : pos - kskip) : pos;
           const bool skipc = kc >= kchunks;
           const bool sring = SB && skipc;
           const int ksx = kc - kchunks;
           const bool second = pair_skip && ksx >= 0 && (ksx & 1) == 1;   // 2nd of a pair
-          const bool closing = !(pair_skip && ksx >= 0) || second || kc == nchunks - 1;
+          const bool closing = !(pair_skip && ksx >= 0) || second || ksx == kskip - 1;
           if (!second) {
             mbar_wait(sring ? &sfull[ss] : &hfull[hs], sring ? sph : hph);
             tc_fence_after();
@@ -1553,7 +1559,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                   const uint64_t adesc = smem_desc_sw128(hbase + prow * 128);
 #pragma unroll
                   for (int kq = 0; kq < 4; ++kq)
-                    tc_mma2(d0 + (ROWS - 1 - rr) * N, adesc + 2 * kq, bdesc + 2 * kq, id64, 1u);
+                    tc_mma2(d0 + (ROWS - 1 - rr) * N, adesc + 2 * kq, bdesc + 2 * kq, id64,
+                            (pos | kq) ? 1u : 0u);
                 }
                 if (!ha.resident) tc_commit2_mc(&bempty[bs]);
               }
@@ -1588,7 +1595,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
 #pragma unroll
                   for (int kq = 0; kq < 4; ++kq)
                     tc_mma2(d0 + dcol, adesc + 2 * kq, bdesc + 2 * kq, id,
-                            (kc | dx | o | kq) ? 1u : 0u);
+                            (pos | dx | o | kq) ? 1u : 0u);
                 }
                 if (!ha.resident) tc_commit2_mc(&bempty[bs]);
               }
@@ -1623,7 +1630,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                   tc_mma2(d0 + rr * N, adesc + 2 * k, bdesc + 2 * k, idesc,
-                          (kc | tap | k) ? 1u : 0u);
+                          (pos | tap | k) ? 1u : 0u);
               }
               if (!ha.resident) tc_commit2_mc(&bempty[bs]);
             }
@@ -3922,6 +3929,13 @@ static int g_pair_skip = [] {
   const char* e = getenv("IG_PAIR_SKIP");
   return e ? atoi(e) : 1;
 }();
+// a tile's skip chunks before its halo chunks: measured slower on every c2
+// layer (r02, tools/ab_layers.sh: enc0.0.c2 796 -> 668, dec1.1.c2 1078 -> 1021
+// TFLOP/s), off unless IG_SKIP_FIRST=1
+static int g_skip_first = [] {
+  const char* e = getenv("IG_SKIP_FIRST");
+  return e ? atoi(e) : 0;
+}();
 static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
                             // 4 CTA pairs with three halo buffers, 5 no 4-row tiles,
                             // 6 separate ring for the skip chunks, 7 2-row/3-buffer out head,
@@ -3988,6 +4002,7 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   ha.l2pf = g_variant != 12 && N == 64 && a.kchunks_a + a.kchunks_b == 1;
   ha.l2pf_skip = g_l2pf_skip;
   ha.pair_skip = g_pair_skip;
+  ha.skip_first = g_skip_first && g_variant == 0;   // A/B variants keep the r01 order
   if (GUT) {
     ha.tiles_x = 1;
     ha.tiles_y = (a.gP + ROWS * 128 - 1) / (ROWS * 128);
