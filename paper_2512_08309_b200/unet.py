@@ -56,7 +56,9 @@ FUSED_GUTTER = True          # narrow levels (w <= 64) in the gutter layout (1-D
 # Off: measured slower (r01: enc0.0.c2 479 -> 847 us) -- the c2 epilogue, not
 # the MMAs, is then the per-tile critical path (a second round of tanh /
 # shuffles / stores per column pair), which costs more than the pool kernel.
-FUSED_POOL = False
+# Re-measured r02 with the DYN / paired-skip kernels (IG_FUSED_POOL=1): 7.25 ->
+# 7.85 ms per 64-window forward, still off.
+FUSED_POOL = os.environ.get("IG_FUSED_POOL", "0") == "1"
 FUSED_QKV = True             # attention q / k / v projections as one ig_conv_qkv launch
 
 
