@@ -255,6 +255,7 @@ struct ConvArgs {
   __nv_bfloat16* out0;
   __nv_bfloat16* out1;
   int res_v8;             // residual read as 32-byte (full-sector) loads
+  int dbg;                // IG_DBG (timing experiments only): 1 no epilogue math, 2 no MMAs
 };
 
 template <int N>
@@ -395,13 +396,18 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
         tmem_ld32_nw(taddr + c0 + hb, r);
         tmem_ld32_nw(taddr + c0 + hb + 32, r + 32);
         tmem_wait_ld();
-        float ss = 0.f;
+        // eight interleaved partial sums: one 64-deep FFMA chain per head was
+        // the epilogue's critical path (ncu r02: long/short scoreboard on it)
+        float ps[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ps[j] = 0.f;
 #pragma unroll
         for (int i = 0; i < 64; ++i) {
           const float v = __uint_as_float(r[i]) * (s_scale ? s_scale[c0 + hb + i] : 1.f);
           r[i] = __float_as_uint(v);
-          ss = fmaf(v, v, ss);
+          ps[i & 7] = fmaf(v, v, ps[i & 7]);
         }
+        const float ss = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
         const float inv = hsc / (1e-4f + sqrtf(ss) * 0.125f);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -514,7 +520,23 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
   }
 }
 
-template <int N>
+// WRES (1x1 convs whose whole weight matrix fits in 128 KB, i.e. the attention
+// block's q / k / v and output projections): the CTA's weights -- one group's
+// with groups > 1, the grid then a multiple of the group count so a CTA's work
+// items all belong to one group -- are loaded ONCE and stay resident; only the
+// 16 KB activation boxes stream through a WRES_STAGES ring.  Per 128-pixel tile
+// the SMEM fill drops from 192 KB (K = 256: 64 KB of A + 128 KB of weights) to
+// 64 KB; with the weights streamed the fill, not the tensor core, set the pace
+// (ncu r02, qkv: tensor pipe 31%, 45.5 us for 25.8 GFLOP).
+constexpr int WRES_STAGES = 5;
+constexpr int WRES_BYTES = 128 * 1024;
+template <int N, bool WRES>
+__host__ __device__ constexpr int conv_tc_smem() {
+  return WRES ? 1024 + WRES_STAGES * ConvCfg<N>::A_BYTES + WRES_BYTES + 256 + 1024
+              : ConvCfg<N>::SMEM;
+}
+
+template <int N, bool WRES = false>
 __global__ void __launch_bounds__(320, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
@@ -523,15 +545,18 @@ __global__ void __launch_bounds__(320, 1)
                    const __grid_constant__ CUtensorMap map_sb,
                    const __grid_constant__ CUtensorMap map_ws, const ConvArgs args) {
   using Cfg = ConvCfg<N>;
+  constexpr int STAGES = WRES ? WRES_STAGES : Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + Cfg::STAGES * Cfg::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE);
-  uint64_t* empty = full + Cfg::STAGES;
-  uint64_t* tfull = empty + Cfg::STAGES;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(
+      smem + (WRES ? STAGES * Cfg::A_BYTES + WRES_BYTES : STAGES * Cfg::STAGE));
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* wfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
   float* s_scale = reinterpret_cast<float*>(tmem_slot + 4);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -545,7 +570,7 @@ __global__ void __launch_bounds__(320, 1)
     prefetch_map(&map_a);
     if (args.kchunks_b) prefetch_map(&map_b);
     prefetch_map(&map_w);
-    for (int s = 0; s < Cfg::STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -553,6 +578,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 256);
     }
+    mbar_init(wfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -573,6 +599,17 @@ __global__ void __launch_bounds__(320, 1)
       int stage = 0;
       uint32_t phase = 0;
       const int total = args.num_tiles * args.groups;
+      if constexpr (WRES) {
+        // this CTA's group (gridDim.x is a multiple of args.groups), all K blocks
+        const int wrow = (int)(blockIdx.x % args.groups) * N;
+        mbar_expect_tx(wfull, (uint32_t)(kblocks * Cfg::B_BYTES));
+        for (int kb = 0; kb < kblocks; ++kb) {
+          if (kb < kmain)
+            tma_load_2d(sB + kb * Cfg::B_BYTES, &map_w, wfull, kb * 64, wrow);
+          else
+            tma_load_2d(sB + kb * Cfg::B_BYTES, &map_ws, wfull, (kb - kmain) * 64, 0);
+        }
+      }
       for (int gt = blockIdx.x; gt < total; gt += gridDim.x) {
         // groups > 1: the groups of one pixel tile are consecutive work items,
         // so concurrently running CTAs read its A boxes from L2
@@ -591,8 +628,26 @@ __global__ void __launch_bounds__(320, 1)
         }
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], Cfg::STAGE);
           uint8_t* a_dst = sA + stage * Cfg::A_BYTES;
+          if constexpr (WRES) {
+            // 1x1: the centre tap of a main or skip source, weights resident
+            mbar_expect_tx(&full[stage], Cfg::A_BYTES);
+            if (kb < args.kchunks_a)
+              tma_load_4d(a_dst, &map_a, &full[stage], kb * 64, x0, y0, img);
+            else if (kb < kmain)
+              tma_load_4d(a_dst, &map_b, &full[stage], (kb - args.kchunks_a) * 64, x0, y0, img);
+            else if (kb - kmain < args.kskip_a)
+              tma_load_4d(a_dst, &map_sa, &full[stage], (kb - kmain) * 64, x0, y0, img);
+            else
+              tma_load_4d(a_dst, &map_sb, &full[stage], (kb - kmain - args.kskip_a) * 64, x0, y0,
+                          img);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+          mbar_expect_tx(&full[stage], Cfg::STAGE);
           if (kb < kmain) {
             const int tap = kb / kchunks;
             const int kc = kb - tap * kchunks;
@@ -613,7 +668,7 @@ __global__ void __launch_bounds__(320, 1)
               tma_load_4d(a_dst, &map_sb, &full[stage], (ks - args.kskip_a) * 64, x0, y0, img);
             tma_load_2d(sB + stage * Cfg::B_BYTES, &map_ws, &full[stage], ks * 64, 0);
           }
-          if (++stage == Cfg::STAGES) {
+          if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -627,6 +682,7 @@ __global__ void __launch_bounds__(320, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      if constexpr (WRES) mbar_wait(wfull, 0);
       const int total = args.num_tiles * args.groups;
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
         const int acc = it & 1;
@@ -638,15 +694,18 @@ __global__ void __launch_bounds__(320, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t adesc = smem_desc_sw128(smem_u32(sA + stage * Cfg::A_BYTES));
-          const uint64_t bdesc = smem_desc_sw128(smem_u32(sB + stage * Cfg::B_BYTES));
+          const uint64_t bdesc =
+              smem_desc_sw128(smem_u32(sB + (WRES ? kb : stage) * Cfg::B_BYTES));
           if (elect_one()) {
+            if (!(args.dbg & 2)) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)  // K = 16 per MMA: +32 B in the 128 B swizzled row
-              tc_mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) ? 1u : 0u);
+              for (int k = 0; k < 4; ++k)  // K = 16 per MMA: +32 B in the 128 B swizzled row
+                tc_mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) ? 1u : 0u);
+            }
             tc_commit(&empty[stage]);
           }
           __syncwarp();
-          if (++stage == Cfg::STAGES) {
+          if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -666,12 +725,23 @@ __global__ void __launch_bounds__(320, 1)
     const int total = args.num_tiles * args.groups;
     for (int gt = blockIdx.x; gt < total; gt += gridDim.x, ++it) {
       const int acc = it & 1;
+      if (args.res && gt + (int)gridDim.x < total) {
+        // warm L2 with the next tile's residual span (2 x 128 B lines per
+        // thread): read after the accumulator is ready, an HBM round trip per
+        // tile was exposed (attention projection)
+        const int64_t pn = (int64_t)((gt + gridDim.x) / args.groups) * 128 + m;
+        const __nv_bfloat16* rn = args.res + pn * args.cout + half * NC;
+#pragma unroll
+        for (int q = 0; q < NC * 2; q += 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(rn) + q));
+      }
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const int tile = gt / args.groups;
       const int64_t p = (int64_t)tile * 128 + m;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * N;
-      if (args.groups > 1) {
+      if (args.dbg & 1) {
+      } else if (args.groups > 1) {
         const int g = gt - tile * args.groups;
         ConvArgs ga = args;
         ga.out0 = args.outg[g];
@@ -3758,6 +3828,11 @@ static int make_w_map(CUtensorMap* m, const void* base, int ktot, int cout, int 
   return r == CUDA_SUCCESS ? IG_OK : IG_ERR_CUDA;
 }
 
+static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
+                            // 4 CTA pairs with three halo buffers, 5 no 4-row tiles,
+                            // 6 separate ring for the skip chunks, 7 2-row/3-buffer out head,
+                            // 8 per-tap out head for C = 1, 20 streamed 1x1 weights
+
 template <int N>
 static int launch_conv_tc(const ig_conv_params_t* p, const ConvArgs& a, cudaStream_t st) {
   using Cfg = ConvCfg<N>;
@@ -3790,9 +3865,20 @@ static int launch_conv_tc(const ig_conv_params_t* p, const ConvArgs& a, cudaStre
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(conv_tc_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    cudaFuncSetAttribute(conv_tc_kernel<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         conv_tc_smem<N, true>());
     attr_set = true;
   }
   const int work = a.num_tiles * a.groups;
+  const int kblocks = p->taps * (a.kchunks_a + a.kchunks_b) + a.kskip_a + a.kskip_b;
+  // resident weights for the fused q / k / v 1x1 conv (variant 20: streamed, A/B;
+  // r02: qkv 49.7 -> 47.0 us per 64 windows; the projection measured 42.1 -> 43.1,
+  // so the groups == 1 convs keep streaming)
+  if (p->taps == 1 && a.groups > 1 && kblocks * Cfg::B_BYTES <= WRES_BYTES && g_variant != 20) {
+    const int grid = ((work < kNumSMs ? work : kNumSMs) / a.groups) * a.groups;
+    { conv_tc_kernel<N, true><<<grid, 320, conv_tc_smem<N, true>(), st>>>(ma, mb, mw, msa, msb, mws, a); note_launch(); }
+    return cuda_check("ig_conv_tc(wres)");
+  }
   const int grid = work < kNumSMs ? work : kNumSMs;
   { conv_tc_kernel<N><<<grid, 320, Cfg::SMEM, st>>>(ma, mb, mw, msa, msb, mws, a); note_launch(); }
   return cuda_check("ig_conv_tc");
@@ -3902,6 +3988,10 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
   return cuda_check("ig_conv_tc(halo)");
 }
 
+static int g_dbg = [] {
+  const char* e = getenv("IG_DBG");
+  return e ? atoi(e) : 0;
+}();
 static int g_res_v8 = [] {
   const char* e = getenv("IG_RES_V8");
   return e ? atoi(e) : 1;
@@ -3936,10 +4026,6 @@ static int g_skip_first = [] {
   const char* e = getenv("IG_SKIP_FIRST");
   return e ? atoi(e) : 0;
 }();
-static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
-                            // 4 CTA pairs with three halo buffers, 5 no 4-row tiles,
-                            // 6 separate ring for the skip chunks, 7 2-row/3-buffer out head,
-                            // 8 per-tap out head for C = 1
 static int make_w_map_rows(CUtensorMap* m, const void* base, int ktot, int cout, int brows) {
   cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)cout};
   cuuint64_t strides[1] = {(cuuint64_t)ktot * 2};
@@ -4096,6 +4182,7 @@ static int conv_args(const ig_conv_params_t* p, ConvArgs* a, bool tc) {
   a->out0 = reinterpret_cast<__nv_bfloat16*>(p->out0);
   a->out1 = reinterpret_cast<__nv_bfloat16*>(p->out1);
   a->res_v8 = g_res_v8;
+  a->dbg = g_dbg;
   IG_REQUIRE(p->csa % 64 == 0 && p->csb % 64 == 0 && p->csa >= 0 && p->csb >= 0,
              "conv: skip channels must be multiples of 64");
   IG_REQUIRE(p->csa > 0 || p->csb == 0, "conv: skip_b without skip_a");

@@ -735,6 +735,46 @@ def test_conv_qkv_fused_equals_three_launches(n, h, w):
     assert lib().ig_conv_qkv(p, fused[1].data_ptr(), fused[2].data_ptr(), st) != 0
 
 
+@pytest.mark.parametrize("n,h,w,groups", [(64, 32, 32, 3), (64, 32, 32, 1), (2, 16, 16, 3),
+                                          (1, 8, 16, 1)])
+def test_conv_1x1_resident_weights_match_streamed(n, h, w, groups):
+    """The fused q / k / v conv with resident weights (WRES) is bit-identical
+    to the streamed-weight kernel (variant 20), grids above and below one wave;
+    the projection case (streamed either way) checks the residual mp_sum."""
+    c = 256
+    g = torch.Generator(device=DEV).manual_seed(n * 7 + h + groups)
+    x = torch.randn(n, h, w, c, device=DEV, generator=g).bfloat16()
+    r = torch.randn(n, h, w, c, device=DEV, generator=g).bfloat16()
+    wt = (torch.randn(groups * c, c, device=DEV, generator=g) / 16).bfloat16()
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for variant in (0, 20):
+        check(lib().ig_conv_set_variant(variant))
+        try:
+            o = [torch.full_like(x, 7.0) for _ in range(3)]
+            if groups == 3:
+                p = ConvParams(n, h, w, c, 0, c, 1, x.data_ptr(), None, wt.data_ptr(), None,
+                               None, None, 0.0, 1.0, 1.0, o[0].data_ptr(), None)
+                p.head_norm, p.head_scale = 1, unet.Q_SCALE
+                check(lib().ig_conv_qkv(p, o[1].data_ptr(), o[2].data_ptr(), st), "ig_conv_qkv")
+            else:
+                p = ConvParams(n, h, w, c, 0, c, 1, x.data_ptr(), None, wt.data_ptr(), None,
+                               None, r.data_ptr(), float(unet.ATTN_RA), float(unet.ATTN_RB),
+                               unet.MP_SILU_GAIN, o[0].data_ptr(), o[1].data_ptr())
+                check(lib().ig_conv_tc(p, None, st), "ig_conv_tc")
+            torch.cuda.synchronize()
+            outs.append(o)
+        finally:
+            check(lib().ig_conv_set_variant(0))
+    for a, b in zip(*outs):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    if groups == 1:
+        y = x.float().reshape(-1, c) @ wt.float().t()
+        ref = unet.ATTN_RA * r.float().reshape(-1, c) + unet.ATTN_RB * y
+        err = (outs[0][0].float().reshape(-1, c) - ref).abs().max().item()
+        assert err < 2e-2 * ref.abs().max().item(), err
+
+
 @pytest.mark.parametrize("n,hw,c", [(2, 1024, 256), (1, 200, 128)])
 def test_attention_p_in_tmem_matches_smem_path(n, hw, c):
     """The default attention kernel (attention2_kernel) keeps P in its own TMEM
