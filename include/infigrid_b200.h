@@ -19,6 +19,7 @@
  *   ig_block_mean          transforms.py:61-67 block_mean (float32 / float64 accumulation)
  *   ig_upsample_nn         transforms.py:70-72 upsample_nn
  *   ig_normalize_u8        transforms.py:117-135 normalize_heightmap_u8 (render path)
+ *   ig_hillshade_u8        cli.py:230-249 hillshade (render --hillshade)
  *   ig_convert             numpy astype at transforms.py:93,101 (dtype-preserving decode)
  *   ig_laplacian_residual  transforms.py:89-95 (high = x - up(low))
  *   ig_laplacian_merge     transforms.py:98-101 / :104-114 (up(low)+high [, signed_square])
@@ -188,6 +189,11 @@ int ig_convert(const void* in, int32_t in_dtype, int64_t n, void* out, int32_t o
  * float64, out (images, 3, hw) uint8; minmax: device scratch of 2*images u64 */
 int ig_normalize_u8(const void* in, int32_t dtype, int32_t images, int64_t hw, void* minmax,
                     uint8_t* out, void* cuda_stream);
+/* hillshade (cli.py:230-249): Horn 3x3 slope shading of one (h, w) float32 /
+ * float64 raster to uint8, float64 arithmetic; cos_zenith / sin_zenith /
+ * azimuth as the reference computes them on the host */
+int ig_hillshade_u8(const void* elev, int32_t dtype, int32_t h, int32_t w, double cos_zenith,
+                    double sin_zenith, double azimuth, uint8_t* out, void* cuda_stream);
 /* upsample_nn (transforms.py:70-72): out[p][Y][X] = in[p][Y/f][X/f], any
  * element size (1/2/4/8 bytes) */
 int ig_upsample_nn(const void* in, int32_t elem_bytes, int64_t planes, int32_t h, int32_t w,

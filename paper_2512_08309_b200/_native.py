@@ -66,6 +66,7 @@ SIGNATURES = {
     "ig_convert": [V, I32, I64, V, I32, V],
     "ig_upsample_nn": [V, I32, I64, I32, I32, I32, V, V],
     "ig_normalize_u8": [V, I32, I32, I64, V, V, V],
+    "ig_hillshade_u8": [V, I32, I32, I32, F64, F64, F64, V, V],
     "ig_tiles_resolve": [V, I64, I64, I32, I32, I32, I32, I32, I64, I64, I32, I32, V, V],
     "ig_patch_features": [V, I64, I32, I32, I32, I32, I32, I32, V, V],
     "ig_condition_window": [V, I64, I64, I32, I32, I32, I32, I32, U64, V, I32, I32, I32, V, V, V],

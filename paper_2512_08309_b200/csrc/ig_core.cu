@@ -1015,6 +1015,38 @@ __global__ void __launch_bounds__(256) normalize_u8_kernel(const T* __restrict__
     o[2 * hw + i] = u;
   }
 }
+// Horn 3x3 hillshade to uint8 (reference cli.py:230-249): edge-clamped
+// neighbours, the gradient sums in the reference's association order, every
+// arithmetic step an explicit round-to-nearest float64 op (no FMA contraction
+// -- numpy evaluates each product and sum separately), CUDA's float64
+// atan / hypot / atan2 / sin / cos for numpy's, round half to even, clamp.
+// cz / sz: numpy's cos / sin of the zenith, azi the light's azimuth (radians),
+// computed on the host exactly as the reference does.
+template <typename T>
+__global__ void __launch_bounds__(256) hillshade_u8_kernel(const T* __restrict__ z, int h, int w,
+                                                           double cz, double sz, double azi,
+                                                           uint8_t* __restrict__ out) {
+  const int64_t total = (int64_t)h * w;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / w), x = (int)(i - (int64_t)(i / w) * w);
+    const int ym = y > 0 ? y - 1 : 0, yp = y < h - 1 ? y + 1 : h - 1;
+    const int xm = x > 0 ? x - 1 : 0, xp = x < w - 1 ? x + 1 : w - 1;
+    auto at = [&](int yy, int xx) { return (double)z[(int64_t)yy * w + xx]; };
+    const double a = at(ym, xm), b = at(ym, x), c = at(ym, xp);
+    const double d = at(y, xm), f = at(y, xp);
+    const double g = at(yp, xm), hh = at(yp, x), k = at(yp, xp);
+    const double right = radd(radd(c, rmul(2.0, f)), k), left = radd(radd(a, rmul(2.0, d)), g);
+    const double below = radd(radd(g, rmul(2.0, hh)), k), above = radd(radd(a, rmul(2.0, b)), c);
+    const double gx = rdiv(rsub(right, left), 8.0), gy = rdiv(rsub(below, above), 8.0);
+    const double slope = atan(hypot(gx, gy));
+    const double aspect = atan2(gy, -gx);
+    const double lum =
+        rmul(255.0, radd(rmul(cz, cos(slope)), rmul(rmul(sz, sin(slope)), cos(rsub(azi, aspect)))));
+    const double r = fmin(fmax(rint(lum), 0.0), 255.0);
+    out[i] = (uint8_t)r;
+  }
+}
 }  // namespace ig
 
 // =====================================================================
@@ -1331,6 +1363,21 @@ int ig_normalize_u8(const void* in, int32_t dtype, int32_t images, int64_t hw, v
     normalize_u8_kernel<double><<<grid, 256, 0, st>>>((const double*)in, hw, mm, out); note_launch();
   }
   return cuda_check("ig_normalize_u8");
+}
+
+int ig_hillshade_u8(const void* elev, int32_t dtype, int32_t h, int32_t w, double cos_zenith,
+                    double sin_zenith, double azimuth, uint8_t* out, void* cuda_stream) {
+  IG_REQUIRE(dtype == IG_DTYPE_F32 || dtype == IG_DTYPE_F64, "hillshade_u8: float input");
+  IG_REQUIRE(h >= 0 && w >= 0, "hillshade_u8: negative shape %dx%d", h, w);
+  if (h == 0 || w == 0) return IG_OK;
+  const int grid = grid_for((int64_t)h * w, 256);
+  if (dtype == IG_DTYPE_F32)
+    { hillshade_u8_kernel<float><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const float*)elev, h, w, cos_zenith, sin_zenith, azimuth, out); note_launch(); }
+  else
+    { hillshade_u8_kernel<double><<<grid, 256, 0, as_stream(cuda_stream)>>>(
+        (const double*)elev, h, w, cos_zenith, sin_zenith, azimuth, out); note_launch(); }
+  return cuda_check("ig_hillshade_u8");
 }
 
 int ig_upsample_nn(const void* in, int32_t elem_bytes, int64_t planes, int32_t h, int32_t w,

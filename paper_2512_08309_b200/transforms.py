@@ -10,6 +10,7 @@ float64 for decode(encode(x)) == x to hold bit-exactly.
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -258,6 +259,32 @@ def laplacian_stabilize(pair: LaplacianPair, blur_radius: int = 1) -> LaplacianP
     if not d:
         return LaplacianPair(dev.download(low_hat), pair.high, pair.factor, pair.dtype)
     return LaplacianPair(low_hat, pair.high, pair.factor, pair.dtype)
+
+
+def hillshade_u8(elev, azimuth_deg: float = 315.0, altitude_deg: float = 45.0):
+    """Horn 3x3 slope shading to uint8 on the device (reference cli.py:230-249):
+    float64 arithmetic in the reference's operation order; the light's
+    cos / sin are evaluated on the host with numpy, as the reference does.
+    numpy in -> numpy out; a CUDA tensor stays on the device."""
+    was_dev = isinstance(elev, torch.Tensor)
+    if was_dev:
+        t = elev.contiguous()
+        if t.dtype not in (torch.float32, torch.float64):
+            t = _convert(t, torch.float64)
+    else:
+        arr = np.asarray(elev)
+        if arr.dtype not in (np.float32, np.float64):
+            arr = arr.astype(np.float64)
+        t = dev.upload(np.ascontiguousarray(arr))
+    if t.dim() != 2:
+        raise ShapeError(f"hillshade expects a 2-D raster, got {tuple(t.shape)}")
+    zen = math.radians(90.0 - altitude_deg)
+    azi = math.radians(360.0 - azimuth_deg + 90.0)
+    h, w = t.shape
+    out = torch.empty((h, w), dtype=torch.uint8, device=t.device)
+    call("ig_hillshade_u8", t.data_ptr(), _dt(t), h, w, float(np.cos(zen)), float(np.sin(zen)),
+         azi, out.data_ptr(), dev.stream_ptr())
+    return out if was_dev else dev.download(out)
 
 
 def normalize_heightmap_u8(batch):

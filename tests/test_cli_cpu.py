@@ -1,17 +1,15 @@
-"""CLI host logic (mirrors the reference's tests/test_cli.py parsing and
-render cases): config / region validation, the translation period, and the
-hillshade render (host float64, byte-identical to the reference's PGM in
-tests/golden/cli.npz)."""
+"""CLI host logic (mirrors the reference's tests/test_cli.py parsing cases):
+config / region validation, the translation period and the exit codes of
+failures caught before any device work.  Rendering runs on the device:
+tests/test_gpu_cli.py."""
 
 import json
 
-import numpy as np
 import pytest
 
 from paper_2512_08309_b200 import cli
 from paper_2512_08309_b200.errors import ConfigError
 from paper_2512_08309_b200.grid import Region
-from paper_2512_08309_b200.pipeline import save_raster
 
 BASE = {"seed": 7, "stages": [{"steps": 2, "window": 16, "stride": 8,
                                "denoiser": {"kind": "shrink_smooth", "radius": 1,
@@ -64,30 +62,6 @@ def test_translation_period(golden):
     # the stage-0 feature lattice (16 * patch 4 = 64 stage-0 px) in finest
     # (stage-1) pixels, times scale 4; the reference's own value is 256 too
     assert cli.translation_period(two) == 256
-
-
-def _pgm_body(data: bytes) -> bytes:
-    return data.split(b"\n", 3)[3]
-
-
-def test_render_golden(tmp_path, golden):
-    """Hillshade render byte-identical to the reference CLI's (host float64; the
-    plain render normalises on the device: tests/test_gpu_cli.py)."""
-    _, g = golden("cli")
-    raster = str(tmp_path / "r.bin")
-    save_raster(raster, g["render_in"])
-    for tag, extra in (("hill", ["--hillshade"]),):
-        out = str(tmp_path / f"{tag}.pgm")
-        assert cli.main(["render", raster, out] + extra) == 0
-        assert open(out, "rb").read() == g["pgm_" + tag].tobytes(), tag
-
-
-def test_render_flat_hillshade(tmp_path):
-    raster = str(tmp_path / "r.bin")
-    out = str(tmp_path / "r.pgm")
-    save_raster(raster, np.full((1, 8, 8), 5.0, dtype=np.float32))
-    assert cli.main(["render", raster, out, "--hillshade"]) == 0
-    assert set(_pgm_body(open(out, "rb").read())) == {180}     # 255 * cos(45 deg)
 
 
 def test_exit_codes_host(tmp_path, capsys):

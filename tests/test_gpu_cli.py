@@ -116,6 +116,64 @@ def test_dense_helpers():
     assert dense.count_denoiser_calls_naive(2, lay, Region(0, 0, 16, 16)) == 9 + 9 * 9
 
 
+def _pgm_body(data: bytes) -> bytes:
+    return data.split(b"\n", 3)[3]
+
+
+def test_render_hillshade_golden(tmp_path, golden):
+    """Device hillshade render byte-identical to the reference CLI's PGM."""
+    _, g = golden("cli")
+    raster = str(tmp_path / "r.bin")
+    save_raster(raster, g["render_in"])
+    out = str(tmp_path / "hill.pgm")
+    assert cli.main(["render", raster, out, "--hillshade"]) == 0
+    assert open(out, "rb").read() == g["pgm_hill"].tobytes()
+
+
+def test_render_flat_hillshade(tmp_path):
+    raster = str(tmp_path / "r.bin")
+    out = str(tmp_path / "r.pgm")
+    save_raster(raster, np.full((1, 8, 8), 5.0, dtype=np.float32))
+    assert cli.main(["render", raster, out, "--hillshade"]) == 0
+    assert set(_pgm_body(open(out, "rb").read())) == {180}     # 255 * cos(45 deg)
+
+
+def _hillshade_numpy(elev):
+    """The reference's expression (cli.py:230-249), numpy float64 -- the checker."""
+    import math
+    z = np.pad(elev.astype(np.float64), 1, mode="edge")
+    a, b, c = z[:-2, :-2], z[:-2, 1:-1], z[:-2, 2:]
+    d, f = z[1:-1, :-2], z[1:-1, 2:]
+    g, h, i = z[2:, :-2], z[2:, 1:-1], z[2:, 2:]
+    dzdx = ((c + 2 * f + i) - (a + 2 * d + g)) / 8.0
+    dzdy = ((g + 2 * h + i) - (a + 2 * b + c)) / 8.0
+    zen, az = math.radians(45.0), math.radians(135.0)
+    slope = np.arctan(np.hypot(dzdx, dzdy))
+    aspect = np.arctan2(dzdy, -dzdx)
+    shade = 255.0 * (np.cos(zen) * np.cos(slope) +
+                     np.sin(zen) * np.sin(slope) * np.cos(az - aspect))
+    return np.clip(np.rint(shade), 0, 255).astype(np.uint8)
+
+
+@pytest.mark.parametrize("shape,scale,dtype", [((1, 1), 1.0, np.float64), ((1, 37), 3.0, np.float64),
+                                               ((3, 3), 0.5, np.float32),
+                                               ((257, 131), 40.0, np.float64),
+                                               ((512, 512), 2.0, np.float32),
+                                               ((64, 600), 1e4, np.float64)])
+def test_hillshade_device_matches_numpy(shape, scale, dtype):
+    """ig_hillshade_u8 against the reference's float64 numpy expression on
+    smooth and rough fields (f32 input is widened exactly, as astype does)."""
+    from paper_2512_08309_b200 import transforms
+    rng = np.random.default_rng(shape[0] * 1000 + shape[1])
+    elev = np.cumsum(np.cumsum(rng.standard_normal(shape), 0), 1) * scale
+    elev = elev.astype(dtype)
+    got = transforms.hillshade_u8(elev)
+    want = _hillshade_numpy(elev)
+    diff = np.count_nonzero(got != want)
+    assert got.dtype == np.uint8 and got.shape == shape
+    assert diff == 0, f"{diff} of {got.size} pixels differ (max {np.abs(got.astype(int) - want).max()})"
+
+
 def test_render_constant_is_128(tmp_path):
     raster = str(tmp_path / "r.bin")
     out = str(tmp_path / "r.pgm")
