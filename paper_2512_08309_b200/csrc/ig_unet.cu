@@ -839,46 +839,53 @@ __device__ __forceinline__ void epi_pool_pair(const ConvArgs& a, const float* s_
         y1[i] += bb;
       }
     }
+    // 16 channels per step, 32-byte (whole-sector) stores: with 16-byte stores
+    // every warp store touched 32 lines for half a sector each, and the L1
+    // store path, not the MMAs, set the pace of the fused-pool epilogue
 #pragma unroll
-    for (int i = 0; i < BC / 8; ++i) {
-      uint4 o0, o1, q0, q1, po, pa;
-      __nv_bfloat162* ob0 = reinterpret_cast<__nv_bfloat162*>(&o0);
-      __nv_bfloat162* ob1 = reinterpret_cast<__nv_bfloat162*>(&o1);
-      __nv_bfloat162* qb0 = reinterpret_cast<__nv_bfloat162*>(&q0);
-      __nv_bfloat162* qb1 = reinterpret_cast<__nv_bfloat162*>(&q1);
-      __nv_bfloat162* pob = reinterpret_cast<__nv_bfloat162*>(&po);
-      __nv_bfloat162* pab = reinterpret_cast<__nv_bfloat162*>(&pa);
+    for (int i = 0; i < BC / 16; ++i) {
+      uint4 o0[2], o1[2], q0[2], q1[2], po[2], pa[2];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int k = 8 * i + 2 * j;
-        ob0[j] = __floats2bfloat162_rn(y0[k], y0[k + 1]);
-        ob1[j] = __floats2bfloat162_rn(y1[k], y1[k + 1]);
-        qb0[j] = __floats2bfloat162_rn(gsilu(y0[k], hg), gsilu(y0[k + 1], hg));
-        qb1[j] = __floats2bfloat162_rn(gsilu(y1[k], hg), gsilu(y1[k + 1], hg));
-        const float2 f0 = __bfloat1622float2(ob0[j]), f1 = __bfloat1622float2(ob1[j]);
-        const float h0x = f0.x + __shfl_xor_sync(0xffffffffu, f0.x, 1);
-        const float h0y = f0.y + __shfl_xor_sync(0xffffffffu, f0.y, 1);
-        const float h1x = f1.x + __shfl_xor_sync(0xffffffffu, f1.x, 1);
-        const float h1y = f1.y + __shfl_xor_sync(0xffffffffu, f1.y, 1);
-        const float mx = (h0x + h1x) * 0.25f, my = (h0y + h1y) * 0.25f;
-        pob[j] = __floats2bfloat162_rn(mx, my);
-        pab[j] = __floats2bfloat162_rn(gsilu(mx, hg), gsilu(my, hg));
+      for (int hh = 0; hh < 2; ++hh) {
+        __nv_bfloat162* ob0 = reinterpret_cast<__nv_bfloat162*>(&o0[hh]);
+        __nv_bfloat162* ob1 = reinterpret_cast<__nv_bfloat162*>(&o1[hh]);
+        __nv_bfloat162* qb0 = reinterpret_cast<__nv_bfloat162*>(&q0[hh]);
+        __nv_bfloat162* qb1 = reinterpret_cast<__nv_bfloat162*>(&q1[hh]);
+        __nv_bfloat162* pob = reinterpret_cast<__nv_bfloat162*>(&po[hh]);
+        __nv_bfloat162* pab = reinterpret_cast<__nv_bfloat162*>(&pa[hh]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = 16 * i + 8 * hh + 2 * j;
+          ob0[j] = __floats2bfloat162_rn(y0[k], y0[k + 1]);
+          ob1[j] = __floats2bfloat162_rn(y1[k], y1[k + 1]);
+          qb0[j] = __floats2bfloat162_rn(gsilu(y0[k], hg), gsilu(y0[k + 1], hg));
+          qb1[j] = __floats2bfloat162_rn(gsilu(y1[k], hg), gsilu(y1[k + 1], hg));
+          const float2 f0 = __bfloat1622float2(ob0[j]), f1 = __bfloat1622float2(ob1[j]);
+          const float h0x = f0.x + __shfl_xor_sync(0xffffffffu, f0.x, 1);
+          const float h0y = f0.y + __shfl_xor_sync(0xffffffffu, f0.y, 1);
+          const float h1x = f1.x + __shfl_xor_sync(0xffffffffu, f1.x, 1);
+          const float h1y = f1.y + __shfl_xor_sync(0xffffffffu, f1.y, 1);
+          const float mx = (h0x + h1x) * 0.25f, my = (h0y + h1y) * 0.25f;
+          pob[j] = __floats2bfloat162_rn(mx, my);
+          pab[j] = __floats2bfloat162_rn(gsilu(mx, hg), gsilu(my, hg));
+        }
       }
-      const int64_t co = c0 + b + 8 * i;
+      const int64_t co = c0 + b + 16 * i;
       if (out0) {
-        *reinterpret_cast<uint4*>(out0 + p0 * cout + co) = o0;
-        *reinterpret_cast<uint4*>(out0 + p1 * cout + co) = o1;
+        stg_v8(out0 + p0 * cout + co, o0[0], o0[1]);
+        stg_v8(out0 + p1 * cout + co, o1[0], o1[1]);
       }
       if (out1) {
-        *reinterpret_cast<uint4*>(out1 + p0 * cout + co) = q0;
-        *reinterpret_cast<uint4*>(out1 + p1 * cout + co) = q1;
+        stg_v8(out1 + p0 * cout + co, q0[0], q0[1]);
+        stg_v8(out1 + p1 * cout + co, q1[0], q1[1]);
       }
       if (even) {
-        *reinterpret_cast<uint4*>(pool0 + pp * cout + co) = po;
-        *reinterpret_cast<uint4*>(pool1 + pp * cout + co) = pa;
+        stg_v8(pool0 + pp * cout + co, po[0], po[1]);
+        stg_v8(pool1 + pp * cout + co, pa[0], pa[1]);
         if (pz >= 0) {
-          *reinterpret_cast<uint4*>(pool0 + pz * cout + co) = make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(pool1 + pz * cout + co) = make_uint4(0, 0, 0, 0);
+          const uint4 zz = make_uint4(0, 0, 0, 0);
+          stg_v8(pool0 + pz * cout + co, zz, zz);
+          stg_v8(pool1 + pz * cout + co, zz, zz);
         }
       }
     }

@@ -53,12 +53,13 @@ FUSED_UP = True              # 2x upsample folded into the consumer convs' TMA l
 FUSED_OUT = True             # output conv + preconditioning in one kernel (ig_unet_out_head)
 FUSED_GUTTER = True          # narrow levels (w <= 64) in the gutter layout (1-D tap shifts)
 # encoder 2x2 pool written by the producing conv's epilogue (bit-exact, tested).
-# Off: measured slower (r01: enc0.0.c2 479 -> 847 us) -- the c2 epilogue, not
-# the MMAs, is then the per-tile critical path (a second round of tanh /
-# shuffles / stores per column pair), which costs more than the pool kernel.
-# Re-measured r02 with the DYN / paired-skip kernels (IG_FUSED_POOL=1): 7.25 ->
-# 7.85 ms per 64-window forward, still off.
-FUSED_POOL = os.environ.get("IG_FUSED_POOL", "0") == "1"
+# The epilogue's global stores are its limiter: with 16-byte stores (every warp
+# store touching 32 lines for half a sector each) the fused pool measured slower
+# (r01: enc0.0.c2 479 -> 847 us); with whole-sector 32-byte stores (r02)
+# enc0.0.c2 + pool 512 -> 467 us and enc1.0.c2 + pool 312 -> 293 us, forward
+# 7.69 -> 7.59 ms per 64 windows (median of 4 alternated runs).  IG_FUSED_POOL:
+# 0 off, 2 only into standard-layout levels.
+FUSED_POOL = int(os.environ.get("IG_FUSED_POOL", "1"))
 FUSED_QKV = True             # attention q / k / v projections as one ig_conv_qkv launch
 
 
@@ -441,7 +442,8 @@ class UNetDevice:
                 wsk = self._skip_weights(nm, x.shape[3], c2.cout)
                 pool = None
                 if k + 1 < len(ops) and ops[k + 1][0] == "down" and \
-                        self._fusable_pool(h1, gut, c2.cout_pad):
+                        self._fusable_pool(h1, gut, c2.cout_pad) and \
+                        (FUSED_POOL != 2 or not self._gutter(lv + 1, w // 2)):
                     # the 2x2 pool of this block's output, written by its epilogue
                     ng = self._gutter(lv + 1, w // 2)
                     n_, h_ = h1.shape[0], h1.shape[1]
