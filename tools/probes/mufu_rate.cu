@@ -36,6 +36,31 @@ __global__ void f2fp_kernel(float* out, long long* cyc, int iters) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
   out[blockIdx.x * blockDim.x + threadIdx.x] = (float)acc;
 }
+// packed half-precision ex2: two results per instruction if MUFU runs it as one op
+__global__ void ex2h2_kernel(float* out, long long* cyc, int iters, int bf) {
+  uint32_t a = 0x3c003c00u + threadIdx.x, b = a ^ 0x10001u, c = a ^ 0x20002u, d = a ^ 0x30003u;
+  __syncthreads();
+  long long t0 = clock64();
+  if (bf) {
+    for (int i = 0; i < iters; ++i) {
+      asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(a));
+      asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(b));
+      asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(c));
+      asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(d));
+    }
+  } else {
+    for (int i = 0; i < iters; ++i) {
+      asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(a));
+      asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(b));
+      asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(c));
+      asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(d));
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (float)(a ^ b ^ c ^ d);
+}
 int main() {
   float* out; long long* cyc;
   cudaMalloc(&out, 148 * 1024 * 4);
@@ -52,5 +77,14 @@ int main() {
       printf("%s threads/SM %4d: %.2f ops/clk/SM\n", k ? "cvt.f16x2" : "ex2", threads, ops / h[0]);
     }
   }
+  for (int threads : {256, 512, 1024})
+    for (int bf = 0; bf < 2; ++bf) {
+      ex2h2_kernel<<<148, threads>>>(out, cyc, iters, bf);
+      long long h[148];
+      cudaDeviceSynchronize();
+      cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+      printf("%s threads/SM %4d: %.2f instr/clk/SM (x2 values)\n",
+             bf ? "ex2.bf16x2" : "ex2.f16x2", threads, 4.0 * iters * threads / h[0]);
+    }
   return 0;
 }
