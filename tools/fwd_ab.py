@@ -19,10 +19,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--windows", type=int, default=128)
 ap.add_argument("--reps", type=int, default=6)
 ap.add_argument("--tag", default="")
-ap.add_argument("--variant", type=int, default=0, help="ig_conv_set_variant (A/B)")
+ap.add_argument("--variant", type=int, default=None, help="ig_conv_set_variant (A/B)")
 args = ap.parse_args()
 from paper_2512_08309_b200._native import check, lib  # noqa: E402
-check(lib().ig_conv_set_variant(args.variant))
+if args.variant is not None:   # else IG_CONV_VARIANT (read at load) stands
+    check(lib().ig_conv_set_variant(args.variant))
 cfg = unet.UNetConfig()
 n = args.windows
 wxy = torch.tensor([[256 * k, 0] for k in range(n)], dtype=torch.int64, device="cuda")

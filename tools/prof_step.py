@@ -17,11 +17,12 @@ from paper_2512_08309_b200.grid import Region, WindowLayout  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--windows", type=int, default=64)
 ap.add_argument("--full", action="store_true")
-ap.add_argument("--variant", type=int, default=0, help="ig_conv_set_variant (A/B timing)")
+ap.add_argument("--variant", type=int, default=None, help="ig_conv_set_variant (A/B timing)")
 ap.add_argument("--fused-pool", action="store_true", help="unet.FUSED_POOL = True (A/B timing)")
 args = ap.parse_args()
 from paper_2512_08309_b200._native import check, lib  # noqa: E402
-check(lib().ig_conv_set_variant(args.variant))
+if args.variant is not None:   # else IG_CONV_VARIANT (read at load) stands
+    check(lib().ig_conv_set_variant(args.variant))
 unet.FUSED_POOL = unet.FUSED_POOL or args.fused_pool
 cfg = unet.UNetConfig()
 if args.full:
