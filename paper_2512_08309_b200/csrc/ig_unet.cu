@@ -528,12 +528,48 @@ __device__ __forceinline__ void epi_span(const ConvArgs& a, const float* s_scale
 // the SMEM fill drops from 192 KB (K = 256: 64 KB of A + 128 KB of weights) to
 // 64 KB; with the weights streamed the fill, not the tensor core, set the pace
 // (ncu r02, qkv: tensor pipe 31%, 45.5 us for 25.8 GFLOP).
-constexpr int WRES_STAGES = 5;
+// The grouped (q / k / v) WRES launch also stores through TMA: each epilogue
+// warp group stages one head (128 pixels x 64 channels, SWIZZLE_128B) in its
+// 16 KB buffer and one thread issues a bulk tensor store -- the per-lane
+// 32-byte global stores (32 lines per warp instruction) were the L1's limiter.
+constexpr int WRES_STAGES = 4;
 constexpr int WRES_BYTES = 128 * 1024;
+constexpr int WRES_STAGE_OUT = 2 * 16384;   // two epilogue warp groups x one head
 template <int N, bool WRES>
 __host__ __device__ constexpr int conv_tc_smem() {
-  return WRES ? 1024 + WRES_STAGES * ConvCfg<N>::A_BYTES + WRES_BYTES + 256 + 1024
+  return WRES ? 1024 + WRES_STAGES * ConvCfg<N>::A_BYTES + WRES_BYTES + 2048 + WRES_STAGE_OUT
               : ConvCfg<N>::SMEM;
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+// One 128-pixel x 64-channel output slab of a warp group through its 16 KB
+// staging buffer `sb` (this thread: pixel m, 16-byte chunks w[4c..4c+3],
+// SWIZZLE_128B positions) and one bulk tensor store at (c0, p0); the buffer is
+// rewritten only after the group's previous store has read it.
+__device__ __forceinline__ void slab_store(uint8_t* sb, int m, const uint32_t (&w)[32],
+                                           bool issuer, uint32_t bar, const CUtensorMap* map,
+                                           int c0, int p0) {
+  if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  named_bar_sync(bar, 128);
+  const uint32_t row = smem_u32(sb) + m * 128;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(row + ((c ^ (m & 7)) << 4)),
+                 "r"(w[4 * c]), "r"(w[4 * c + 1]), "r"(w[4 * c + 2]), "r"(w[4 * c + 3])
+                 : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  named_bar_sync(bar, 128);
+  if (issuer) {
+    tma_store_2d(map, smem_u32(sb), c0, p0);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
 }
 
 template <int N, bool WRES = false>
@@ -543,7 +579,10 @@ __global__ void __launch_bounds__(320, 1)
                    const __grid_constant__ CUtensorMap map_w,
                    const __grid_constant__ CUtensorMap map_sa,
                    const __grid_constant__ CUtensorMap map_sb,
-                   const __grid_constant__ CUtensorMap map_ws, const ConvArgs args) {
+                   const __grid_constant__ CUtensorMap map_ws,
+                   const __grid_constant__ CUtensorMap map_o0,
+                   const __grid_constant__ CUtensorMap map_o1,
+                   const __grid_constant__ CUtensorMap map_o2, const ConvArgs args) {
   using Cfg = ConvCfg<N>;
   constexpr int STAGES = WRES ? WRES_STAGES : Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -558,6 +597,7 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* wfull = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
   float* s_scale = reinterpret_cast<float*>(tmem_slot + 4);
+  uint8_t* s_out = reinterpret_cast<uint8_t*>(full) + 2048;   // WRES: TMA-store staging
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kchunks = args.kchunks_a + args.kchunks_b;
@@ -741,6 +781,87 @@ __global__ void __launch_bounds__(320, 1)
       const int64_t p = (int64_t)tile * 128 + m;
       const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * N;
       if (args.dbg & 1) {
+      } else if (WRES && args.groups > 1) {
+        // head-normalised q / k / v through the TMA store (see WRES_STAGE_OUT)
+        const int g = gt - tile * args.groups;
+        const CUtensorMap* mo = g == 0 ? &map_o0 : (g == 1 ? &map_o1 : &map_o2);
+        const float hsc = g == 0 ? args.head_scale : 1.f;
+        uint8_t* sb = s_out + half * 16384;
+        const bool issuer = warp == 2 + 4 * half && lane == 0;
+#pragma unroll 1
+        for (int hb = 0; hb < NC; hb += 64) {
+          uint32_t r[64];
+          tmem_ld32_nw(taddr + half * NC + hb, r);
+          tmem_ld32_nw(taddr + half * NC + hb + 32, r + 32);
+          tmem_wait_ld();
+          float ps[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) ps[j] = 0.f;
+#pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            const float v = __uint_as_float(r[i]);
+            ps[i & 7] = fmaf(v, v, ps[i & 7]);
+          }
+          const float ss =
+              ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+          const float inv = hsc / (1e-4f + sqrtf(ss) * 0.125f);
+          uint32_t w[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float a0 = __uint_as_float(r[2 * j]) * inv;
+            const float a1 = __uint_as_float(r[2 * j + 1]) * inv;
+            if (g == 2) {                      // v: f16 (the attention PV operand)
+              const __half2 h2 = __floats2half2_rn(a0, a1);
+              w[j] = *reinterpret_cast<const uint32_t*>(&h2);
+            } else {
+              const __nv_bfloat162 b2 = __floats2bfloat162_rn(a0, a1);
+              w[j] = *reinterpret_cast<const uint32_t*>(&b2);
+            }
+          }
+          slab_store(sb, m, w, issuer, 1 + half, mo, half * NC + hb, tile * 128);
+        }
+      } else if (WRES) {
+        // 1x1 with residual mp_sum and both outputs (the attention projection):
+        // y = ra * res + rb * acc, out0 = y, out1 = mp_silu(y), as epi_span
+        uint8_t* sb = s_out + half * 16384;
+        const bool issuer = warp == 2 + 4 * half && lane == 0;
+        const float hg = 0.5f * args.act_gain, ra = args.res_a, rb = args.res_b;
+        const __nv_bfloat16* __restrict__ resp = args.res + p * args.cout + half * NC;
+#pragma unroll 1
+        for (int hb = 0; hb < NC; hb += 64) {
+          uint4 rs[8];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) ldg_nc_v8(resp + hb + 16 * i, rs[2 * i], rs[2 * i + 1]);
+          uint32_t r[64];
+          tmem_ld32_nw(taddr + half * NC + hb, r);
+          tmem_ld32_nw(taddr + half * NC + hb + 32, r + 32);
+          tmem_wait_ld();
+          float y[64];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const __nv_bfloat162* rb2 = reinterpret_cast<const __nv_bfloat162*>(&rs[i]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 f = __bfloat1622float2(rb2[j]);
+              y[8 * i + 2 * j] = fmaf(ra, f.x, rb * __uint_as_float(r[8 * i + 2 * j]));
+              y[8 * i + 2 * j + 1] = fmaf(ra, f.y, rb * __uint_as_float(r[8 * i + 2 * j + 1]));
+            }
+          }
+          uint32_t w[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(y[2 * j], y[2 * j + 1]);
+            w[j] = *reinterpret_cast<const uint32_t*>(&b2);
+          }
+          slab_store(sb, m, w, issuer, 1 + half, &map_o0, half * NC + hb, tile * 128);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const __nv_bfloat162 b2 =
+                __floats2bfloat162_rn(gsilu(y[2 * j], hg), gsilu(y[2 * j + 1], hg));
+            w[j] = *reinterpret_cast<const uint32_t*>(&b2);
+          }
+          slab_store(sb, m, w, issuer, 1 + half, &map_o1, half * NC + hb, tile * 128);
+        }
       } else if (args.groups > 1) {
         const int g = gt - tile * args.groups;
         ConvArgs ga = args;
@@ -754,6 +875,8 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
+    if (WRES && (warp == 2 || warp == 6) && lane == 0)
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   __syncthreads();
   if (warp == 1) {
@@ -3878,16 +4001,41 @@ static int launch_conv_tc(const ig_conv_params_t* p, const ConvArgs& a, cudaStre
   }
   const int work = a.num_tiles * a.groups;
   const int kblocks = p->taps * (a.kchunks_a + a.kchunks_b) + a.kskip_a + a.kskip_b;
-  // resident weights for the fused q / k / v 1x1 conv (variant 20: streamed, A/B;
-  // r02: qkv 49.7 -> 47.0 us per 64 windows; the projection measured 42.1 -> 43.1,
-  // so the groups == 1 convs keep streaming)
-  if (p->taps == 1 && a.groups > 1 && kblocks * Cfg::B_BYTES <= WRES_BYTES && g_variant != 20) {
+  // per-group output maps of the WRES q / k / v launch: [pixels][cout] rows,
+  // one box = 128 pixels x 64 channels (one head), SWIZZLE_128B
+  CUtensorMap mo[3] = {ma, ma, ma};
+  const int64_t npix = (int64_t)p->n * p->h * p->w;
+  // groups == 1 through the TMA-store epilogue: 1x1, residual, both outputs
+  const bool wres1 = a.groups == 1 && p->taps == 1 && p->res && p->out0 && p->out1 && !p->up2 &&
+                     !p->bias && !p->scale && !p->gutter && N % 128 == 0;
+  if (a.groups > 1 || wres1) {
+    void* const outs[3] = {a.groups > 1 ? (void*)a.outg[0] : p->out0,
+                           a.groups > 1 ? (void*)a.outg[1] : p->out1,
+                           a.groups > 1 ? (void*)a.outg[2] : p->out1};
+    for (int g = 0; g < 3; ++g) {
+      cuuint64_t dims[2] = {(cuuint64_t)p->cout, (cuuint64_t)npix};
+      cuuint64_t strides[1] = {(cuuint64_t)p->cout * 2};
+      cuuint32_t box[2] = {64, 128};
+      cuuint32_t es[2] = {1, 1};
+      if (encode_fn()(&mo[g], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, outs[g], dims, strides, box,
+                      es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        set_error("ig_conv_qkv: cuTensorMapEncodeTiled(output) failed");
+        return IG_ERR_CUDA;
+      }
+    }
+  }
+  // resident weights + TMA-store epilogue for the attention block's 1x1 convs
+  // (variant 20: streamed weights, per-lane stores; A/B)
+  if (p->taps == 1 && (a.groups > 1 || wres1) && kblocks * Cfg::B_BYTES <= WRES_BYTES &&
+      g_variant != 20) {
     const int grid = ((work < kNumSMs ? work : kNumSMs) / a.groups) * a.groups;
-    { conv_tc_kernel<N, true><<<grid, 320, conv_tc_smem<N, true>(), st>>>(ma, mb, mw, msa, msb, mws, a); note_launch(); }
+    { conv_tc_kernel<N, true><<<grid, 320, conv_tc_smem<N, true>(), st>>>(ma, mb, mw, msa, msb, mws, mo[0], mo[1], mo[2], a); note_launch(); }
     return cuda_check("ig_conv_tc(wres)");
   }
   const int grid = work < kNumSMs ? work : kNumSMs;
-  { conv_tc_kernel<N><<<grid, 320, Cfg::SMEM, st>>>(ma, mb, mw, msa, msb, mws, a); note_launch(); }
+  { conv_tc_kernel<N><<<grid, 320, Cfg::SMEM, st>>>(ma, mb, mw, msa, msb, mws, ma, ma, ma, a); note_launch(); }
   return cuda_check("ig_conv_tc");
 }
 

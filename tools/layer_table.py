@@ -43,6 +43,7 @@ def layer_ops(cfg, win):
     seq = [] if fused else [("gather", "gather", win, 0, cfg.cin_pad, 0, 1, 0)]
     h = win
     c = ch[0]
+    pooled = False
     for k, op in enumerate(prog.ops):
         nxt = prog.ops[k + 1][0] if k + 1 < len(prog.ops) else None
         c2_outs = 1 if nxt in ("attn", "out") else 2     # unet.forward_after_stem
@@ -54,8 +55,13 @@ def layer_ops(cfg, win):
             c1 = prog.convs[nm + ".c1"]
             seq.append(("conv", nm + ".c1", h, c1.cin, c1.cout, 9, 1, 0))
             c2 = prog.convs[nm + ".c2"]
+            # the 2x2 pool written by the c2 epilogue (unet._fusable_pool): two more
+            # outputs at a quarter of the pixels, no separate pool launch
+            pooled = bool(unet.FUSED_POOL and nxt == "down" and h % 128 == 0
+                          and c2.cout in (64, 128))
             # c2 with the fused skip GEMM: reads the block input (c1.cin) once more
-            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, c2_outs, c1.cin / c2.cout))
+            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, c2_outs + 0.5 * pooled,
+                        c1.cin / c2.cout))
             c = c2.cout
         elif op[0] == "attn":
             nm = op[1]
@@ -67,7 +73,9 @@ def layer_ops(cfg, win):
             seq.append(("attn", nm + ".attn", h, c, 0, 0, 0, 0))
             seq.append(("conv", nm + ".proj", h, c, c, 1, 2, 1))
         elif op[0] == "down":
-            seq.append(("pool", "down", h, 0, 0, 0, 0, 0))
+            if not pooled:
+                seq.append(("pool", "down", h, c, 0, 0, 0, 0))
+            pooled = False
             h //= 2
         elif op[0] == "dec":
             nm = op[1]
@@ -113,6 +121,8 @@ def main():
             by = px * 2 * cin * 4
         elif kind == "up":
             by = px * 2 * cin * 5            # read h^2 c, write (2h)^2 c
+        elif kind == "pool":
+            by = px * 2 * cin * 1.5          # read x, write pool(x) and its mp_silu
         else:
             by = 0.0
         bound = max(fl / tf, by / bw) * 1e6
