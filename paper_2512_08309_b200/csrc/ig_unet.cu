@@ -1043,6 +1043,8 @@ struct HaloArgs {
   int l2pf_skip;     // CTA-pair kernel: L2-prefetch the next tile's 1x1 skip-GEMM boxes
   int pair_skip;     // CTA-pair kernel: two 1x1 skip chunks per halo slot
   int skip_first;    // CTA-pair kernel: a tile's skip chunks before its halo chunks
+  int tma_out;       // CTA-pair kernel: outputs through SMEM slabs + bulk tensor stores
+  int stage_off;     //   (the two 16 KB staging buffers at this offset of the SMEM base)
 };
 
 template <int N, int ROWS>
@@ -1430,7 +1432,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                       const __grid_constant__ CUtensorMap map_w,
                       const __grid_constant__ CUtensorMap map_sa,
                       const __grid_constant__ CUtensorMap map_sb,
-                      const __grid_constant__ CUtensorMap map_ws, const HaloArgs ha) {
+                      const __grid_constant__ CUtensorMap map_ws,
+                      const __grid_constant__ CUtensorMap map_o0,
+                      const __grid_constant__ CUtensorMap map_o1, const HaloArgs ha) {
   using Cfg = HaloCfg<N, ROWS>;
   constexpr int HBYTES = gut_slot_bytes<N, ROWS, GUT>();
   constexpr int BH = N / 2;                    // weight rows staged by this CTA
@@ -1868,7 +1872,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       const int tile = 2 * pr + (int)rank;
       const int img = tile / tiles_per_img;
       const int r = tile - img * tiles_per_img;
-      if constexpr (GUT) {
+      if (args.dbg & 1) {
+        // timing experiment only (IG_DBG): accumulator released unread
+      } else if constexpr (GUT) {
         // ROWS = 2: warp group g drains accumulator row g; ROWS = 1: the two
         // warp groups split the columns of the one row
         constexpr int NC = ROWS == 2 ? N : N / 2;
@@ -1901,6 +1907,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             epi_pool_pair<N / 2>(args, args.scale ? s_scale : nullptr, p0, p0 + args.w, pp, pz,
                                  grp * (N / 2), tl + (2 * j) * N, tl + (2 * j + 1) * N);
           }
+        } else if (ha.tma_out) {
+          // as epi_span (scale, mp_silu), each 128-pixel x 64-channel slab of an
+          // output staged in the warp group's buffer and bulk-stored by TMA
+          uint8_t* sb = smem + ha.stage_off + grp * 16384;
+          const bool issuer = warp == 2 + 4 * grp && lane == 0;
+          const float hg = 0.5f * args.act_gain;
+#pragma unroll 1
+          for (int row = grp; row < ROWS; row += 2) {
+            const int p0 = (int)(((int64_t)img * args.h + y0 + row) * args.w + x0);
+            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N +
+                                   (DYN ? (ROWS - 1 - row) : row) * N;
+#pragma unroll 1
+            for (int c0 = 0; c0 < N; c0 += 64) {
+              uint32_t r[64];
+              tmem_ld32_nw(taddr + c0, r);
+              tmem_ld32_nw(taddr + c0 + 32, r + 32);
+              tmem_wait_ld();
+              if (args.scale) {
+#pragma unroll
+                for (int i = 0; i < 64; ++i)
+                  r[i] = __float_as_uint(__uint_as_float(r[i]) * s_scale[c0 + i]);
+              }
+              uint32_t w[32];
+              if (args.out0) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                  const __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r[2 * j]),
+                                                                  __uint_as_float(r[2 * j + 1]));
+                  w[j] = *reinterpret_cast<const uint32_t*>(&b2);
+                }
+                slab_store(sb, m, w, issuer, 1 + grp, &map_o0, c0, p0);
+              }
+              if (args.out1) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                  const __nv_bfloat162 b2 =
+                      __floats2bfloat162_rn(gsilu(__uint_as_float(r[2 * j]), hg),
+                                            gsilu(__uint_as_float(r[2 * j + 1]), hg));
+                  w[j] = *reinterpret_cast<const uint32_t*>(&b2);
+                }
+                slab_store(sb, m, w, issuer, 1 + grp, &map_o1, c0, p0);
+              }
+            }
+          }
         } else {
           // warp group g drains accumulator rows g, g+2, ..
 #pragma unroll
@@ -1916,6 +1966,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc ? l_tempty1 : l_tempty0);
     }
+    if (ha.tma_out && (warp == 2 || warp == 6) && lane == 0)
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   cluster_sync_all();                          // no CTA leaves while its peer may signal it
@@ -4143,6 +4195,15 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
   return cuda_check("ig_conv_tc(halo)");
 }
 
+// TMA-store epilogue of the CTA-pair conv (1: the non-DYN layers, 2: also DYN).
+// r02 layer A/B (ncu launch lists): enc1.0.c1 141.7 -> 124.3, dec1.0.c2 310.0 ->
+// 300.2, dec1.1.c1 312.3 -> 303.4 us per 64 windows (forward -47 us); the DYN
+// layers lose a third of their weight ring to the staging (dec0.0.c1 688 -> 863)
+// and the four-row cout-64 layers have no room, so they keep per-lane stores.
+static int g_tma_out = [] {
+  const char* e = getenv("IG_TMA_OUT");
+  return e ? atoi(e) : 1;
+}();
 static int g_dbg = [] {
   const char* e = getenv("IG_DBG");
   return e ? atoi(e) : 0;
@@ -4244,6 +4305,29 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   ha.l2pf_skip = g_l2pf_skip;
   ha.pair_skip = g_pair_skip;
   ha.skip_first = g_skip_first && g_variant == 0;   // A/B variants keep the r01 order
+  // TMA-store epilogue (IG_TMA_OUT; variants keep per-lane stores)
+  ha.tma_out = g_tma_out && g_variant == 0 && !GUT && !p->pool0 && !p->res && !p->bias &&
+               !p->up2 && N % 64 == 0 && (p->out0 || p->out1) &&
+               (g_tma_out > 1 || !DYN);
+  CUtensorMap mo0 = ma, mo1 = ma;
+  if (ha.tma_out) {
+    const int64_t npix = (int64_t)p->n * p->h * p->w;
+    for (int k = 0; k < 2; ++k) {
+      void* base = k ? p->out1 : p->out0;
+      if (!base) continue;
+      cuuint64_t dims[2] = {(cuuint64_t)p->cout, (cuuint64_t)npix};
+      cuuint64_t strides[1] = {(cuuint64_t)p->cout * 2};
+      cuuint32_t box[2] = {64, 128};
+      cuuint32_t es[2] = {1, 1};
+      if (encode_fn()(k ? &mo1 : &mo0, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides,
+                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        set_error("ig_conv_tc(halo2): cuTensorMapEncodeTiled(output) failed");
+        return IG_ERR_CUDA;
+      }
+    }
+  }
   if (GUT) {
     ha.tiles_x = 1;
     ha.tiles_y = (a.gP + ROWS * 128 - 1) / (ROWS * 128);
@@ -4261,46 +4345,61 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   constexpr int kBudget = 226 * 1024;
   constexpr int SBYTES = ROWS * 128 * 128;
   int smem = 0;
-  ha.hbufs = 0;
-  // variant 6: skip chunks in their own ring (when it fits next to resident
-  // weights), so an 8-MMA skip chunk never holds a halo slot.  Off by default:
-  // measured neutral-to-slower (r01: enc0.0.c2 479 -> 492 us, dec0.1.c2 571 -> 606)
   const int kskip = a.kskip_a + a.kskip_b;
-  ha.sbufs = 0;
-  if (kskip && g_variant == 6) {
-    for (int sb = (kskip >= 2 ? 2 : 1); sb >= 1 && !ha.sbufs; --sb)
-      if (1024 + 2 * HBYTES + sb * SBYTES + 512 + 1024 + wbytes <= kBudget) ha.sbufs = sb;
-  }
-  // (r01: three buffers measured slower for the layers whose weights are
-  // resident with two -- they then stream per tile).  Layers that stream their
-  // weights anyway (multi-chunk cout 128) may take a third halo slot, so a short
-  // skip chunk's load is two chunks ahead (IG_HALO3=1 / variant 4 to force it).
-  // Measured slower (r02, tools/ab_layers.sh: dec1.0.c1 1608 -> 1439, dec1.1.c2
-  // 1039 -> 976 TFLOP/s; the weight ring drops to 3 stages), so off by default.
-  const bool streams2 = 1024 + 2 * HBYTES + 512 + 1024 + wbytes > kBudget;
-  const bool try3 = g_variant == 4 || (g_halo3 && streams2 && !DYN && !GUT && N == 128);
-  for (int hb = try3 ? 3 : 2; hb >= 2 && !ha.hbufs; --hb) {
-    const int fixed = 1024 + hb * HBYTES + ha.sbufs * SBYTES + 512 + 1024;
-    if (fixed + wbytes <= kBudget) {
-      ha.hbufs = hb;
-      ha.resident = 1;
-      ha.b_stages = 1;
-      smem = fixed + wbytes;
-    } else {
-      int stages = (kBudget - fixed) / wunit;
-      if (stages > 16) stages = 16;
-      if (stages >= (hb == 3 ? 3 : 2)) {
+  // SMEM plan for `stage_bytes` of output staging: false when the weight ring
+  // would not fit
+  auto plan = [&](int stage_bytes) -> bool {
+    ha.hbufs = 0;
+    // variant 6: skip chunks in their own ring (when it fits next to resident
+    // weights), so an 8-MMA skip chunk never holds a halo slot.  Off by default:
+    // measured neutral-to-slower (r01: enc0.0.c2 479 -> 492 us, dec0.1.c2 571 -> 606)
+    ha.sbufs = 0;
+    if (kskip && g_variant == 6) {
+      for (int sb = (kskip >= 2 ? 2 : 1); sb >= 1 && !ha.sbufs; --sb)
+        if (1024 + 2 * HBYTES + sb * SBYTES + 512 + 1024 + stage_bytes + wbytes <= kBudget)
+          ha.sbufs = sb;
+    }
+    // (r01: three buffers measured slower for the layers whose weights are
+    // resident with two -- they then stream per tile).  Layers that stream their
+    // weights anyway (multi-chunk cout 128) may take a third halo slot, so a short
+    // skip chunk's load is two chunks ahead (IG_HALO3=1 / variant 4 to force it).
+    // Measured slower (r02, tools/ab_layers.sh: dec1.0.c1 1608 -> 1439, dec1.1.c2
+    // 1039 -> 976 TFLOP/s; the weight ring drops to 3 stages), so off by default.
+    const bool streams2 = 1024 + 2 * HBYTES + 512 + 1024 + stage_bytes + wbytes > kBudget;
+    const bool try3 = g_variant == 4 || (g_halo3 && streams2 && !DYN && !GUT && N == 128);
+    for (int hb = try3 ? 3 : 2; hb >= 2 && !ha.hbufs; --hb) {
+      const int fixed = 1024 + hb * HBYTES + ha.sbufs * SBYTES + 512 + 1024 + stage_bytes;
+      if (fixed + wbytes <= kBudget) {
         ha.hbufs = hb;
-        ha.resident = 0;
-        ha.b_stages = stages;
-        smem = fixed + stages * wunit;
+        ha.resident = 1;
+        ha.b_stages = 1;
+        smem = fixed + wbytes;
+      } else {
+        int stages = (kBudget - fixed) / wunit;
+        if (stages > 16) stages = 16;
+        // the output staging may not cost a thin weight ring
+        const int need = stage_bytes ? (DYN ? 2 : 4) : (hb == 3 ? 3 : 2);
+        if (stages >= need) {
+          ha.hbufs = hb;
+          ha.resident = 0;
+          ha.b_stages = stages;
+          smem = fixed + stages * wunit;
+        }
       }
     }
+    return ha.hbufs != 0;
+  };
+  if (!(ha.tma_out && plan(2 * 16384 + 1024))) {
+    ha.tma_out = 0;
+    plan(0);
   }
   if (!ha.hbufs) {
     set_error("ig_conv_tc(halo2): no room for the weight ring");
     return IG_ERR_UNSUPPORTED;
   }
+  // staging after the barriers / scale vector, 1 KB aligned (SWIZZLE_128B)
+  ha.stage_off = (ha.hbufs * HBYTES + ha.sbufs * SBYTES +
+                  (ha.resident ? wbytes : ha.b_stages * wunit) + 512 + 1024 + 1023) & ~1023;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(conv_halo2_kernel<N, ROWS, GUT, DYN>,
@@ -4309,7 +4408,7 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   }
   const int ctas = 2 * ((ha.c.num_tiles + 1) / 2);
   const int grid = ctas < kNumSMs ? ctas : kNumSMs;
-  { conv_halo2_kernel<N, ROWS, GUT, DYN><<<grid, Cfg::THREADS, smem, st>>>(ma, mb, mw, msa, msb, mws, ha); note_launch(); }
+  { conv_halo2_kernel<N, ROWS, GUT, DYN><<<grid, Cfg::THREADS, smem, st>>>(ma, mb, mw, msa, msb, mws, mo0, mo1, ha); note_launch(); }
   return cuda_check("ig_conv_tc(halo2)");
 }
 
