@@ -549,6 +549,26 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
+// 32-channel variant (SWIZZLE_64B, 8 KB per warp group: 64-byte rows, chunk c
+// at c ^ ((row >> 1) & 3)) for kernels that cannot spare 32 KB of staging
+__device__ __forceinline__ void slab_store32(uint8_t* sb, int m, const uint32_t (&w)[16],
+                                             bool issuer, uint32_t bar, const CUtensorMap* map,
+                                             int c0, int p0) {
+  if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  named_bar_sync(bar, 128);
+  const uint32_t row = smem_u32(sb) + m * 64;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(row + ((c ^ ((m >> 1) & 3)) << 4)),
+                 "r"(w[4 * c]), "r"(w[4 * c + 1]), "r"(w[4 * c + 2]), "r"(w[4 * c + 3])
+                 : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  named_bar_sync(bar, 128);
+  if (issuer) {
+    tma_store_2d(map, smem_u32(sb), c0, p0);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
 // One 128-pixel x 64-channel output slab of a warp group through its 16 KB
 // staging buffer `sb` (this thread: pixel m, 16-byte chunks w[4c..4c+3],
 // SWIZZLE_128B positions) and one bulk tensor store at (c0, p0); the buffer is
@@ -1906,6 +1926,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N;
             epi_pool_pair<N / 2>(args, args.scale ? s_scale : nullptr, p0, p0 + args.w, pp, pz,
                                  grp * (N / 2), tl + (2 * j) * N, tl + (2 * j + 1) * N);
+          }
+        } else if (ha.tma_out == 2) {
+          // 32-channel slabs (8 KB per warp group), as the branch below
+          uint8_t* sb = smem + ha.stage_off + grp * 8192;
+          const bool issuer = warp == 2 + 4 * grp && lane == 0;
+          const float hg = 0.5f * args.act_gain;
+#pragma unroll 1
+          for (int row = grp; row < ROWS; row += 2) {
+            const int p0 = (int)(((int64_t)img * args.h + y0 + row) * args.w + x0);
+            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N +
+                                   (DYN ? (ROWS - 1 - row) : row) * N;
+#pragma unroll 1
+            for (int c0 = 0; c0 < N; c0 += 32) {
+              uint32_t r[32];
+              tmem_ld32_nw(taddr + c0, r);
+              tmem_wait_ld();
+              if (args.scale) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  r[i] = __float_as_uint(__uint_as_float(r[i]) * s_scale[c0 + i]);
+              }
+              uint32_t w[16];
+              if (args.out0) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                  const __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r[2 * j]),
+                                                                  __uint_as_float(r[2 * j + 1]));
+                  w[j] = *reinterpret_cast<const uint32_t*>(&b2);
+                }
+                slab_store32(sb, m, w, issuer, 1 + grp, &map_o0, c0, p0);
+              }
+              if (args.out1) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                  const __nv_bfloat162 b2 =
+                      __floats2bfloat162_rn(gsilu(__uint_as_float(r[2 * j]), hg),
+                                            gsilu(__uint_as_float(r[2 * j + 1]), hg));
+                  w[j] = *reinterpret_cast<const uint32_t*>(&b2);
+                }
+                slab_store32(sb, m, w, issuer, 1 + grp, &map_o1, c0, p0);
+              }
+            }
           }
         } else if (ha.tma_out) {
           // as epi_span (scale, mp_silu), each 128-pixel x 64-channel slab of an
@@ -4195,14 +4257,17 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
   return cuda_check("ig_conv_tc(halo)");
 }
 
-// TMA-store epilogue of the CTA-pair conv (1: the non-DYN layers, 2: also DYN).
-// r02 layer A/B (ncu launch lists): enc1.0.c1 141.7 -> 124.3, dec1.0.c2 310.0 ->
-// 300.2, dec1.1.c1 312.3 -> 303.4 us per 64 windows (forward -47 us); the DYN
-// layers lose a third of their weight ring to the staging (dec0.0.c1 688 -> 863)
-// and the four-row cout-64 layers have no room, so they keep per-lane stores.
+// TMA-store epilogue of the CTA-pair conv.  r02 layer A/B (ncu launch lists,
+// us per 64 windows): 1 = the non-DYN layers with 64-channel slabs (enc1.0.c1
+// 141.7 -> 124.3, dec1.0.c2 310.0 -> 300.2, dec1.1.c1 312.3 -> 303.4); 2 (default)
+// = also the DYN layers with 32-channel slabs, whose weight ring keeps its three
+// stages (enc0.0.c1 313 -> 279, dec0.0.c1 703 -> 679, dec0.1.c1 518 -> 498; with
+// 64-channel slabs the ring lost a stage: dec0.0.c1 688 -> 863); 3 = also the
+// four-row cout-64 c2 layers on a two-stage weight ring (dec0.0.c2 506 -> 550,
+// slower).  0: per-lane stores everywhere.
 static int g_tma_out = [] {
   const char* e = getenv("IG_TMA_OUT");
-  return e ? atoi(e) : 1;
+  return e ? atoi(e) : 2;
 }();
 static int g_dbg = [] {
   const char* e = getenv("IG_DBG");
@@ -4309,6 +4374,10 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   ha.tma_out = g_tma_out && g_variant == 0 && !GUT && !p->pool0 && !p->res && !p->bias &&
                !p->up2 && N % 64 == 0 && (p->out0 || p->out1) &&
                (g_tma_out > 1 || !DYN);
+  // DYN layers (their weight ring cannot spare 32 KB): 32-channel slabs, 16 KB;
+  // IG_TMA_OUT=3 also for the four-row cout-64 layers (A/B)
+  if (ha.tma_out && (DYN || (g_tma_out > 2 && ROWS == 4))) ha.tma_out = 2;
+  const int slab_c = ha.tma_out == 2 ? 32 : 64;
   CUtensorMap mo0 = ma, mo1 = ma;
   if (ha.tma_out) {
     const int64_t npix = (int64_t)p->n * p->h * p->w;
@@ -4317,10 +4386,11 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
       if (!base) continue;
       cuuint64_t dims[2] = {(cuuint64_t)p->cout, (cuuint64_t)npix};
       cuuint64_t strides[1] = {(cuuint64_t)p->cout * 2};
-      cuuint32_t box[2] = {64, 128};
+      cuuint32_t box[2] = {(cuuint32_t)slab_c, 128};
       cuuint32_t es[2] = {1, 1};
       if (encode_fn()(k ? &mo1 : &mo0, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides,
-                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      slab_c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
         set_error("ig_conv_tc(halo2): cuTensorMapEncodeTiled(output) failed");
@@ -4378,7 +4448,8 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
         int stages = (kBudget - fixed) / wunit;
         if (stages > 16) stages = 16;
         // the output staging may not cost a thin weight ring
-        const int need = stage_bytes ? (DYN ? 2 : 4) : (hb == 3 ? 3 : 2);
+        const int need =
+            stage_bytes ? (DYN ? 3 : (ROWS == 4 && g_tma_out > 2 ? 2 : 4)) : (hb == 3 ? 3 : 2);
         if (stages >= need) {
           ha.hbufs = hb;
           ha.resident = 0;
@@ -4389,7 +4460,7 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
     }
     return ha.hbufs != 0;
   };
-  if (!(ha.tma_out && plan(2 * 16384 + 1024))) {
+  if (!(ha.tma_out && plan(2 * 128 * slab_c * 2 + 1024))) {
     ha.tma_out = 0;
     plan(0);
   }
