@@ -549,6 +549,26 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
+// 16-channel variant (SWIZZLE_32B, 4 KB per warp group: 32-byte rows, chunk c
+// at c ^ ((row >> 2) & 1))
+__device__ __forceinline__ void slab_store16(uint8_t* sb, int m, const uint32_t (&w)[8],
+                                             bool issuer, uint32_t bar, const CUtensorMap* map,
+                                             int c0, int p0) {
+  if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  named_bar_sync(bar, 128);
+  const uint32_t row = smem_u32(sb) + m * 32;
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(row + ((c ^ ((m >> 2) & 1)) << 4)),
+                 "r"(w[4 * c]), "r"(w[4 * c + 1]), "r"(w[4 * c + 2]), "r"(w[4 * c + 3])
+                 : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  named_bar_sync(bar, 128);
+  if (issuer) {
+    tma_store_2d(map, smem_u32(sb), c0, p0);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
 // 32-channel variant (SWIZZLE_64B, 8 KB per warp group: 64-byte rows, chunk c
 // at c ^ ((row >> 1) & 3)) for kernels that cannot spare 32 KB of staging
 __device__ __forceinline__ void slab_store32(uint8_t* sb, int m, const uint32_t (&w)[16],
@@ -1926,6 +1946,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             const uint32_t tl = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N;
             epi_pool_pair<N / 2>(args, args.scale ? s_scale : nullptr, p0, p0 + args.w, pp, pz,
                                  grp * (N / 2), tl + (2 * j) * N, tl + (2 * j + 1) * N);
+          }
+        } else if (ha.tma_out == 3) {
+          // 16-channel slabs (4 KB per warp group), as the branch below
+          uint8_t* sb = smem + ha.stage_off + grp * 4096;
+          const bool issuer = warp == 2 + 4 * grp && lane == 0;
+          const float hg = 0.5f * args.act_gain;
+#pragma unroll 1
+          for (int row = grp; row < ROWS; row += 2) {
+            const int p0 = (int)(((int64_t)img * args.h + y0 + row) * args.w + x0);
+            const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ROWS * N +
+                                   (DYN ? (ROWS - 1 - row) : row) * N;
+#pragma unroll 1
+            for (int c0 = 0; c0 < N; c0 += 32) {
+              uint32_t r[32];
+              tmem_ld32_nw(taddr + c0, r);
+              tmem_wait_ld();
+              if (args.scale) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  r[i] = __float_as_uint(__uint_as_float(r[i]) * s_scale[c0 + i]);
+              }
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                uint32_t w[8];
+                if (args.out0) {
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) {
+                    const __nv_bfloat162 b2 = __floats2bfloat162_rn(
+                        __uint_as_float(r[16 * hh + 2 * j]), __uint_as_float(r[16 * hh + 2 * j + 1]));
+                    w[j] = *reinterpret_cast<const uint32_t*>(&b2);
+                  }
+                  slab_store16(sb, m, w, issuer, 1 + grp, &map_o0, c0 + 16 * hh, p0);
+                }
+                if (args.out1) {
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) {
+                    const __nv_bfloat162 b2 =
+                        __floats2bfloat162_rn(gsilu(__uint_as_float(r[16 * hh + 2 * j]), hg),
+                                              gsilu(__uint_as_float(r[16 * hh + 2 * j + 1]), hg));
+                    w[j] = *reinterpret_cast<const uint32_t*>(&b2);
+                  }
+                  slab_store16(sb, m, w, issuer, 1 + grp, &map_o1, c0 + 16 * hh, p0);
+                }
+              }
+            }
           }
         } else if (ha.tma_out == 2) {
           // 32-channel slabs (8 KB per warp group), as the branch below
@@ -4258,16 +4323,17 @@ static int launch_conv_halo(const ig_conv_params_t* p, const ConvArgs& a, cudaSt
 }
 
 // TMA-store epilogue of the CTA-pair conv.  r02 layer A/B (ncu launch lists,
-// us per 64 windows): 1 = the non-DYN layers with 64-channel slabs (enc1.0.c1
-// 141.7 -> 124.3, dec1.0.c2 310.0 -> 300.2, dec1.1.c1 312.3 -> 303.4); 2 (default)
-// = also the DYN layers with 32-channel slabs, whose weight ring keeps its three
-// stages (enc0.0.c1 313 -> 279, dec0.0.c1 703 -> 679, dec0.1.c1 518 -> 498; with
-// 64-channel slabs the ring lost a stage: dec0.0.c1 688 -> 863); 3 = also the
-// four-row cout-64 c2 layers on a two-stage weight ring (dec0.0.c2 506 -> 550,
-// slower).  0: per-lane stores everywhere.
+// us per 64 windows): 1 = the non-DYN cout-128 layers with 64-channel slabs
+// (enc1.0.c1 141.7 -> 124.3, dec1.0.c2 310.0 -> 300.2, dec1.1.c1 312.3 -> 303.4);
+// 2 = also the DYN layers with 32-channel slabs, whose weight ring keeps its
+// three stages (enc0.0.c1 313 -> 279, dec0.0.c1 703 -> 679, dec0.1.c1 518 -> 498;
+// with 64-channel slabs the ring lost a stage: dec0.0.c1 688 -> 863); 3 (default)
+// = also the four-row cout-64 c2 layers with 16-channel slabs, four weight stages
+// kept (dec0.0.c2 491.8 -> 481.3, dec0.1.c2 445.3 -> 432.3; 32-channel slabs left
+// them two stages: 506 -> 550).  0: per-lane stores everywhere.
 static int g_tma_out = [] {
   const char* e = getenv("IG_TMA_OUT");
-  return e ? atoi(e) : 2;
+  return e ? atoi(e) : 3;
 }();
 static int g_dbg = [] {
   const char* e = getenv("IG_DBG");
@@ -4375,9 +4441,10 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
                !p->up2 && N % 64 == 0 && (p->out0 || p->out1) &&
                (g_tma_out > 1 || !DYN);
   // DYN layers (their weight ring cannot spare 32 KB): 32-channel slabs, 16 KB;
-  // IG_TMA_OUT=3 also for the four-row cout-64 layers (A/B)
-  if (ha.tma_out && (DYN || (g_tma_out > 2 && ROWS == 4))) ha.tma_out = 2;
-  const int slab_c = ha.tma_out == 2 ? 32 : 64;
+  // the four-row cout-64 layers (two 100 KB halo slots): 16-channel slabs, 8 KB
+  if (ha.tma_out && DYN) ha.tma_out = 2;
+  if (ha.tma_out && g_tma_out > 2 && ROWS == 4 && !DYN) ha.tma_out = 3;
+  const int slab_c = ha.tma_out == 3 ? 16 : (ha.tma_out == 2 ? 32 : 64);
   CUtensorMap mo0 = ma, mo1 = ma;
   if (ha.tma_out) {
     const int64_t npix = (int64_t)p->n * p->h * p->w;
@@ -4390,7 +4457,9 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
       cuuint32_t es[2] = {1, 1};
       if (encode_fn()(k ? &mo1 : &mo0, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides,
                       box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      slab_c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                      slab_c == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
+                      : slab_c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                     : CU_TENSOR_MAP_SWIZZLE_128B,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
         set_error("ig_conv_tc(halo2): cuTensorMapEncodeTiled(output) failed");
@@ -4448,8 +4517,7 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
         int stages = (kBudget - fixed) / wunit;
         if (stages > 16) stages = 16;
         // the output staging may not cost a thin weight ring
-        const int need =
-            stage_bytes ? (DYN ? 3 : (ROWS == 4 && g_tma_out > 2 ? 2 : 4)) : (hb == 3 ? 3 : 2);
+        const int need = stage_bytes ? (DYN ? 3 : 4) : (hb == 3 ? 3 : 2);
         if (stages >= need) {
           ha.hbufs = hb;
           ha.resident = 0;
