@@ -4140,7 +4140,8 @@ static int make_w_map(CUtensorMap* m, const void* base, int ktot, int cout, int 
 static int g_variant = 0;   // 0 auto, 1 per-tap only, 2 no row-ring, 3 no CTA pairs,
                             // 4 CTA pairs with three halo buffers, 5 no 4-row tiles,
                             // 6 separate ring for the skip chunks, 7 2-row/3-buffer out head,
-                            // 8 per-tap out head for C = 1, 20 streamed 1x1 weights
+                            // 8 per-tap out head for C = 1, 20 streamed 1x1 weights,
+                            // 21 default kernels with per-lane epilogue stores
 
 template <int N>
 static int launch_conv_tc(const ig_conv_params_t* p, const ConvArgs& a, cudaStream_t st) {
@@ -4208,7 +4209,7 @@ static int launch_conv_tc(const ig_conv_params_t* p, const ConvArgs& a, cudaStre
   // resident weights + TMA-store epilogue for the attention block's 1x1 convs
   // (variant 20: streamed weights, per-lane stores; A/B)
   if (p->taps == 1 && (a.groups > 1 || wres1) && kblocks * Cfg::B_BYTES <= WRES_BYTES &&
-      g_variant != 20) {
+      g_variant != 20 && g_variant != 21) {
     const int grid = ((work < kNumSMs ? work : kNumSMs) / a.groups) * a.groups;
     { conv_tc_kernel<N, true><<<grid, 320, conv_tc_smem<N, true>(), st>>>(ma, mb, mw, msa, msb, mws, mo[0], mo[1], mo[2], a); note_launch(); }
     return cuda_check("ig_conv_tc(wres)");
@@ -4435,8 +4436,9 @@ static int launch_conv_halo2(const ig_conv_params_t* p, const ConvArgs& a, cudaS
   ha.l2pf = g_variant != 12 && N == 64 && a.kchunks_a + a.kchunks_b == 1;
   ha.l2pf_skip = g_l2pf_skip;
   ha.pair_skip = g_pair_skip;
-  ha.skip_first = g_skip_first && g_variant == 0;   // A/B variants keep the r01 order
+  ha.skip_first = g_skip_first && (g_variant == 0 || g_variant == 21);   // A/B variants keep the r01 order
   // TMA-store epilogue (IG_TMA_OUT; variants keep per-lane stores)
+  // variant 21: the default kernels with per-lane stores (bit-identity tests)
   ha.tma_out = g_tma_out && g_variant == 0 && !GUT && !p->pool0 && !p->res && !p->bias &&
                !p->up2 && N % 64 == 0 && (p->out0 || p->out1) &&
                (g_tma_out > 1 || !DYN);
@@ -4683,7 +4685,8 @@ int ig_conv_tc(const ig_conv_params_t* p, void* workspace, void* cuda_stream) {
     // multi-chunk layers.
     // cout-64 3x3 convs without a skip GEMM (the c1 layers of the 256^2 level):
     // the dy taps in N (DYN); any A/B variant (e.g. 19): the per-tap schedule
-    if (p->cout == 64 && !p->pool0 && g_variant == 0 && g_dyn_skip >= (a.kskip_a + a.kskip_b ? 1 : 0))
+    if (p->cout == 64 && !p->pool0 && (g_variant == 0 || g_variant == 21) &&
+        g_dyn_skip >= (a.kskip_a + a.kskip_b ? 1 : 0))
       return launch_conv_halo2<64, 2, false, true>(p, a, st);
     const bool deep = g_variant != 15 || a.kchunks_a + a.kchunks_b >= 2 ||
                       a.kskip_a + a.kskip_b >= 3;

@@ -775,6 +775,29 @@ def test_conv_1x1_resident_weights_match_streamed(n, h, w, groups):
         assert err < 2e-2 * ref.abs().max().item(), err
 
 
+@pytest.mark.parametrize("steps_t", [2, 1])
+def test_unet_tma_store_epilogues_bit_identical(steps_t):
+    """Every TMA-store epilogue (CTA-pair convs with 64/32/16-channel slabs, the
+    resident-weight q/k/v and projection) writes the same bits as the per-lane
+    store epilogues of the same kernels (variant 21): the default network's Phi
+    on 256-px windows, both sigma steps, is bitwise equal."""
+    cfg = unet.UNetConfig()
+    n = 3
+    g = torch.Generator(device=DEV).manual_seed(11 + steps_t)
+    src = torch.randn(n, 1, 256, 256, device=DEV, generator=g)
+    wxy = torch.tensor([[256 * k + 128, -384] for k in range(n)], dtype=torch.int64, device=DEV)
+    outs = []
+    for variant in (0, 21):
+        check(lib().ig_conv_set_variant(variant))
+        try:
+            outs.append(unet.unet_phi_batch(cfg, src, None, wxy, 256, steps_t, None, seed=5,
+                                            steps=2))
+            torch.cuda.synchronize()
+        finally:
+            check(lib().ig_conv_set_variant(0))
+    assert torch.equal(outs[0].view(torch.int32), outs[1].view(torch.int32))
+
+
 @pytest.mark.parametrize("n,hw,c", [(2, 1024, 256), (1, 200, 128)])
 def test_attention_p_in_tmem_matches_smem_path(n, hw, c):
     """The default attention kernel (attention2_kernel) keeps P in its own TMEM
