@@ -2518,6 +2518,10 @@ __global__ void __launch_bounds__(128) unet_stem_kernel(
     const __nv_bfloat16* __restrict__ wstem, float act_gain, __nv_bfloat16* __restrict__ out_x,
     __nv_bfloat16* __restrict__ out_xa, float* __restrict__ x_noisy) {
   static_assert(9 * P <= 64 && P <= GPL, "stem: planes do not tap-pack into 64 channels");
+  // bf16 slots per position: the next power of two >= P.  With GPL (8) slots a
+  // warp's 32 positions were 16 B apart and every plane store / tap load was a
+  // 4-way bank conflict (ncu r02: 4.5M excess shared wavefronts per launch)
+  constexpr int SPL = P <= 2 ? 2 : (P <= 4 ? 4 : 8);
   __shared__ __align__(1024) uint8_t sA[128 * 128];       // packed A tile (SW128)
   __shared__ __align__(1024) uint8_t sB[STEM_N * 128];    // stem weights (SW128)
   __shared__ __align__(16) __nv_bfloat16 planes[STEM_PLANES_MAX * GPL];
@@ -2557,8 +2561,13 @@ __global__ void __launch_bounds__(128) unet_stem_kernel(
   for (int q = tid; q < npos; q += 128) {
     const int hy = q / hw, hx = q - hy * hw;
     const int y = y0 + hy - 1, x = x0 + hx - 1;
-    __nv_bfloat16* pq = planes + q * GPL;
-    *reinterpret_cast<uint4*>(pq) = make_uint4(0, 0, 0, 0);
+    __nv_bfloat16* pq = planes + q * SPL;
+    if constexpr (SPL == 2)
+      *reinterpret_cast<uint32_t*>(pq) = 0u;
+    else if constexpr (SPL == 4)
+      *reinterpret_cast<uint2*>(pq) = make_uint2(0, 0);
+    else
+      *reinterpret_cast<uint4*>(pq) = make_uint4(0, 0, 0, 0);
     if (y >= 0 && y < win && x >= 0 && x < win) {
       const bool interior = hy >= 1 && hy <= srows && hx >= 1 && hx <= tw;
       gather_planes(src, src_batched, sx0, sy0, sw, sh, C, k, win, y, x, WX + x, WY + y, cpar,
@@ -2589,9 +2598,17 @@ __global__ void __launch_bounds__(128) unet_stem_kernel(
       for (int tap = 0; tap < 9; ++tap) {
         union {
           uint4 v;
+          uint2 v2;
+          uint32_t v1;
           __nv_bfloat16 e[8];
         } pv;
-        pv.v = *reinterpret_cast<const uint4*>(planes + (q0 + (tap / 3) * hw + tap % 3) * GPL);
+        const __nv_bfloat16* pt = planes + (q0 + (tap / 3) * hw + tap % 3) * SPL;
+        if constexpr (SPL == 2)
+          pv.v1 = *reinterpret_cast<const uint32_t*>(pt);
+        else if constexpr (SPL == 4)
+          pv.v2 = *reinterpret_cast<const uint2*>(pt);
+        else
+          pv.v = *reinterpret_cast<const uint4*>(pt);
 #pragma unroll
         for (int p = 0; p < P; ++p) row.e[tap * P + p] = pv.e[p];
       }
