@@ -36,7 +36,9 @@ def launches(path):
 
 
 def layer_ops(cfg, win):
-    """Expected launch sequence of one forward: (kind, name, h, cin, cout, taps, outs, res)."""
+    """Expected launch sequence of one forward: (kind, name, h, cin, cout, taps, outs, res[,
+    rd]) -- rd, when given, is the input channels read per output pixel (a source read
+    2x upsampled inside the TMA load counts a quarter of its channels)."""
     prog = build_program(cfg)
     ch = cfg.channels()
     fused = unet.FUSED_STEM
@@ -44,6 +46,7 @@ def layer_ops(cfg, win):
     h = win
     c = ch[0]
     pooled = False
+    up = False        # the next decoder block reads its low-res inputs upsampled in the TMA load
     for k, op in enumerate(prog.ops):
         nxt = prog.ops[k + 1][0] if k + 1 < len(prog.ops) else None
         c2_outs = 1 if nxt in ("attn", "out") else 2     # unet.forward_after_stem
@@ -80,14 +83,20 @@ def layer_ops(cfg, win):
         elif op[0] == "dec":
             nm = op[1]
             c1 = prog.convs[nm + ".c1"]
-            seq.append(("conv", nm + ".c1", h, c1.cin, c1.cout, 9, 1, 0))
+            sk = c1.cin - c                                  # skip-connection channels
+            rd1 = (c / 4 if up else c) + sk                  # x (maybe low-res) + skip
+            seq.append(("conv", nm + ".c1", h, c1.cin, c1.cout, 9, 1, 0, rd1))
             c2 = prog.convs[nm + ".c2"]
-            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, c2_outs, c1.cin / c2.cout))
+            seq.append(("conv", nm + ".c2", h, c2.cin, c2.cout, 9, c2_outs, c1.cin / c2.cout,
+                        c2.cin + rd1))
             c = c2.cout
+            up = False
         elif op[0] == "up":
             if not (unet.FUSED_UP and (2 * h) % 128 == 0):   # else folded into the TMA loads
                 seq.append(("up", "up.x", h, c, 0, 0, 0, 0))
                 seq.append(("up", "up.xa", h, c, 0, 0, 0, 0))
+            else:
+                up = True
             h *= 2
         elif op[0] == "out":
             if unet.FUSED_OUT and h % 4 == 0 and h % 128 == 0:
@@ -110,13 +119,13 @@ def main():
     last = L[-len(seq):]
     tot_t = tot_b = 0.0
     print(f"{'layer':14s} {'kernel':28s} {'us':>8s} {'TF/s':>7s} {'GB/s':>7s} {'bound_us':>8s} {'eff':>5s}")
-    for (kind, name, h, cin, cout, taps, outs, res), (kname, us) in zip(seq, last):
+    for (kind, name, h, cin, cout, taps, outs, res, *rd), (kname, us) in zip(seq, last):
         px = n * h * h
         fl = 2.0 * px * cin * cout * taps if kind == "conv" else 0.0
         if kind == "attn":             # q k^T + p v per window: 4 N^2 C
             fl = 4.0 * n * (h * h) ** 2 * cin
         if kind == "conv":
-            by = px * 2 * (cin + cout * (outs + res))
+            by = px * 2 * ((rd[0] if rd else cin + cout * res) + cout * outs)
         elif kind in ("attn", "attn_prep"):
             by = px * 2 * cin * 4
         elif kind == "up":
