@@ -248,11 +248,14 @@ def test_unet_batch_invariance():
     assert torch.equal(full[2], one[0])
 
 
-@pytest.mark.parametrize("win,outer_step", [(64, 2), (64, 1), (256, 1)])
-def test_fused_stem_matches_unfused(win, outer_step):
+@pytest.mark.parametrize("win,outer_step,data_channels", [(64, 2, 1), (64, 1, 1), (256, 1, 1),
+                                                          (64, 2, 2), (64, 1, 3), (64, 1, 6)])
+def test_fused_stem_matches_unfused(win, outer_step, data_channels):
     """ig_unet_stem (gather + tap-packed stem GEMM in one kernel) == gather
-    kernel + stem conv: same x_noisy bits, x / mp_silu(x) to bf16 rounding."""
-    cfg = SMALL
+    kernel + stem conv: same x_noisy bits, x / mp_silu(x) to bf16 rounding;
+    2, 4 and 8 SMEM plane slots per position (P = C + 1 = 2, 3, 4, 7)."""
+    import dataclasses
+    cfg = dataclasses.replace(SMALL, data_channels=data_channels)
     wins, xs = _phi_inputs(cfg, 3, win, seed=2)
     wxy = torch.tensor([[b.x0, b.y0] for b in wins], dtype=torch.int64, device=DEV)
     src = torch.from_numpy(xs).to(DEV)
