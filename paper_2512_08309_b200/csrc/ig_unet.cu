@@ -2835,13 +2835,14 @@ __global__ void __launch_bounds__(256) unet_out_head_kernel(
 // tap.  The partials go to SMEM (f32, [input row][px][tap]) and each output
 // sums its 9 taps -- SMEM traffic per pixel ~0.3 KB instead of the 9x
 // ldmatrix re-reads (1.15 KB) of unet_out_head_kernel.
-template <int C>
-__global__ void __launch_bounds__(256) unet_out_head_tn_kernel(
+template <int C, int THREADS = 256>
+__global__ void __launch_bounds__(THREADS) unet_out_head_tn_kernel(
     const __grid_constant__ CUtensorMap map_xa, const __nv_bfloat16* __restrict__ wout,
     int n, int h, int w, const float* __restrict__ x_noisy, float c_skip, float c_out,
     float* __restrict__ out) {
   constexpr int S = 4;                                  // output rows per tile
   constexpr int IR = S + 2;                             // input rows per tile
+  constexpr int NW = THREADS / 32;                      // warps
   constexpr int NT = (9 * C + 7) / 8;                   // n8 tiles of taps
   constexpr int TP = 9 * C;                             // partials per input pixel
   constexpr int PX = 130;                               // input pixels per row (9 blocks of 16)
@@ -2903,11 +2904,11 @@ __global__ void __launch_bounds__(256) unet_out_head_tn_kernel(
     tile_xy(tile, img, y0, x0);
     // x_noisy of this thread's phase-2 outputs, loaded before the MMA phase so its
     // HBM latency is hidden (ncu: 33% of the stall samples sat on this load)
-    constexpr int NQ = (S * 128 * C + 255) / 256;
+    constexpr int NQ = (S * 128 * C + THREADS - 1) / THREADS;
     float xn[NQ];
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
-      const int q = threadIdx.x + k * 256;
+      const int q = threadIdx.x + k * THREADS;
       xn[k] = 0.f;
       if (q < S * 128 * C) {
         const int c = q / (S * 128), rem = q - c * S * 128;
@@ -2917,7 +2918,7 @@ __global__ void __launch_bounds__(256) unet_out_head_tn_kernel(
     }
     mbar_wait(&bar[sb], (uint32_t)((it >> 1) & 1));
     // 1. partials: IR rows x 9 blocks of 16 input pixels, spread over the 8 warps
-    for (int blk = warp; blk < IR * 9; blk += 8) {
+    for (int blk = warp; blk < IR * 9; blk += NW) {
       const int r = blk / 9, px0 = (blk - r * 9) * 16;
       float acc[NT][4];
 #pragma unroll
@@ -2955,7 +2956,7 @@ __global__ void __launch_bounds__(256) unet_out_head_tn_kernel(
     // 2. each output sums its 9 taps: output (i, x) <- input (i+dy, x+dx) (halo coords)
 #pragma unroll
     for (int k = 0; k < NQ; ++k) {
-      const int q = threadIdx.x + k * 256;
+      const int q = threadIdx.x + k * THREADS;
       if (q >= S * 128 * C) break;
       const int c = q / (S * 128), rem = q - c * S * 128;
       const int i = rem / 128, x = rem - i * 128;
@@ -4896,9 +4897,14 @@ int ig_unet_out_head(const void* xa, int32_t n, int32_t h, int32_t w, int32_t ci
     const int smem = 2 * OutCfg<4>::STRIDE + 6 * 130 * 9 * 4 + 1024 + 64;
     const int64_t tiles = (int64_t)n * (w / 128) * (h / 4);
     const int ctas = (int)(tiles < kNumSMs ? tiles : kNumSMs);
-    auto kern = unet_out_head_tn_kernel<1>;
+    // 16 warps (variant 22: 8): the partial-sum phase is a chain of ldmatrix ->
+    // HMMA dependencies, and 8 warps per SM left it latency-bound (ncu r02:
+    // 12.5% warps active, top stalls wait / short scoreboard): 109 -> 100.5 us
+    // per 64 windows; 32 warps measured 113 us (54 pixel blocks over 32 warps)
+    const int thr = g_variant == 22 ? 256 : 512;
+    auto kern = thr == 256 ? unet_out_head_tn_kernel<1, 256> : unet_out_head_tn_kernel<1, 512>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    { kern<<<ctas, 256, smem, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
+    { kern<<<ctas, thr, smem, reinterpret_cast<cudaStream_t>(cuda_stream)>>>(
         m, reinterpret_cast<const __nv_bfloat16*>(w_out), n, h, w, x_noisy, c_skip, c_out,
         out); note_launch(); }
     return cuda_check("ig_unet_out_head");
